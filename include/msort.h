@@ -1,0 +1,215 @@
+/*
+ * msort.h -- C ABI of the B200-native (sm_100a) stable merge sort.
+ *
+ * The operation (arXiv 2211.16479, /root/reference/PAPER.md; "P:n" = line n):
+ * sort an array of integer keys ascending, as merge sort does
+ * (P:77-84 [Sequential Merge Sort, steps 1-4], Fig. fig:mergesort P:88-112),
+ * stably (equal keys keep their input order -- the tie rule of merge(),
+ * P:107, read as "left run first", R1), optionally carrying a
+ * payload; and the distributed variant in which each process sorts its shard
+ * and the shards are merged across processes (P:398-525 [MPI Merge Sort],
+ * Figs. fig:mpi-scatter-code, fig:mpi-merge-code), here as a balanced,
+ * globally sorted layout across ranks (R10).
+ *
+ * Result contract: element i of the input lands at position
+ *     pos(i) = #{j : k_j < k_i} + #{j < i : k_j = k_i},
+ * which is unique, so results are bit-exact to the CPU oracle (oracle/).
+ *
+ * Conventions for every call:
+ *  - keys/vals/ws are DEVICE pointers on the current CUDA device; the caller
+ *    owns them, the library never frees them.  Host pointers are only the
+ *    explicitly marked `host` arguments.
+ *  - Sorting is in place: the sorted output overwrites keys (and vals).
+ *  - Layout: structure of arrays, keys[n] and vals[n], contiguous; pointers
+ *    must be aligned to their element size (16-byte alignment is NOT needed).
+ *  - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default
+ *    stream) and never synchronise, except msort_sort_distributed*, which
+ *    synchronises `stream` once to read the split matrix (documented there).
+ *    Execution faults surface at the caller's next synchronisation.
+ *  - Errors are returned synchronously as msort_status; nothing throws across
+ *    the ABI.  msort_last_error() returns thread-local detail text.
+ *  - n == 0 or n == 1 is a successful no-op without any launch ("if the input
+ *    array has less than two elements, return").
+ *  - INVALID_VALUE: NULL pointer with n > 0, misaligned pointer, keys/vals
+ *    overlapping, unknown dtype, n > 2^40, workspace too small.
+ *    NOT_SUPPORTED: device is not sm_100 or the dtype combination is not built
+ *    (payloads: MSORT_UINT32 / MSORT_INT32 only, i.e. 4-byte payloads).
+ *  - Thread safety: calls are re-entrant; one msort_comm_t must not be used by
+ *    two calls at once (an NCCL rule).
+ *
+ * There is no CPU fallback: every step runs in the library's sm_100a kernels.
+ */
+#ifndef MSORT_H
+#define MSORT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MSORT_INT32 = 0,
+  MSORT_UINT32 = 1,
+  MSORT_INT64 = 2,
+  MSORT_UINT64 = 3,
+  MSORT_NONE = 255 /* "no payload" for val_dtype */
+} msort_dtype;
+
+typedef enum {
+  MSORT_SUCCESS = 0,
+  MSORT_ERROR_INVALID_VALUE = 1,
+  MSORT_ERROR_NOT_SUPPORTED = 2,
+  MSORT_ERROR_OUT_OF_MEMORY = 3,
+  MSORT_ERROR_CUDA = 4,
+  MSORT_ERROR_NCCL = 5
+} msort_status;
+
+/* A cudaStream_t, passed as an opaque pointer so this header needs no CUDA. */
+typedef void *msort_stream_t;
+
+/* Opaque communicator (owns one NCCL communicator).  Caller-owned. */
+typedef struct msort_comm_s *msort_comm_t;
+
+/* ---------------------------------------------------------------- single GPU */
+
+/* Stable ascending sort of keys[0..n) in place.  Workspace of
+ * msort_workspace_bytes(n, key_dtype, MSORT_NONE, 1) bytes is taken with
+ * cudaMallocAsync/cudaFreeAsync on `stream`. */
+msort_status msort_sort(void *keys, size_t n, msort_dtype key_dtype, msort_stream_t stream);
+
+/* Stable ascending sort of (keys, vals) pairs by key; vals travel with their
+ * keys and equal keys keep input order (P:107 tie rule, R1).
+ * val_dtype must be a 4-byte type (MSORT_UINT32 or MSORT_INT32). */
+msort_status msort_sort_pairs(void *keys, void *vals, size_t n, msort_dtype key_dtype,
+                              msort_dtype val_dtype, msort_stream_t stream);
+
+/* Bytes of device workspace the *_ws calls need: for world <= 1 about
+ * n*(wk+wv) (the O(n) extra space of merge sort) plus n/256*8 bytes of
+ * merge-path partitions; for world > 1 (n = local count) also an n*(wk+wv)
+ * receive buffer and O(world*256) splitter buffers.  bytes: host out. */
+msort_status msort_workspace_bytes(size_t n, msort_dtype key_dtype, msort_dtype val_dtype,
+                                   int world, size_t *bytes);
+
+/* msort_sort / msort_sort_pairs with caller-supplied device workspace
+ * (e.g. from the PyTorch caching allocator).  vals may be NULL with
+ * val_dtype == MSORT_NONE.  ws must be 256-byte aligned and at least
+ * msort_workspace_bytes(n, key_dtype, val_dtype, 1) bytes; it must not overlap
+ * keys/vals.  Nothing is allocated. */
+msort_status msort_sort_ws(void *keys, void *vals, size_t n, msort_dtype key_dtype,
+                           msort_dtype val_dtype, void *ws, size_t ws_bytes,
+                           msort_stream_t stream);
+
+/* --------------------------------------------------------------- multi GPU */
+
+/* Fill `id_out` (host, 128 bytes) with a fresh NCCL unique id.  Rank 0 calls
+ * it and broadcasts the bytes over its own process group. */
+msort_status msort_comm_unique_id(void *id_out);
+
+/* Create a communicator for `rank` of `world` from the 128-byte id (host).
+ * Collective over all ranks; uses the current CUDA device. */
+msort_status msort_comm_init(const void *id, int rank, int world, msort_comm_t *out);
+
+msort_status msort_comm_destroy(msort_comm_t comm);
+
+/* Distributed stable sort (re-designed: local sort, exact
+ * splitters by co-rank, one variable all-to-all over NVLink, local k-way
+ * merge).  Collective: every rank calls it with the same dtypes; n_local may
+ * differ per rank and may be 0.  On return rank r's keys[0..n_local) hold the
+ * global stable positions [K_r, K_r + n_local) of the rank-major
+ * concatenation of all inputs, K_r = sum_{j<r} n_j (R10/R11).
+ * vals: NULL (val_dtype MSORT_NONE) or 4-byte payloads.
+ * split_matrix_out: NULL or host (world+1)*world int64: entry (r, j) = number
+ * of rank j's elements among the first K_r outputs.
+ * Synchronises `stream` once (the exchange sizes are needed on the host). */
+msort_status msort_sort_distributed(void *keys, void *vals, size_t n_local,
+                                    msort_dtype key_dtype, msort_dtype val_dtype,
+                                    msort_comm_t comm, msort_stream_t stream,
+                                    int64_t *split_matrix_out);
+
+/* As msort_sort_distributed with caller workspace of
+ * msort_workspace_bytes(n_local, key_dtype, val_dtype, world) bytes. */
+msort_status msort_sort_distributed_ws(void *keys, void *vals, size_t n_local,
+                                       msort_dtype key_dtype, msort_dtype val_dtype,
+                                       msort_comm_t comm, void *ws, size_t ws_bytes,
+                                       msort_stream_t stream, int64_t *split_matrix_out);
+
+/* Single-process emulation of the distributed sort for `world` virtual ranks
+ * whose shards all live on the current device: the same kernels, the same
+ * splitter planning and the same k-way merge, with the NCCL collectives
+ * replaced by device-side reductions and device-to-device copies.  Used to
+ * check the multi-rank path on one GPU.  keys[r], vals[r] (host arrays of
+ * device pointers; vals NULL for keys only), n_local[r] (host), ws[r] (host
+ * array of device workspaces sized as for msort_sort_distributed_ws).
+ * split_matrix_out as above (host, may be NULL).  Synchronises once. */
+msort_status msort_sort_distributed_emulated(void *const *keys, void *const *vals,
+                                             const size_t *n_local, int world,
+                                             msort_dtype key_dtype, msort_dtype val_dtype,
+                                             void *const *ws, size_t ws_bytes,
+                                             msort_stream_t stream,
+                                             int64_t *split_matrix_out);
+
+/* --------------------------------------------- splitter planning (host side)
+ * The host-side arithmetic of the splitter co-rank, the same
+ * functions the device kernels run.  Exported so the multi-process protocol
+ * can be tested on CPU over gloo.  All arrays are host arrays.
+ *
+ * Keys are compared through their order-preserving unsigned image
+ * (int32: x ^ 2^31, int64: x ^ 2^63, unsigned: x).  For each boundary
+ * r = 1..world-1 the search keeps an inclusive interval [lo_r, hi_r] of images
+ * holding v*_r, the image of the key at global position K_r. */
+
+/* Number of search rounds for a key dtype (8 bits per round: 4 or 8). */
+int msort_plan_rounds(msort_dtype key_dtype);
+
+/* Candidates per boundary per round (256). */
+int msort_plan_candidates_per_round(void);
+
+/* lohi[2*(world-1)] := {0, max image} for every boundary. */
+msort_status msort_plan_init(msort_dtype key_dtype, int world, uint64_t *lohi);
+
+/* cand[(world-1)*B] := the B bucket upper ends of each boundary's interval. */
+msort_status msort_plan_candidates(int world, const uint64_t *lohi, uint64_t *cand);
+
+/* Given total[(world-1)*B] = sum over ranks of #{keys with image <= cand},
+ * narrow each interval to the first bucket whose total exceeds K_r
+ * (the last bucket if none).  K[world+1] = prefix sums of the shard sizes. */
+msort_status msort_plan_narrow(int world, const uint64_t *K, const uint64_t *total,
+                               uint64_t *lohi);
+
+/* Split matrix from the gathered counts: lteq[j*(world-1)*2 + (r-1)*2 + {0,1}]
+ * = (#keys < v*_r, #keys == v*_r) on rank j.  out[(world+1)*world]:
+ *   s[r][j] = lt_j + clamp(K_r - sum_j' lt_j' - sum_{j'<j} eq_j', 0, eq_j),
+ *   s[0][.] = 0, s[world][j] = n_j. */
+msort_status msort_plan_fill(int world, const uint64_t *K, const uint64_t *lteq,
+                             int64_t *out);
+
+/* ------------------------------------------------------- status and timing */
+
+const char *msort_status_string(msort_status s);
+const char *msort_last_error(void);
+
+/* Kernel accounting.  The library counts every kernel it launches; when
+ * profiling is enabled it also brackets each launch with CUDA events on the
+ * launching stream.  msort_profile_read synchronises those events and
+ * returns, per kernel class (0 tile_sort, 1 partition, 2 merge_pass,
+ * 3 splitter, 4 kway_merge, 5 NCCL collectives / exchange), the launch count
+ * and total device milliseconds since the last reset.  Host arrays of
+ * MSORT_PROFILE_CLASSES. */
+#define MSORT_PROFILE_CLASSES 6
+void msort_profile_enable(int on);
+void msort_profile_reset(void);
+msort_status msort_profile_read(int64_t *launches, double *ms);
+
+/* Total launches of the library's OWN kernels (class 5, NCCL, excluded)
+ * since process start / the last msort_profile_reset. */
+int64_t msort_launch_count(void);
+
+/* Tile size (elements) used for key dtype with/without payload. */
+int msort_tile_size(msort_dtype key_dtype, msort_dtype val_dtype);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSORT_H */

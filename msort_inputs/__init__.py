@@ -93,6 +93,48 @@ def keys(n: int, seed: int, dist="u31", out: np.ndarray | None = None) -> np.nda
     return out
 
 
+def _i64(c: int) -> int:
+    """A 64-bit constant as the signed int64 with the same bits."""
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+def _srl(z, s: int):
+    """Logical right shift of int64 torch tensors (bit pattern of uint64)."""
+    return (z >> s) & ((1 << (64 - s)) - 1)
+
+
+def keys_torch(n: int, seed: int, dist="u31", device="cuda", start: int = 0):
+    """The same counter-mode SplitMix64 keys as `keys`, drawn with torch int64
+    ops (wrap-around multiply, masked shifts) on any device -- bit-identical to
+    the numpy version (tests/test_oracle.py::test_torch_generator_matches).
+    Used to build large inputs on the GPU quickly; pure plumbing."""
+    import torch
+
+    idx = torch.arange(start + 1, start + n + 1, dtype=torch.int64, device=device)
+    z = idx * _i64(int(GOLDEN_GAMMA)) + _i64(seed & 0xFFFFFFFFFFFFFFFF)
+    z = (z ^ _srl(z, 30)) * _i64(int(_M1))
+    z = (z ^ _srl(z, 27)) * _i64(int(_M2))
+    z = z ^ _srl(z, 31)
+    del idx
+    if dist == "u31":
+        return _srl(z, 33).to(torch.int32)
+    if dist in ("u32", "i32"):
+        hi = _srl(z, 32)
+        hi = torch.where(hi >= (1 << 31), hi - (1 << 32), hi).to(torch.int32)
+        return hi.view(torch.uint32) if dist == "u32" else hi
+    if dist == "i64":
+        return z
+    if dist == "u64":
+        return z.view(torch.uint64)
+    if isinstance(dist, tuple) and dist[0] == "mod":
+        m = int(dist[1])
+        assert 0 < m < (1 << 31)
+        hi = _srl(z, 32)
+        lo = z & 0xFFFFFFFF
+        return _srl(hi * m + _srl(lo * m, 32), 32)
+    raise ValueError(f"unknown dist {dist!r}")
+
+
 def index_payload(n: int) -> np.ndarray:
     """Original-index payload v_i = i (uint32), used to observe stability."""
     assert n <= (1 << 32)

@@ -1,0 +1,330 @@
+"""Thin Python binding of libmsort.so (include/msort.h): argument marshalling only.
+
+Every step of the sort runs in the library's sm_100a CUDA kernels; PyTorch
+supplies device memory (workspace from its caching allocator), the current
+stream and process groups.  There is no CPU fallback: if the library is not
+built, importing this package raises.
+
+Names follow the C ABI (msort_sort, msort_sort_pairs, msort_sort_distributed,
+...).  `sort`, `sort_pairs` are functional conveniences that work on a clone
+(the paper's sorts are pure functions).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libmsort.so")
+
+MSORT_INT32, MSORT_UINT32, MSORT_INT64, MSORT_UINT64, MSORT_NONE = 0, 1, 2, 3, 255
+MSORT_PROFILE_CLASSES = 6
+PROFILE_CLASS_NAMES = ("tile_sort", "partition", "merge_pass", "splitter", "kway_merge", "nccl")
+
+_TORCH_DT = {torch.int32: MSORT_INT32, torch.int64: MSORT_INT64}
+if hasattr(torch, "uint32"):
+    _TORCH_DT[torch.uint32] = MSORT_UINT32
+if hasattr(torch, "uint64"):
+    _TORCH_DT[torch.uint64] = MSORT_UINT64
+_NP_DT = {np.dtype(np.int32): MSORT_INT32, np.dtype(np.uint32): MSORT_UINT32,
+          np.dtype(np.int64): MSORT_INT64, np.dtype(np.uint64): MSORT_UINT64}
+
+EXPORTED = (
+    "msort_sort", "msort_sort_pairs", "msort_workspace_bytes", "msort_sort_ws",
+    "msort_comm_unique_id", "msort_comm_init", "msort_comm_destroy", "msort_sort_distributed",
+    "msort_sort_distributed_ws", "msort_sort_distributed_emulated", "msort_plan_rounds",
+    "msort_plan_candidates_per_round", "msort_plan_init", "msort_plan_candidates",
+    "msort_plan_narrow", "msort_plan_fill", "msort_status_string", "msort_last_error",
+    "msort_profile_enable", "msort_profile_reset", "msort_profile_read", "msort_launch_count",
+    "msort_tile_size",
+)
+
+
+class MsortError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2211_16479_b200.build` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    c = ctypes
+    vp, sz, i32, i64p = c.c_void_p, c.c_size_t, c.c_int, c.POINTER(c.c_int64)
+    u64p = c.POINTER(c.c_uint64)
+    L.msort_sort.argtypes = [vp, sz, i32, vp]
+    L.msort_sort_pairs.argtypes = [vp, vp, sz, i32, i32, vp]
+    L.msort_workspace_bytes.argtypes = [sz, i32, i32, i32, c.POINTER(c.c_size_t)]
+    L.msort_sort_ws.argtypes = [vp, vp, sz, i32, i32, vp, sz, vp]
+    L.msort_comm_unique_id.argtypes = [vp]
+    L.msort_comm_init.argtypes = [vp, i32, i32, c.POINTER(vp)]
+    L.msort_comm_destroy.argtypes = [vp]
+    L.msort_sort_distributed.argtypes = [vp, vp, sz, i32, i32, vp, vp, i64p]
+    L.msort_sort_distributed_ws.argtypes = [vp, vp, sz, i32, i32, vp, vp, sz, vp, i64p]
+    L.msort_sort_distributed_emulated.argtypes = [c.POINTER(vp), c.POINTER(vp),
+                                                  c.POINTER(c.c_size_t), i32, i32, i32,
+                                                  c.POINTER(vp), sz, vp, i64p]
+    L.msort_plan_rounds.argtypes = [i32]
+    L.msort_plan_rounds.restype = i32
+    L.msort_plan_candidates_per_round.restype = i32
+    L.msort_plan_init.argtypes = [i32, i32, u64p]
+    L.msort_plan_candidates.argtypes = [i32, u64p, u64p]
+    L.msort_plan_narrow.argtypes = [i32, u64p, u64p, u64p]
+    L.msort_plan_fill.argtypes = [i32, u64p, u64p, i64p]
+    L.msort_status_string.argtypes = [i32]
+    L.msort_status_string.restype = c.c_char_p
+    L.msort_last_error.restype = c.c_char_p
+    L.msort_profile_enable.argtypes = [i32]
+    L.msort_profile_read.argtypes = [i64p, c.POINTER(c.c_double)]
+    L.msort_launch_count.restype = c.c_int64
+    L.msort_tile_size.argtypes = [i32, i32]
+    L.msort_tile_size.restype = i32
+    for f in ("msort_sort", "msort_sort_pairs", "msort_workspace_bytes", "msort_sort_ws",
+              "msort_comm_unique_id", "msort_comm_init", "msort_comm_destroy",
+              "msort_sort_distributed", "msort_sort_distributed_ws",
+              "msort_sort_distributed_emulated", "msort_plan_init", "msort_plan_candidates",
+              "msort_plan_narrow", "msort_plan_fill", "msort_profile_read"):
+        getattr(L, f).restype = i32
+    return L
+
+
+lib = _load()
+
+
+def _check(st: int, what: str):
+    if st != 0:
+        name = lib.msort_status_string(st).decode()
+        detail = lib.msort_last_error().decode()
+        raise MsortError(f"{what}: {name}: {detail}")
+
+
+def _dt(t: torch.Tensor) -> int:
+    try:
+        return _TORCH_DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported key dtype {t.dtype}") from None
+
+
+def _vdt(v: torch.Tensor | None) -> int:
+    if v is None:
+        return MSORT_NONE
+    if v.dtype == torch.int32:
+        return MSORT_INT32
+    if hasattr(torch, "uint32") and v.dtype == torch.uint32:
+        return MSORT_UINT32
+    raise TypeError(f"payload must be a 4-byte integer tensor, got {v.dtype}")
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _check_tensor(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous() or t.dim() != 1:
+        raise ValueError(f"{name} must be a contiguous 1-D tensor")
+
+
+def msort_workspace_bytes(n: int, key_dtype: int, val_dtype: int = MSORT_NONE,
+                          world: int = 1) -> int:
+    out = ctypes.c_size_t()
+    _check(lib.msort_workspace_bytes(n, key_dtype, val_dtype, world, ctypes.byref(out)),
+           "msort_workspace_bytes")
+    return out.value
+
+
+def workspace(n: int, keys_dtype: torch.dtype, with_vals: bool, world: int = 1,
+              device=None) -> torch.Tensor:
+    """A workspace tensor from PyTorch's caching allocator."""
+    nb = msort_workspace_bytes(n, _TORCH_DT[keys_dtype], MSORT_UINT32 if with_vals else MSORT_NONE,
+                               world)
+    return torch.empty(max(nb, 1), dtype=torch.uint8, device=device)
+
+
+def msort_sort(keys: torch.Tensor, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Stable ascending sort of a 1-D CUDA tensor in place."""
+    return msort_sort_pairs(keys, None, ws=ws, stream=stream)[0]
+
+
+def msort_sort_pairs(keys: torch.Tensor, vals: torch.Tensor | None, ws: torch.Tensor | None = None,
+                     stream=None):
+    """Stable sort of (keys, vals) by key, in place; ties keep input order."""
+    _check_tensor(keys, "keys")
+    if vals is not None:
+        _check_tensor(vals, "vals")
+        if vals.numel() != keys.numel() or vals.device != keys.device:
+            raise ValueError("keys/vals size or device mismatch")
+    n = keys.numel()
+    kd, vd = _dt(keys), _vdt(vals)
+    if n < 2:
+        return keys, vals
+    if ws is None:
+        ws = workspace(n, keys.dtype, vals is not None, device=keys.device)
+    with torch.cuda.device(keys.device):
+        _check(lib.msort_sort_ws(_ptr(keys), _ptr(vals), n, kd, vd, _ptr(ws), ws.numel(),
+                                 ctypes.c_void_p(_stream(stream))), "msort_sort_ws")
+    return keys, vals
+
+
+def sort(x: torch.Tensor) -> torch.Tensor:
+    """Functional stable sort: returns a sorted copy."""
+    return msort_sort(x.clone())
+
+
+def sort_pairs(k: torch.Tensor, v: torch.Tensor):
+    return msort_sort_pairs(k.clone(), v.clone())
+
+
+# ------------------------------------------------------------- distributed
+class Comm:
+    """An NCCL communicator of libmsort built over a torch process group
+    (the unique id is broadcast over the group)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        idb = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _check(lib.msort_comm_unique_id(idb), "msort_comm_unique_id")
+        obj = [bytes(idb.raw) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        idb = ctypes.create_string_buffer(obj[0], 128)
+        h = ctypes.c_void_p()
+        _check(lib.msort_comm_init(idb, self.rank, self.world, ctypes.byref(h)), "msort_comm_init")
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            _check(lib.msort_comm_destroy(self.handle), "msort_comm_destroy")
+            self.handle = None
+
+
+def msort_sort_distributed(keys: torch.Tensor, comm: Comm, vals: torch.Tensor | None = None,
+                           ws: torch.Tensor | None = None, stream=None,
+                           return_split: bool = False):
+    """Collective stable sort: rank r ends with global positions [K_r, K_r+n_r)."""
+    _check_tensor(keys, "keys")
+    if vals is not None:
+        _check_tensor(vals, "vals")
+    n = keys.numel()
+    kd, vd = _dt(keys), _vdt(vals)
+    if ws is None:
+        ws = workspace(n, keys.dtype, vals is not None, world=comm.world, device=keys.device)
+    split = np.zeros((comm.world + 1) * comm.world, dtype=np.int64)
+    with torch.cuda.device(keys.device):
+        _check(lib.msort_sort_distributed_ws(
+            _ptr(keys), _ptr(vals), n, kd, vd, comm.handle, _ptr(ws), ws.numel(),
+            ctypes.c_void_p(_stream(stream)),
+            split.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "msort_sort_distributed_ws")
+    split = split.reshape(comm.world + 1, comm.world)
+    return (keys, vals, split) if return_split else (keys, vals)
+
+
+def msort_sort_distributed_emulated(keys: list, vals: list | None = None, stream=None):
+    """p virtual ranks on one GPU (same kernels/planning; collectives emulated
+    on the device).  Sorts every shard tensor in place; returns the split matrix."""
+    p = len(keys)
+    for k in keys:
+        _check_tensor(k, "keys")
+    kd = _dt(keys[0])
+    vd = _vdt(vals[0]) if vals else MSORT_NONE
+    nmax = max(k.numel() for k in keys)
+    wsb = msort_workspace_bytes(nmax, kd, vd, p)
+    wss = [torch.empty(wsb, dtype=torch.uint8, device=keys[0].device) for _ in range(p)]
+    VP = ctypes.c_void_p * p
+    kp = VP(*[k.data_ptr() for k in keys])
+    vp = VP(*[v.data_ptr() for v in vals]) if vals else None
+    np_ = (ctypes.c_size_t * p)(*[k.numel() for k in keys])
+    wp = VP(*[w.data_ptr() for w in wss])
+    split = np.zeros((p + 1) * p, dtype=np.int64)
+    with torch.cuda.device(keys[0].device):
+        _check(lib.msort_sort_distributed_emulated(
+            kp, vp, np_, p, kd, vd, wp, wsb, ctypes.c_void_p(_stream(stream)),
+            split.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+            "msort_sort_distributed_emulated")
+    return split.reshape(p + 1, p)
+
+
+# --------------------------------------------------- planning (host side)
+def _u64p(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+
+
+def plan_rounds(key_dtype: int) -> int:
+    return lib.msort_plan_rounds(key_dtype)
+
+
+def plan_candidates_per_round() -> int:
+    return lib.msort_plan_candidates_per_round()
+
+
+def plan_init(key_dtype: int, world: int) -> np.ndarray:
+    lohi = np.zeros(2 * max(world - 1, 0) + 1, dtype=np.uint64)
+    _check(lib.msort_plan_init(key_dtype, world, _u64p(lohi)), "msort_plan_init")
+    return lohi[: 2 * (world - 1)]
+
+
+def plan_candidates(world: int, lohi: np.ndarray) -> np.ndarray:
+    B = plan_candidates_per_round()
+    lohi = np.ascontiguousarray(lohi, dtype=np.uint64)
+    cand = np.zeros(max(world - 1, 0) * B + 1, dtype=np.uint64)
+    _check(lib.msort_plan_candidates(world, _u64p(lohi), _u64p(cand)), "msort_plan_candidates")
+    return cand[: (world - 1) * B].reshape(world - 1, B)
+
+
+def plan_narrow(world: int, K: np.ndarray, total: np.ndarray, lohi: np.ndarray) -> np.ndarray:
+    K = np.ascontiguousarray(K, dtype=np.uint64)
+    total = np.ascontiguousarray(total, dtype=np.uint64).ravel()
+    lohi = np.ascontiguousarray(lohi, dtype=np.uint64).copy()
+    _check(lib.msort_plan_narrow(world, _u64p(K), _u64p(total), _u64p(lohi)), "msort_plan_narrow")
+    return lohi
+
+
+def plan_fill(world: int, K: np.ndarray, lteq: np.ndarray) -> np.ndarray:
+    K = np.ascontiguousarray(K, dtype=np.uint64)
+    lteq = np.ascontiguousarray(lteq, dtype=np.uint64).ravel()
+    if lteq.size == 0:
+        lteq = np.zeros(1, dtype=np.uint64)
+    out = np.zeros((world + 1) * world, dtype=np.int64)
+    _check(lib.msort_plan_fill(world, _u64p(K), _u64p(lteq),
+                               out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+           "msort_plan_fill")
+    return out.reshape(world + 1, world)
+
+
+# --------------------------------------------------------------- profiling
+def profile_enable(on: bool = True):
+    lib.msort_profile_enable(1 if on else 0)
+
+
+def profile_reset():
+    lib.msort_profile_reset()
+
+
+def profile_read():
+    la = (ctypes.c_int64 * MSORT_PROFILE_CLASSES)()
+    ms = (ctypes.c_double * MSORT_PROFILE_CLASSES)()
+    _check(lib.msort_profile_read(la, ms), "msort_profile_read")
+    return {PROFILE_CLASS_NAMES[i]: (int(la[i]), float(ms[i])) for i in range(MSORT_PROFILE_CLASSES)}
+
+
+def launch_count() -> int:
+    return int(lib.msort_launch_count())
+
+
+def tile_size(key_dtype: int, val_dtype: int = MSORT_NONE) -> int:
+    return int(lib.msort_tile_size(key_dtype, val_dtype))

@@ -1,0 +1,77 @@
+// msort_internal.h -- host-side plumbing shared by the library's translation
+// units (error text, kernel accounting, workspace carving, tile geometry).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/msort.h"
+
+namespace msort {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& s);
+msort_status cuda_fail(cudaError_t e, const char* what);
+#define MSORT_CUDA_TRY(expr)                                            \
+  do {                                                                  \
+    cudaError_t _e = (expr);                                            \
+    if (_e != cudaSuccess) return ::msort::cuda_fail(_e, #expr);        \
+  } while (0)
+#define MSORT_TRY(expr)                                                 \
+  do {                                                                  \
+    msort_status _s = (expr);                                           \
+    if (_s != MSORT_SUCCESS) return _s;                                 \
+  } while (0)
+
+// ------------------------------------------------------ kernel accounting
+enum KernelClass { KC_TILE_SORT = 0, KC_PARTITION = 1, KC_MERGE = 2, KC_SPLITTER = 3,
+                   KC_KWAY = 4, KC_NCCL = 5 };
+
+// Bracket a kernel launch: counts it, and when profiling is on records a
+// pair of CUDA events on the launching stream.
+struct LaunchScope {
+  LaunchScope(KernelClass kc, cudaStream_t s);
+  ~LaunchScope();
+  KernelClass kc;
+  cudaStream_t s;
+  int slot;
+};
+
+// ------------------------------------------------------- tile geometry
+// Tile sort (K1): NT threads x VT items; merge passes (K3) use the same tile
+// so every pair boundary (a multiple of 2T) is a tile boundary.
+constexpr int kNT = 256;
+template <class K, bool PAIRS>
+struct Geometry {
+  static constexpr int NT = kNT;
+  static constexpr int VT = sizeof(K) == 4 ? 16 : 16;
+  static constexpr int T = NT * VT;
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+size_t dtype_size(msort_dtype d);
+int tile_size_for(msort_dtype kd, msort_dtype vd);
+
+// Single-GPU workspace: [keys n*wk][vals n*4][partition (ntiles+1)*8].
+size_t single_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd);
+
+// Distributed extras: receive buffers + splitter scratch.
+constexpr int kCandidates = 256;  // candidates per boundary per round (8 bits)
+size_t dist_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd, int world);
+
+// Single-GPU sort with explicit workspace (sort_single.cu).
+msort_status sort_single_dispatch(void* keys, void* vals, size_t n, msort_dtype kd,
+                                  msort_dtype vd, void* ws, size_t ws_bytes, cudaStream_t s);
+
+// Stable merge of `runs` consecutive sorted runs (run r = [off[r], off[r+1]) of
+// src) into dst, ties to the lower run; used by the distributed k-way merge.
+// Ping-pongs through tmp; the result lands in dst.  (sort_single.cu)
+msort_status kway_merge_dispatch(void* src_k, void* src_v, void* tmp_k, void* tmp_v,
+                                 void* dst_k, void* dst_v, const int64_t* off_host, int runs,
+                                 msort_dtype kd, msort_dtype vd, void* part_ws, cudaStream_t s);
+
+}  // namespace msort

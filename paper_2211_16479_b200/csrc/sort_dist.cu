@@ -1,0 +1,492 @@
+// sort_dist.cu -- multi-GPU stable merge sort (one process per GPU, NCCL).
+//
+// The paper's MPI merge sort: scatter equal chunks from rank 0
+// (P:412-434), sort each chunk locally (the "subsort"), then merge
+// up a rank tree until rank 0 holds everything.  Re-designed for
+// B200 + NVLink 5 / NVSwitch (every peer at full bandwidth):
+//   D1  local sort of each rank's shard            (sort_single.cu, K1..K3)
+//   D2  exact splitters by co-ranking the sorted shards: value-space
+//       bucket search, 8 bits per round, one tiny ncclAllReduce per round,
+//       then one ncclAllGather of (lt, eq) and a rank-order tie fill (K4)
+//   D3  one variable all-to-all of the sorted segments (grouped
+//       ncclSend/ncclRecv), the only bulk transfer
+//   D4  local stable k-way merge of the received runs, lower rank first (K5)
+// Output: rank r holds global stable positions [K_r, K_r + n_r) (DESIGN.md
+// R10/R11), so the call is in place and balanced for any key distribution.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "msort_device.cuh"
+#include "msort_internal.h"
+#include "plan.cuh"
+
+struct msort_comm_s {
+  ncclComm_t comm;
+  int rank;
+  int world;
+};
+
+namespace msort {
+
+constexpr int B = kCandidates;
+constexpr int kMaxWorld = 128;
+
+static msort_status nccl_fail(ncclResult_t r, const char* what) {
+  set_error(std::string(what) + ": " + ncclGetErrorString(r));
+  return MSORT_ERROR_NCCL;
+}
+#define MSORT_NCCL_TRY(expr)                                  \
+  do {                                                        \
+    ncclResult_t _r = (expr);                                 \
+    if (_r != ncclSuccess) return ::msort::nccl_fail(_r, #expr); \
+  } while (0)
+
+// ------------------------------------------------------------- K4 kernels
+__global__ void k4_set_u64(uint64_t* p, uint64_t v) { *p = v; }
+
+__global__ void k4_init(uint64_t* lohi, int nb, uint64_t umax) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nb) lohi[2 * r] = 0, lohi[2 * r + 1] = umax;
+}
+
+// cnt[r*B + b] = #{x in local shard : image(x) <= candidate b of boundary r}
+template <class K>
+__global__ void __launch_bounds__(256)
+    k4_count(const K* __restrict__ keys, int64_t n, const uint64_t* __restrict__ lohi, int nb,
+             uint64_t* __restrict__ cnt) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nb * B) return;
+  int r = t / B, b = t % B;
+  uint64_t c = plan::candidate(lohi[2 * r], lohi[2 * r + 1], b, B);
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {  // upper bound in image space (images are monotone in key order)
+    int64_t mid = (lo + hi) >> 1;
+    if ((uint64_t)KeyTraits<K>::image(__ldg(keys + mid)) <= c) lo = mid + 1;
+    else hi = mid;
+  }
+  cnt[t] = (uint64_t)lo;
+}
+
+// One thread per boundary r = 1..world-1: narrow [lo, hi] from the global counts.
+__global__ void k4_narrow(uint64_t* lohi, const uint64_t* __restrict__ total,
+                          const uint64_t* __restrict__ nsz, int world) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= world - 1) return;
+  uint64_t K = 0;
+  for (int j = 0; j <= r; ++j) K += nsz[j];  // K_{r+1}
+  uint64_t lo = lohi[2 * r], hi = lohi[2 * r + 1];
+  plan::narrow(lo, hi, total + (size_t)r * B, B, K);
+  lohi[2 * r] = lo, lohi[2 * r + 1] = hi;
+}
+
+// (lt, eq) of the local shard at v*_r = lo_r (= hi_r after the last round).
+template <class K>
+__global__ void k4_lteq(const K* __restrict__ keys, int64_t n, const uint64_t* __restrict__ lohi,
+                        int nb, uint64_t* __restrict__ lteq) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2 * nb) return;
+  int r = t / 2, upper = t % 2;
+  uint64_t v = lohi[2 * r];
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    uint64_t x = (uint64_t)KeyTraits<K>::image(__ldg(keys + mid));
+    if (upper ? x <= v : x < v) lo = mid + 1;
+    else hi = mid;
+  }
+  lteq[t] = (uint64_t)lo;  // t even: lower bound (lt); odd: upper bound (le)
+}
+
+// le -> eq in place after the gather would need a pass; instead convert locally
+__global__ void k4_le_to_eq(uint64_t* lteq, int nb) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nb) lteq[2 * r + 1] -= lteq[2 * r];
+}
+
+__global__ void k4_fill(const uint64_t* __restrict__ lteq_all, const uint64_t* __restrict__ nsz,
+                        int world, int64_t* __restrict__ split) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (world + 1) * world) return;
+  int r = t / world, j = t % world;
+  int64_t v;
+  if (r == 0) v = 0;
+  else if (r == world) v = (int64_t)nsz[j];
+  else {
+    uint64_t K = 0;
+    for (int q = 0; q < r; ++q) K += nsz[q];
+    v = plan::fill_one(K, lteq_all, world, r, j);
+  }
+  split[t] = v;
+}
+
+// ------------------------------------------ emulation collectives (1 GPU)
+struct PtrTable {
+  uint64_t* p[kMaxWorld];
+};
+__global__ void k_emul_allreduce(PtrTable t, int world, int count) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  uint64_t s = 0;
+  for (int r = 0; r < world; ++r) s += t.p[r][i];
+  for (int r = 0; r < world; ++r) t.p[r][i] = s;
+}
+__global__ void k_emul_allgather(PtrTable src, PtrTable dst, int world, int count) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= world * count) return;
+  int from = i / count, k = i % count;
+  uint64_t v = src.p[from][k];
+  for (int r = 0; r < world; ++r) dst.p[r][i] = v;
+}
+
+// -------------------------------------------------------- workspace carve
+struct DistWs {
+  char* sort_ws;
+  size_t sort_ws_bytes;
+  void* rk;  // receive keys
+  void* rv;  // receive vals
+  uint64_t *nsz_send, *nsz, *lohi, *cnt, *lteq, *lteq_all;
+  int64_t* split;
+};
+
+static size_t d2_bytes(int world) {
+  size_t nb = world > 1 ? world - 1 : 1;
+  size_t b = 0;
+  b += align_up(8, 256);                               // nsz_send
+  b += align_up(8 * (size_t)world, 256);               // nsz
+  b += align_up(16 * nb, 256);                         // lohi
+  b += align_up(8 * nb * B, 256);                      // cnt
+  b += align_up(16 * nb, 256);                         // lteq
+  b += align_up(16 * nb * (size_t)world, 256);         // lteq_all
+  b += align_up(8 * (size_t)(world + 1) * world, 256); // split
+  return b;
+}
+
+static DistWs carve(void* ws, size_t n, msort_dtype kd, msort_dtype vd, int world) {
+  DistWs d{};
+  char* w = static_cast<char*>(ws);
+  const size_t wk = dtype_size(kd);
+  const bool pairs = vd != MSORT_NONE;
+  d.sort_ws = w;
+  d.sort_ws_bytes = single_ws_bytes(n, kd, vd);
+  w += align_up(d.sort_ws_bytes, 256);
+  d.rk = w;
+  w += align_up(n * wk, 256);
+  d.rv = pairs ? w : nullptr;
+  if (pairs) w += align_up(n * 4, 256);
+  size_t nb = world > 1 ? world - 1 : 1;
+  d.nsz_send = (uint64_t*)w; w += align_up(8, 256);
+  d.nsz = (uint64_t*)w; w += align_up(8 * (size_t)world, 256);
+  d.lohi = (uint64_t*)w; w += align_up(16 * nb, 256);
+  d.cnt = (uint64_t*)w; w += align_up(8 * nb * B, 256);
+  d.lteq = (uint64_t*)w; w += align_up(16 * nb, 256);
+  d.lteq_all = (uint64_t*)w; w += align_up(16 * nb * (size_t)world, 256);
+  d.split = (int64_t*)w;
+  return d;
+}
+
+size_t dist_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd, int world) {
+  size_t b = align_up(single_ws_bytes(n, kd, vd), 256);
+  b += align_up(n * dtype_size(kd), 256);
+  if (vd != MSORT_NONE) b += align_up(n * 4, 256);
+  b += d2_bytes(world);
+  return b;
+}
+
+// ------------------------------------------------------------ the driver
+struct RankIO {
+  void* keys;
+  void* vals;
+  size_t n;
+  DistWs ws;
+};
+
+static ncclDataType_t nccl_type(msort_dtype d) {
+  switch (d) {
+    case MSORT_INT32: return ncclInt32;
+    case MSORT_UINT32: return ncclUint32;
+    case MSORT_INT64: return ncclInt64;
+    default: return ncclUint64;
+  }
+}
+
+// Collectives over NCCL: one local rank.
+struct NcclColl {
+  msort_comm_s* c;
+  cudaStream_t s;
+  int world() const { return c->world; }
+  msort_status allgather_u64(RankIO* io, uint64_t* DistWs::*src, uint64_t* DistWs::*dst,
+                             size_t count) {
+    LaunchScope ls(KC_NCCL, s);
+    MSORT_NCCL_TRY(ncclAllGather(io[0].ws.*src, io[0].ws.*dst, count, ncclUint64, c->comm, s));
+    return MSORT_SUCCESS;
+  }
+  msort_status allreduce_u64(RankIO* io, uint64_t* DistWs::*buf, size_t count) {
+    LaunchScope ls(KC_NCCL, s);
+    MSORT_NCCL_TRY(ncclAllReduce(io[0].ws.*buf, io[0].ws.*buf, count, ncclUint64, ncclSum,
+                                 c->comm, s));
+    return MSORT_SUCCESS;
+  }
+  // D3: rank me sends keys[s[r][me], s[r+1][me]) to every r; receives run j
+  // (length s[me+1][j] - s[me][j]) into recv at offset sum_{j'<j} of those.
+  msort_status exchange(RankIO* io, const std::vector<int64_t>& S, msort_dtype kd,
+                        msort_dtype vd) {
+    const int p = c->world, me = c->rank;
+    const size_t wk = dtype_size(kd);
+    RankIO& r0 = io[0];
+    auto sp = [&](int r, int j) { return S[(size_t)r * p + j]; };
+    int64_t roff = 0;
+    LaunchScope ls(KC_NCCL, s);
+    MSORT_NCCL_TRY(ncclGroupStart());
+    for (int j = 0; j < p; ++j) {
+      // receive run j
+      int64_t rc = sp(me + 1, j) - sp(me, j);
+      int64_t sc = sp(j + 1, me) - sp(j, me);  // what I send to rank j
+      if (j == me) {
+        if (rc > 0) {
+          MSORT_CUDA_TRY(cudaMemcpyAsync((char*)r0.ws.rk + roff * wk,
+                                         (char*)r0.keys + sp(me, me) * wk, rc * wk,
+                                         cudaMemcpyDeviceToDevice, s));
+          if (vd != MSORT_NONE)
+            MSORT_CUDA_TRY(cudaMemcpyAsync((char*)r0.ws.rv + roff * 4,
+                                           (char*)r0.vals + sp(me, me) * 4, rc * 4,
+                                           cudaMemcpyDeviceToDevice, s));
+        }
+      } else {
+        if (sc > 0) {
+          MSORT_NCCL_TRY(ncclSend((char*)r0.keys + sp(j, me) * wk, (size_t)sc, nccl_type(kd), j,
+                                  c->comm, s));
+          if (vd != MSORT_NONE)
+            MSORT_NCCL_TRY(ncclSend((char*)r0.vals + sp(j, me) * 4, (size_t)sc, ncclUint32, j,
+                                    c->comm, s));
+        }
+        if (rc > 0) {
+          MSORT_NCCL_TRY(ncclRecv((char*)r0.ws.rk + roff * wk, (size_t)rc, nccl_type(kd), j,
+                                  c->comm, s));
+          if (vd != MSORT_NONE)
+            MSORT_NCCL_TRY(ncclRecv((char*)r0.ws.rv + roff * 4, (size_t)rc, ncclUint32, j,
+                                    c->comm, s));
+        }
+      }
+      roff += rc;
+    }
+    MSORT_NCCL_TRY(ncclGroupEnd());
+    return MSORT_SUCCESS;
+  }
+  int rank_of(int local) const { return c->rank + local; }
+};
+
+// Collectives emulated on one device for `world` virtual ranks.
+struct EmulColl {
+  int p;
+  cudaStream_t s;
+  int world() const { return p; }
+  msort_status allgather_u64(RankIO* io, uint64_t* DistWs::*src, uint64_t* DistWs::*dst,
+                             size_t count) {
+    PtrTable a{}, b{};
+    for (int r = 0; r < p; ++r) a.p[r] = io[r].ws.*src, b.p[r] = io[r].ws.*dst;
+    LaunchScope ls(KC_SPLITTER, s);
+    int tot = (int)(p * count);
+    k_emul_allgather<<<(tot + 255) / 256, 256, 0, s>>>(a, b, p, (int)count);
+    MSORT_CUDA_TRY(cudaGetLastError());
+    return MSORT_SUCCESS;
+  }
+  msort_status allreduce_u64(RankIO* io, uint64_t* DistWs::*buf, size_t count) {
+    PtrTable a{};
+    for (int r = 0; r < p; ++r) a.p[r] = io[r].ws.*buf;
+    LaunchScope ls(KC_SPLITTER, s);
+    k_emul_allreduce<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(a, p, (int)count);
+    MSORT_CUDA_TRY(cudaGetLastError());
+    return MSORT_SUCCESS;
+  }
+  msort_status exchange(RankIO* io, const std::vector<int64_t>& S, msort_dtype kd,
+                        msort_dtype vd) {
+    const size_t wk = dtype_size(kd);
+    auto sp = [&](int r, int j) { return S[(size_t)r * p + j]; };
+    for (int me = 0; me < p; ++me) {
+      int64_t roff = 0;
+      for (int j = 0; j < p; ++j) {
+        int64_t rc = sp(me + 1, j) - sp(me, j);
+        if (rc > 0) {
+          MSORT_CUDA_TRY(cudaMemcpyAsync((char*)io[me].ws.rk + roff * wk,
+                                         (char*)io[j].keys + sp(me, j) * wk, rc * wk,
+                                         cudaMemcpyDeviceToDevice, s));
+          if (vd != MSORT_NONE)
+            MSORT_CUDA_TRY(cudaMemcpyAsync((char*)io[me].ws.rv + roff * 4,
+                                           (char*)io[j].vals + sp(me, j) * 4, rc * 4,
+                                           cudaMemcpyDeviceToDevice, s));
+        }
+        roff += rc;
+      }
+    }
+    return MSORT_SUCCESS;
+  }
+  int rank_of(int local) const { return local; }
+};
+
+template <class K>
+static void launch_count(const RankIO& io, int nb, cudaStream_t s) {
+  int tot = nb * B;
+  k4_count<K><<<(tot + 255) / 256, 256, 0, s>>>((const K*)io.keys, (int64_t)io.n, io.ws.lohi, nb,
+                                                io.ws.cnt);
+}
+template <class K>
+static void launch_lteq(const RankIO& io, int nb, cudaStream_t s) {
+  k4_lteq<K><<<(2 * nb + 255) / 256, 256, 0, s>>>((const K*)io.keys, (int64_t)io.n, io.ws.lohi,
+                                                  nb, io.ws.lteq);
+}
+
+static int rounds_for(msort_dtype kd) { return dtype_size(kd) == 4 ? 4 : 8; }
+
+template <class Coll>
+static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msort_dtype vd,
+                             cudaStream_t s, int64_t* split_out) {
+  const int p = C.world();
+  const int nb = p - 1;
+  // D1: local sorts
+  for (int l = 0; l < nloc; ++l)
+    if (io[l].n >= 2)
+      MSORT_TRY(sort_single_dispatch(io[l].keys, io[l].vals, io[l].n, kd, vd, io[l].ws.sort_ws,
+                                     io[l].ws.sort_ws_bytes, s));
+  std::vector<int64_t> S((size_t)(p + 1) * p);
+  if (p == 1) {
+    S[0] = 0, S[1] = (int64_t)io[0].n;
+    if (split_out) memcpy(split_out, S.data(), S.size() * 8);
+    return MSORT_SUCCESS;
+  }
+  const uint64_t umax = dtype_size(kd) == 4 ? 0xffffffffull : ~0ull;
+  // D2: sizes, then the bucket search, then (lt, eq) and the fill
+  for (int l = 0; l < nloc; ++l) {
+    LaunchScope ls(KC_SPLITTER, s);
+    k4_set_u64<<<1, 1, 0, s>>>(io[l].ws.nsz_send, (uint64_t)io[l].n);
+    k4_init<<<(nb + 127) / 128, 128, 0, s>>>(io[l].ws.lohi, nb, umax);
+  }
+  MSORT_CUDA_TRY(cudaGetLastError());
+  MSORT_TRY(C.allgather_u64(io, &DistWs::nsz_send, &DistWs::nsz, 1));
+  const int R = rounds_for(kd);
+  for (int round = 0; round < R; ++round) {
+    for (int l = 0; l < nloc; ++l) {
+      LaunchScope ls(KC_SPLITTER, s);
+      switch (kd) {
+        case MSORT_INT32: launch_count<int32_t>(io[l], nb, s); break;
+        case MSORT_UINT32: launch_count<uint32_t>(io[l], nb, s); break;
+        case MSORT_INT64: launch_count<int64_t>(io[l], nb, s); break;
+        default: launch_count<uint64_t>(io[l], nb, s); break;
+      }
+    }
+    MSORT_CUDA_TRY(cudaGetLastError());
+    MSORT_TRY(C.allreduce_u64(io, &DistWs::cnt, (size_t)nb * B));
+    for (int l = 0; l < nloc; ++l) {
+      LaunchScope ls(KC_SPLITTER, s);
+      k4_narrow<<<(nb + 127) / 128, 128, 0, s>>>(io[l].ws.lohi, io[l].ws.cnt, io[l].ws.nsz, p);
+    }
+    MSORT_CUDA_TRY(cudaGetLastError());
+  }
+  for (int l = 0; l < nloc; ++l) {
+    LaunchScope ls(KC_SPLITTER, s);
+    switch (kd) {
+      case MSORT_INT32: launch_lteq<int32_t>(io[l], nb, s); break;
+      case MSORT_UINT32: launch_lteq<uint32_t>(io[l], nb, s); break;
+      case MSORT_INT64: launch_lteq<int64_t>(io[l], nb, s); break;
+      default: launch_lteq<uint64_t>(io[l], nb, s); break;
+    }
+    k4_le_to_eq<<<(nb + 127) / 128, 128, 0, s>>>(io[l].ws.lteq, nb);
+  }
+  MSORT_CUDA_TRY(cudaGetLastError());
+  MSORT_TRY(C.allgather_u64(io, &DistWs::lteq, &DistWs::lteq_all, (size_t)2 * nb));
+  for (int l = 0; l < nloc; ++l) {
+    LaunchScope ls(KC_SPLITTER, s);
+    int tot = (p + 1) * p;
+    k4_fill<<<(tot + 127) / 128, 128, 0, s>>>(io[l].ws.lteq_all, io[l].ws.nsz, p, io[l].ws.split);
+  }
+  MSORT_CUDA_TRY(cudaGetLastError());
+  // The one host synchronisation: the exchange sizes are needed on the host.
+  MSORT_CUDA_TRY(cudaMemcpyAsync(S.data(), io[0].ws.split, S.size() * 8, cudaMemcpyDeviceToHost, s));
+  MSORT_CUDA_TRY(cudaStreamSynchronize(s));
+  if (split_out) memcpy(split_out, S.data(), S.size() * 8);
+  // sanity: every rank's output count equals its input count
+  for (int l = 0; l < nloc; ++l) {
+    int me = C.rank_of(l);
+    int64_t got = 0;
+    for (int j = 0; j < p; ++j) got += S[(size_t)(me + 1) * p + j] - S[(size_t)me * p + j];
+    if (got != (int64_t)io[l].n) {
+      set_error("split matrix inconsistent with local size (ranks disagree on inputs?)");
+      return MSORT_ERROR_INVALID_VALUE;
+    }
+  }
+  // D3: exchange
+  MSORT_TRY(C.exchange(io, S, kd, vd));
+  // D4: k-way merge of the received runs (source-rank order) into keys
+  for (int l = 0; l < nloc; ++l) {
+    int me = C.rank_of(l);
+    std::vector<int64_t> off(p + 1);
+    off[0] = 0;
+    for (int j = 0; j < p; ++j) off[j + 1] = off[j] + S[(size_t)(me + 1) * p + j] - S[(size_t)me * p + j];
+    if (io[l].n == 0) continue;
+    const size_t wk = dtype_size(kd);
+    char* sw = io[l].ws.sort_ws;  // sort workspace doubles as the ping-pong buffer
+    void* tk = sw;
+    void* tv = vd != MSORT_NONE ? sw + align_up(io[l].n * wk, 256) : nullptr;
+    void* part = sw + align_up(io[l].n * wk, 256) + (vd != MSORT_NONE ? align_up(io[l].n * 4, 256) : 0);
+    MSORT_TRY(kway_merge_dispatch(io[l].ws.rk, io[l].ws.rv, tk, tv, io[l].keys, io[l].vals,
+                                  off.data(), p, kd, vd, part, s));
+  }
+  return MSORT_SUCCESS;
+}
+
+msort_status dist_nccl(void* keys, void* vals, size_t n, msort_dtype kd, msort_dtype vd,
+                       msort_comm_s* comm, void* ws, cudaStream_t s, int64_t* split_out) {
+  if (comm->world > kMaxWorld) {
+    set_error("world too large");
+    return MSORT_ERROR_NOT_SUPPORTED;
+  }
+  RankIO io{keys, vd == MSORT_NONE ? nullptr : vals, n, carve(ws, n, kd, vd, comm->world)};
+  NcclColl C{comm, s};
+  return dist_run(C, &io, 1, kd, vd, s, split_out);
+}
+
+msort_status dist_emulated(void* const* keys, void* const* vals, const size_t* n, int world,
+                           msort_dtype kd, msort_dtype vd, void* const* ws, cudaStream_t s,
+                           int64_t* split_out) {
+  if (world > kMaxWorld) {
+    set_error("world too large");
+    return MSORT_ERROR_NOT_SUPPORTED;
+  }
+  std::vector<RankIO> io(world);
+  for (int r = 0; r < world; ++r)
+    io[r] = RankIO{keys[r], vd == MSORT_NONE || !vals ? nullptr : vals[r], n[r],
+                   carve(ws[r], n[r], kd, vd, world)};
+  EmulColl C{world, s};
+  return dist_run(C, io.data(), world, kd, vd, s, split_out);
+}
+
+msort_status comm_unique_id(void* out) {
+  ncclUniqueId id;
+  MSORT_NCCL_TRY(ncclGetUniqueId(&id));
+  memcpy(out, &id, sizeof(id));
+  return MSORT_SUCCESS;
+}
+
+msort_status comm_init(const void* idp, int rank, int world, msort_comm_s** out) {
+  ncclUniqueId id;
+  memcpy(&id, idp, sizeof(id));
+  ncclComm_t c;
+  MSORT_NCCL_TRY(ncclCommInitRank(&c, world, id, rank));
+  *out = new msort_comm_s{c, rank, world};
+  return MSORT_SUCCESS;
+}
+
+msort_status comm_destroy(msort_comm_s* c) {
+  if (!c) return MSORT_SUCCESS;
+  ncclResult_t r = ncclCommDestroy(c->comm);
+  delete c;
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
+  return MSORT_SUCCESS;
+}
+
+int comm_world(msort_comm_s* c) { return c->world; }
+
+}  // namespace msort

@@ -1,0 +1,161 @@
+"""GPU parity of the distributed path (D1-D4) on one B200.
+
+Multi-rank: the library's single-process emulation runs p virtual ranks on
+one device with the same kernels, splitter planning and k-way merge (the
+NCCL calls replaced by device reductions/copies).  The real NCCL path runs at
+p = 1 with a one-rank communicator.  Expected values: oracle.split_matrix and
+oracle slices of the stably sorted rank-major concatenation (R10/R11),
+plus the independent C5 split matrices of SURVEY.md §8(c) addendum.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import msort_inputs as mi
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ms():
+    import paper_2211_16479_b200 as m
+
+    return m
+
+
+def _dev(a):
+    if a.dtype == np.uint32:
+        return torch.from_numpy(a.view(np.int32)).cuda().view(torch.uint32)
+    if a.dtype == np.uint64:
+        return torch.from_numpy(a.view(np.int64)).cuda().view(torch.uint64)
+    return torch.from_numpy(a).cuda()
+
+
+def _host(t, dt):
+    if t.dtype == torch.uint32:
+        t = t.view(torch.int32)
+    if t.dtype == torch.uint64:
+        t = t.view(torch.int64)
+    return t.cpu().numpy().view(dt)
+
+
+def run_emulated(ms, orc, shards, pairs):
+    p = len(shards)
+    K = np.concatenate([[0], np.cumsum([s.size for s in shards])])
+    vals = [np.arange(K[r], K[r + 1], dtype=np.uint32) for r in range(p)] if pairs else None
+    kd = [_dev(s) for s in shards]
+    vd = [_dev(v) for v in vals] if pairs else None
+    split = ms.msort_sort_distributed_emulated(kd, vd)
+    torch.cuda.synchronize()
+    assert np.array_equal(split, orc.split_matrix(shards))
+    cat = np.concatenate(shards)
+    if pairs:
+        ek, ev = orc.sort(cat, np.arange(cat.size, dtype=np.uint32))
+    else:
+        ek, ev = orc.sort(cat), None
+    for r in range(p):
+        assert np.array_equal(_host(kd[r], cat.dtype), ek[K[r]:K[r + 1]]), f"rank {r} keys"
+        if pairs:
+            assert np.array_equal(_host(vd[r], np.uint32), ev[K[r]:K[r + 1]]), f"rank {r} vals"
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 7, 8])
+@pytest.mark.parametrize("pairs", [False, True])
+def test_emulated_random_unequal_sizes(ms, orc, p, pairs):
+    rng = np.random.default_rng(p * 10 + pairs)
+    for trial in range(3):
+        sizes = rng.integers(0, 40000, size=p)
+        if trial == 1:
+            sizes[0] = 0
+        if trial == 2 and p > 2:
+            sizes[p // 2] = 0
+            sizes[-1] = 1
+        shards = [mi.keys(int(s), 1000 * p + 10 * trial + r, "i32") for r, s in enumerate(sizes)]
+        run_emulated(ms, orc, shards, pairs)
+
+
+@pytest.mark.parametrize("dtype,dist", [(np.int64, ("mod", 5)), (np.uint32, "eq"),
+                                        (np.int32, "eq"), (np.uint64, "u64"),
+                                        (np.int64, ("mod", 1000))])
+def test_emulated_duplicates_across_ranks(ms, orc, dtype, dist):
+    """Keys equal across shards: ties must be handed out in rank order."""
+    for p in (2, 3, 8):
+        sizes = [9000 + 1000 * r for r in range(p)]
+        if dist == "eq":
+            shards = [np.full(s, 7, dtype=dtype) for s in sizes]
+        elif dist == "u64":
+            shards = [mi.keys(s, 50 + r, "u64") for r, s in enumerate(sizes)]
+        else:
+            shards = [mi.keys(s, 60 + r, dist).astype(dtype) for r, s in enumerate(sizes)]
+        run_emulated(ms, orc, shards, True)
+
+
+def test_emulated_extremes(ms, orc):
+    for dtype in (np.int32, np.uint32, np.int64, np.uint64):
+        info = np.iinfo(dtype)
+        pool = np.array([info.min, 0, info.max], dtype=dtype)
+        shards = [pool[(mi.splitmix64(5000 + r, r) % np.uint64(3)).astype(np.int64)]
+                  for r in range(4)]
+        run_emulated(ms, orc, shards, True)
+
+
+# SURVEY.md §8(c) addendum: C5 split rows (independent numpy computation)
+C5_ROWS = {
+    2: {1: [134212162, 134223294]},
+    4: {1: [67110172, 67108539, 67110135, 67106610],
+        2: [134217801, 134228923, 134215104, 134209084],
+        3: [201323646, 201329812, 201327789, 201325121]},
+    8: {1: [33556935, 33554878, 33558649, 33554402, 33564042, 33547661, 33550740, 33548149],
+        4: [134219922, 134230981, 134217240, 134211196, 134216455, 134211743, 134221324,
+            134212963],
+        7: [234880444, 234882874, 234877251, 234874288, 234885948, 234884604, 234881155,
+            234881628]},
+}
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_c5_split_matrix_full_size(ms, p):
+    """C5 at full size (2^28 int32 per rank, seed 4+rank): the split matrix
+    equals the survey's, and each rank's output is sorted, in range, and the
+    ranks together are a permutation of the input (multiset via sums/minmax)."""
+    n = 1 << 28
+    kd = [mi.keys_torch(n, 4 + r, "u31", device="cuda") for r in range(p)]
+    sums = sum(int(k.sum(dtype=torch.int64)) for k in kd)
+    split = ms.msort_sort_distributed_emulated(kd)
+    torch.cuda.synchronize()
+    for r, row in C5_ROWS[p].items():
+        assert split[r].tolist() == row
+    prev_max = None
+    for k in kd:
+        assert bool((k[1:] >= k[:-1]).all())
+        if prev_max is not None:
+            assert int(k[0]) >= prev_max
+        prev_max = int(k[-1])
+    assert sum(int(k.sum(dtype=torch.int64)) for k in kd) == sums
+    del kd
+    torch.cuda.empty_cache()
+
+
+def test_nccl_one_rank(ms, orc):
+    """The real NCCL path with a one-rank communicator on this GPU."""
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    comm = ms.Comm()
+    n = 100003
+    k = mi.keys(n, 77, ("mod", 100))
+    v = np.arange(n, dtype=np.uint32)
+    kd, vd = _dev(k), _dev(v)
+    _, _, split = ms.msort_sort_distributed(kd, comm, vals=vd, return_split=True)
+    torch.cuda.synchronize()
+    ek, ev = orc.sort(k, v)
+    assert split.tolist() == [[0], [n]]
+    assert np.array_equal(_host(kd, np.int64), ek)
+    assert np.array_equal(_host(vd, np.uint32), ev)
+    comm.close()

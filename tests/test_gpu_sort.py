@@ -1,0 +1,202 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Every expected value comes from oracle/ on the same seeded input.  Sizes span
+several tiles and ragged tails; the BASELINE.json configs C1-C4 run at full
+size, C5's per-GPU shard (2^28 int32, the bench workload) too.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import msort_inputs as mi
+
+pytestmark = pytest.mark.gpu
+
+NP_OF = {"i32": np.int32, "u32": np.uint32, "i64": np.int64, "u64": np.uint64}
+
+
+@pytest.fixture(scope="module")
+def ms():
+    import paper_2211_16479_b200 as m
+
+    assert torch.cuda.is_available()
+    return m
+
+
+def to_dev(a: np.ndarray) -> torch.Tensor:
+    if a.dtype == np.uint32:
+        return torch.from_numpy(a.view(np.int32)).cuda().view(torch.uint32)
+    if a.dtype == np.uint64:
+        return torch.from_numpy(a.view(np.int64)).cuda().view(torch.uint64)
+    return torch.from_numpy(a).cuda()
+
+
+def to_host(t: torch.Tensor, dtype) -> np.ndarray:
+    if t.dtype == torch.uint32:
+        t = t.view(torch.int32)
+    elif t.dtype == torch.uint64:
+        t = t.view(torch.int64)
+    return t.cpu().numpy().view(dtype)
+
+
+def gpu_sort(ms, k: np.ndarray, v: np.ndarray | None):
+    kd = to_dev(k)
+    vd = to_dev(v) if v is not None else None
+    ms.msort_sort_pairs(kd, vd)
+    torch.cuda.synchronize()
+    ok = to_host(kd, k.dtype)
+    ov = to_host(vd, np.uint32) if v is not None else None
+    return ok, ov
+
+
+def oracle_sort(orc, k, v):
+    if k.size >= (1 << 24):
+        kk = k.copy()
+        vv = None if v is None else v.copy()
+        orc.paper_mp_inplace(kk, vv, os.cpu_count() or 1)
+        return kk, vv
+    if v is None:
+        return orc.sort(k), None
+    return orc.sort(k, v)
+
+
+def check_parity(ms, orc, k, v):
+    ok, ov = gpu_sort(ms, k, v)
+    ek, ev = oracle_sort(orc, k, v)
+    assert np.array_equal(ok, ek), f"keys differ at {np.nonzero(ok != ek)[0][:5]}"
+    if v is not None:
+        assert np.array_equal(ov, ev), f"payload differs at {np.nonzero(ov != ev)[0][:5]}"
+
+
+def _keys(n, seed, dist, dtype):
+    if dist == "dup":
+        return mi.keys(n, seed, ("mod", 3)).astype(dtype)
+    if dist == "eq":
+        return np.full(n, 5, dtype=dtype)
+    if dist == "asc":
+        return np.arange(n).astype(dtype)
+    if dist == "desc":
+        return np.arange(n)[::-1].astype(dtype).copy()
+    if dist == "ext":  # extremes of the dtype mixed with small values
+        info = np.iinfo(dtype)
+        pool = np.array([info.min, info.min + 1, 0, 1, info.max - 1, info.max], dtype=dtype)
+        return pool[(mi.splitmix64(n, seed) % np.uint64(6)).astype(np.int64)]
+    return mi.keys(n, seed, {np.int32: "i32", np.uint32: "u32", np.int64: "i64",
+                             np.uint64: "u64"}[dtype])
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.uint32, np.int64, np.uint64])
+@pytest.mark.parametrize("pairs", [False, True])
+def test_sizes_around_tiles(ms, orc, dtype, pairs):
+    kd = {np.int32: 0, np.uint32: 1, np.int64: 2, np.uint64: 3}[dtype]
+    T = ms.tile_size(kd, ms.MSORT_UINT32 if pairs else ms.MSORT_NONE)
+    sizes = [0, 1, 2, 3, 17, T - 1, T, T + 1, 2 * T - 1, 2 * T, 2 * T + 1, 3 * T + 5, 5 * T - 3,
+             8 * T, 8 * T + 1, (1 << 17) - 1, (1 << 17) + 1, 123457]
+    for i, n in enumerate(sizes):
+        for dist in ("rand", "dup"):
+            k = _keys(n, 100 + i, dist, dtype)
+            v = mi.index_payload(n) if pairs else None
+            check_parity(ms, orc, k, v)
+
+
+@pytest.mark.parametrize("dist", ["eq", "asc", "desc", "ext", "dup"])
+@pytest.mark.parametrize("dtype", [np.int32, np.uint32, np.int64, np.uint64])
+def test_structured_inputs(ms, orc, dist, dtype):
+    for n in (4096 * 5 + 77, 300001):
+        check_parity(ms, orc, _keys(n, 7, dist, dtype), mi.index_payload(n))
+        check_parity(ms, orc, _keys(n, 8, dist, dtype), None)
+
+
+def test_misaligned_views(ms, orc):
+    """Pointers aligned to the element but not to 16 bytes (offsets 1-3)."""
+    n = 50000
+    for off in (1, 2, 3):
+        base = mi.keys(n + off, 11 + off, "i32")
+        vals = mi.index_payload(n + off)
+        kd = to_dev(base)[off:]
+        vd = to_dev(vals)[off:]
+        ms.msort_sort_pairs(kd, vd)
+        torch.cuda.synchronize()
+        ek, ev = orc.sort(base[off:].copy(), vals[off:].copy())
+        assert np.array_equal(to_host(kd, np.int32), ek)
+        assert np.array_equal(to_host(vd, np.uint32), ev)
+
+
+def test_invalid_arguments(ms):
+    import ctypes
+
+    L = ms.lib
+    assert L.msort_sort(None, 0, 0, None) == 0  # n == 0: no-op
+    t = torch.zeros(8, dtype=torch.int32, device="cuda")
+    assert L.msort_sort(ctypes.c_void_p(t.data_ptr() + 2), 4, 0, None) == 1  # misaligned
+    assert L.msort_sort(ctypes.c_void_p(t.data_ptr()), 4, 7, None) == 1  # bad dtype
+    assert L.msort_sort_pairs(ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(t.data_ptr() + 8), 4,
+                              0, 1, None) == 1  # overlap
+    assert L.msort_sort_pairs(ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(t.data_ptr() + 16), 2,
+                              0, 2, None) == 2  # 8-byte payload not built
+
+
+def test_convenience_calls_allocate(ms, orc):
+    """msort_sort / msort_sort_pairs (library-allocated workspace)."""
+    import ctypes
+
+    n = 70001
+    k = mi.keys(n, 3, "u32")
+    kd = to_dev(k)
+    st = ms.lib.msort_sort(ctypes.c_void_p(kd.data_ptr()), n, ms.MSORT_UINT32,
+                           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert st == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(kd, np.uint32), orc.sort(k))
+
+
+# ----------------------------------------------------- BASELINE.json configs
+def test_c1(ms, orc):
+    k, _ = mi.config_input("C1")
+    check_parity(ms, orc, k, None)
+
+
+def test_c2_random_sorted_reversed(ms, orc):
+    k, _ = mi.config_input("C2")
+    ek = oracle_sort(orc, k, None)[0]
+    for variant in (k, ek, ek[::-1].copy()):  # reading R8: C2s / C2r
+        ok, _ = gpu_sort(ms, variant, None)
+        assert np.array_equal(ok, ek)
+
+
+def test_c3_int64_duplicates_stability(ms, orc):
+    k, v = mi.config_input("C3")
+    ok, ov = gpu_sort(ms, k, v)
+    assert orc.check(k, ok, ov) == 0
+    ek, ev = oracle_sort(orc, k, v)
+    assert np.array_equal(ok, ek) and np.array_equal(ov, ev)
+    # SURVEY.md §8(c) stability pin: first three key-0 payloads
+    assert ov[:3].tolist() == [108, 739, 1575]
+
+
+def test_c4_uint32_pairs(ms, orc):
+    k, v = mi.config_input("C4")
+    ok, ov = gpu_sort(ms, k, v)
+    ek, ev = oracle_sort(orc, k, v)
+    assert np.array_equal(ok, ek) and np.array_equal(ov, ev)
+
+
+def test_c5_shard_full_size(ms, orc):
+    """The bench workload: one 2^28 int32 shard (seed 4), bit-exact."""
+    n = 1 << 28
+    kd = mi.keys_torch(n, 4, "u31", device="cuda")
+    k = kd.cpu().numpy()
+    ms.msort_sort(kd)
+    torch.cuda.synchronize()
+    ek = k.copy()
+    orc.paper_mp_inplace(ek, None, os.cpu_count() or 1)
+    assert np.array_equal(kd.cpu().numpy(), ek)
+
+
+def test_torch_generator_on_gpu_matches_numpy():
+    for dist in ("u31", "u32", ("mod", 1000), "i64"):
+        a = mi.keys(1 << 20, 9, dist)
+        b = mi.keys_torch(1 << 20, 9, dist, device="cuda")
+        assert np.array_equal(a, to_host(b, a.dtype))
