@@ -1,0 +1,368 @@
+#!/usr/bin/env python3
+"""Benchmark: stable merge sort of 2^28 int32 keys per GPU (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: distributed sort)
+
+Workload (BASELINE.json metric "... (int32, 2^28/GPU)", config C5): every rank
+holds 2^28 int32 keys uniform in [0, 2^31) from counter-mode SplitMix64 with
+seed 4 + rank (msort_inputs; DESIGN.md input recipe).  N = 1: one local sort
+(msort_sort_out_ws).  N > 1: the distributed sort (local sort, splitter
+co-rank, NCCL all-to-all, k-way merge; msort_sort_distributed_out_ws), and the
+output is globally sorted across ranks.
+
+A step sorts the pristine input into an output buffer (out-of-place, so no
+restore copy is needed and the input is never sorted data).  Inputs and the
+workspace (1 GiB + 1 GiB + 1 GiB per GPU) are far larger than L2 (126 MB), so
+no L2 flush is done between steps.  Timing: W untimed steps, then K steps
+between a barrier + cuda.synchronize on both sides, CUDA events on the
+launching stream, max over ranks.  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, textbook top-down merge sort)
+on a bounded sample of the same workload on this host's cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sorted keys/sec and % of HBM/NVLink roofline at 1/2/4/8 B200 (int32, 2^28/GPU)"
+N_PER_GPU = 1 << 28
+SEED0 = 4
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU (default 2^28)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload_key: str):
+    """Per-launch dram bytes of the merge pass from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload_key, {}).get("merge_pass_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.rows = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(gpu_index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = [r for (t, r) in self.rows if t0 - 0.15 <= t <= t1 + 0.15] or [r for _, r in self.rows]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"]}
+        sm = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        mx = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if len(r) > 6 + i and r[6 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows),
+                "power_w_max": max((float(r[4]) for r in rows
+                                    if r[4].replace(".", "").isdigit()), default=None)}
+
+
+def cpu_baseline(n_sample: int, samples: int):
+    """The oracle, as it stands, on bounded samples of the workload (rank 0)."""
+    import msort_inputs as mi
+    import oracle
+
+    oracle.build()
+    t = 0.0
+    for s in range(samples):
+        k = mi.keys(n_sample, SEED0 + 100 + s, "u31")
+        t0 = time.perf_counter()
+        oracle.sort_inplace(k)
+        t += time.perf_counter() - t0
+    return {"value": n_sample * samples / t, "unit": "keys/s", "cores": 1, "kind": "oracle",
+            "sample": f"{samples} x 2^{n_sample.bit_length() - 1} int32 keys uniform [0,2^31) "
+                      f"(same generator as the workload), single-threaded top-down merge sort "
+                      f"(oracle/msort_oracle.c), {t:.1f} s of CPU"}
+
+
+def reference_arm(args, rank):
+    """--impl reference: the CPU oracle on a bounded sample per step."""
+    if rank != 0:
+        return
+    import msort_inputs as mi
+    import oracle
+
+    oracle.build()
+    n_s = 1 << 22
+    base = mi.keys(n_s, SEED0, "u31")
+    for _ in range(args.warmup):
+        oracle.sort_inplace(base.copy())
+    t = 0.0
+    for _ in range(args.steps):
+        k = base.copy()
+        t0 = time.perf_counter()
+        oracle.sort_inplace(k)
+        t += time.perf_counter() - t0
+    v = n_s * args.steps / t
+    sample = (f"per step: first 2^22 keys of the rank-0 shard (seed 4), single-threaded "
+              f"top-down merge sort (oracle/msort_oracle.c)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "keys/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": "C5 sample: 2^22 int32 keys uniform [0,2^31), seed 4",
+                   "n_per_step": n_s},
+        "cpu_baseline": {"value": v, "unit": "keys/s", "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+
+    import numpy as np
+    import torch
+
+    import msort_inputs as mi
+    import paper_2211_16479_b200 as ms
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        comm = ms.Comm()
+
+    n = args.n
+    kin = mi.keys_torch(n, SEED0 + rank, "u31", device=dev)
+    kout = torch.empty_like(kin)
+    ws = ms.workspace(n, torch.int32, False, world=world, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if world == 1:
+            ms.msort_sort_out(kin, kout, ws=ws, stream=stream)
+        else:
+            ms.msort_sort_distributed_out(kin, kout, comm, ws=ws, stream=stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    sampler = ClockSampler(local)
+    time.sleep(0.3)  # let nvidia-smi start sampling
+    ms.profile_reset()
+    ms.profile_enable(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    t0 = time.time()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    t1 = time.time()
+    launches = ms.launch_count()
+    ms.profile_enable(False)
+    prof = ms.profile_read()
+    time.sleep(0.2)
+    sampler.stop()
+    ms_total = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+
+    # verify the last step's output (sorted, same multiset sum, ranks ordered)
+    ok = bool((kout[1:] >= kout[:-1]).all()) if n > 1 else True
+    ok &= int(kout.sum(dtype=torch.int64)) == int(kin.sum(dtype=torch.int64)) if world == 1 else True
+    if world > 1:
+        edge = torch.tensor([int(kout[0]), int(kout[-1])], dtype=torch.int64, device=dev)
+        edges = [torch.zeros_like(edge) for _ in range(world)]
+        dist.all_gather(edges, edge)
+        e = torch.stack(edges).cpu().numpy()
+        ok &= bool(all(e[r][1] <= e[r + 1][0] for r in range(world - 1)))
+        s_in = torch.tensor([int(kin.sum(dtype=torch.int64)), int(kout.sum(dtype=torch.int64))],
+                            dtype=torch.int64, device=dev)
+        dist.all_reduce(s_in)
+        ok &= int(s_in[0]) == int(s_in[1])
+        okt = torch.tensor([1 if ok else 0], device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        ok = bool(okt.item())
+
+    # roofline of the dominant kernel (the merge pass) from live CUDA events
+    peak, peak_src = load_peaks()
+    mp_launches, mp_ms = prof["merge_pass"]
+    wk = 4
+    alg_bytes = 2 * n * wk  # each merge pass reads and writes every key once
+    roof = None
+    if mp_launches:
+        avg_s = mp_ms / mp_launches / 1e3
+        ach = alg_bytes / avg_s / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": ncu_traffic(f"C5_n{n}"),
+                "kernel": "k3_merge_pass", "algorithmic_bytes_per_launch": alg_bytes,
+                "launches": mp_launches, "avg_launch_ms": round(mp_ms / mp_launches, 4),
+                "peak_source": peak_src}
+    phases = {k: {"launches_per_step": v[0] / args.steps, "ms_per_step": round(v[1] / args.steps, 4)}
+              for k, v in prof.items() if v[0]}
+    tile = ms.tile_size(ms.MSORT_INT32, ms.MSORT_NONE)
+    ntiles = (n + tile - 1) // tile
+    passes = (ntiles - 1).bit_length()
+    # whole-step roofline: bytes of every executed pass at HBM rate (+ NVLink)
+    step_bytes = (passes + 1) * alg_bytes
+    t_roof = step_bytes / (peak * 1e9)
+    if world > 1:
+        t_roof += n * wk * (world - 1) / world / 770e9 + alg_bytes * 3 / (peak * 1e9)
+
+    clocks = sampler.summary(t0, t1)
+
+    # end to end through the public API: pinned host input -> sort -> pinned host output
+    e2e = None
+    if not args.no_e2e:
+        h_in = kin.cpu().pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        d_in = torch.empty_like(kin)
+        ke = max(3, min(args.steps, 10))
+
+        def e2e_step():
+            d_in.copy_(h_in, non_blocking=True)
+            if world == 1:
+                ms.msort_sort_out(d_in, kout, ws=ws, stream=stream)
+            else:
+                ms.msort_sort_distributed_out(d_in, kout, comm, ws=ws, stream=stream)
+            h_out.copy_(kout, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(ke):
+            e2e_step()
+        f1.record(stream)
+        barrier()
+        te = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        ok &= bool(np.all(h_out.numpy()[1:] >= h_out.numpy()[:-1]))
+        e2e = {"value": world * n * ke / (te / 1e3), "unit": "keys/s",
+               "h2d_bytes_per_step": n * wk, "d2h_bytes_per_step": n * wk,
+               "ms_per_step": te / ke, "steps": ke,
+               "path": "pinned host -> cudaMemcpyAsync -> msort_sort_out_ws -> pinned host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(1 << 24, 3)
+
+    if rank == 0:
+        value = world * n * args.steps / (ms_total / 1e3)
+        line = {
+            "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": "C5: 2^28 int32 keys per GPU, uniform [0,2^31), "
+                                   "counter-mode SplitMix64 seed 4+rank"
+                                   + ("" if world == 1 else "; distributed, globally sorted"),
+                       "n_per_gpu": n, "key_dtype": "int32", "payload": None,
+                       "tile": tile, "merge_passes": passes,
+                       "l2": "inputs larger than L2 (1 GiB/GPU vs 126 MB); no flush; "
+                             "out-of-place sort from the pristine input each step",
+                       "parallelism": f"dp{world}" if world > 1 else "single"},
+            "roofline": roof,
+            "step_roofline": {"bytes_per_gpu": step_bytes, "t_roof_ms": t_roof * 1e3,
+                              "frac": round(t_roof * 1e3 / ms_step, 4),
+                              "floor_frac": round(2 * n * wk / (peak * 1e9) * 1e3 / ms_step, 4)},
+            "phases": phases,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "verified": ok,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

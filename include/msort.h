@@ -101,6 +101,16 @@ msort_status msort_sort_ws(void *keys, void *vals, size_t n, msort_dtype key_dty
                            msort_dtype val_dtype, void *ws, size_t ws_bytes,
                            msort_stream_t stream);
 
+/* Out-of-place form (the paper's sorts return a new array):
+ * sorts in_keys/in_vals (read only, unchanged) into keys_out/vals_out.  The
+ * input may equal the output (then it is msort_sort_ws) but must not
+ * partially overlap it.  Same workspace as msort_sort_ws; no extra HBM pass:
+ * the tile sort reads the input directly. */
+msort_status msort_sort_out_ws(const void *in_keys, const void *in_vals, void *keys_out,
+                               void *vals_out, size_t n, msort_dtype key_dtype,
+                               msort_dtype val_dtype, void *ws, size_t ws_bytes,
+                               msort_stream_t stream);
+
 /* --------------------------------------------------------------- multi GPU */
 
 /* Fill `id_out` (host, 128 bytes) with a fresh NCCL unique id.  Rank 0 calls
@@ -134,6 +144,15 @@ msort_status msort_sort_distributed_ws(void *keys, void *vals, size_t n_local,
                                        msort_dtype key_dtype, msort_dtype val_dtype,
                                        msort_comm_t comm, void *ws, size_t ws_bytes,
                                        msort_stream_t stream, int64_t *split_matrix_out);
+
+/* Out-of-place form of msort_sort_distributed_ws: the local shard is read from
+ * in_keys/in_vals (unchanged) and the rank's output slice is written to
+ * keys_out/vals_out. */
+msort_status msort_sort_distributed_out_ws(const void *in_keys, const void *in_vals,
+                                           void *keys_out, void *vals_out, size_t n_local,
+                                           msort_dtype key_dtype, msort_dtype val_dtype,
+                                           msort_comm_t comm, void *ws, size_t ws_bytes,
+                                           msort_stream_t stream, int64_t *split_matrix_out);
 
 /* Single-process emulation of the distributed sort for `world` virtual ranks
  * whose shards all live on the current device: the same kernels, the same

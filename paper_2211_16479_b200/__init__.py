@@ -34,6 +34,7 @@ _NP_DT = {np.dtype(np.int32): MSORT_INT32, np.dtype(np.uint32): MSORT_UINT32,
 
 EXPORTED = (
     "msort_sort", "msort_sort_pairs", "msort_workspace_bytes", "msort_sort_ws",
+    "msort_sort_out_ws", "msort_sort_distributed_out_ws",
     "msort_comm_unique_id", "msort_comm_init", "msort_comm_destroy", "msort_sort_distributed",
     "msort_sort_distributed_ws", "msort_sort_distributed_emulated", "msort_plan_rounds",
     "msort_plan_candidates_per_round", "msort_plan_init", "msort_plan_candidates",
@@ -50,7 +51,7 @@ class MsortError(RuntimeError):
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2211_16479_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2211_16479_b200/build.py` "
             "(there is no CPU fallback)")
     L = ctypes.CDLL(LIB_PATH)
     c = ctypes
@@ -60,6 +61,9 @@ def _load():
     L.msort_sort_pairs.argtypes = [vp, vp, sz, i32, i32, vp]
     L.msort_workspace_bytes.argtypes = [sz, i32, i32, i32, c.POINTER(c.c_size_t)]
     L.msort_sort_ws.argtypes = [vp, vp, sz, i32, i32, vp, sz, vp]
+    L.msort_sort_out_ws.argtypes = [vp, vp, vp, vp, sz, i32, i32, vp, sz, vp]
+    L.msort_sort_distributed_out_ws.argtypes = [vp, vp, vp, vp, sz, i32, i32, vp, vp, sz, vp,
+                                                i64p]
     L.msort_comm_unique_id.argtypes = [vp]
     L.msort_comm_init.argtypes = [vp, i32, i32, c.POINTER(vp)]
     L.msort_comm_destroy.argtypes = [vp]
@@ -84,6 +88,7 @@ def _load():
     L.msort_tile_size.argtypes = [i32, i32]
     L.msort_tile_size.restype = i32
     for f in ("msort_sort", "msort_sort_pairs", "msort_workspace_bytes", "msort_sort_ws",
+              "msort_sort_out_ws", "msort_sort_distributed_out_ws",
               "msort_comm_unique_id", "msort_comm_init", "msort_comm_destroy",
               "msort_sort_distributed", "msort_sort_distributed_ws",
               "msort_sort_distributed_emulated", "msort_plan_init", "msort_plan_candidates",
@@ -177,9 +182,29 @@ def msort_sort_pairs(keys: torch.Tensor, vals: torch.Tensor | None, ws: torch.Te
     return keys, vals
 
 
+def msort_sort_out(in_keys: torch.Tensor, keys_out: torch.Tensor, in_vals=None, vals_out=None,
+                   ws: torch.Tensor | None = None, stream=None):
+    """Out-of-place stable sort: in_keys (unchanged) -> keys_out."""
+    _check_tensor(in_keys, "in_keys")
+    _check_tensor(keys_out, "keys_out")
+    if keys_out.numel() != in_keys.numel() or keys_out.dtype != in_keys.dtype:
+        raise ValueError("in/out keys mismatch")
+    if (in_vals is None) != (vals_out is None):
+        raise ValueError("give both in_vals and vals_out, or neither")
+    n = in_keys.numel()
+    kd, vd = _dt(in_keys), _vdt(in_vals)
+    if ws is None:
+        ws = workspace(n, in_keys.dtype, in_vals is not None, device=in_keys.device)
+    with torch.cuda.device(in_keys.device):
+        _check(lib.msort_sort_out_ws(_ptr(in_keys), _ptr(in_vals), _ptr(keys_out), _ptr(vals_out),
+                                     n, kd, vd, _ptr(ws), ws.numel(),
+                                     ctypes.c_void_p(_stream(stream))), "msort_sort_out_ws")
+    return keys_out, vals_out
+
+
 def sort(x: torch.Tensor) -> torch.Tensor:
-    """Functional stable sort: returns a sorted copy."""
-    return msort_sort(x.clone())
+    """Functional stable sort: returns a sorted copy (input unchanged)."""
+    return msort_sort_out(x, torch.empty_like(x))[0]
 
 
 def sort_pairs(k: torch.Tensor, v: torch.Tensor):
@@ -232,6 +257,28 @@ def msort_sort_distributed(keys: torch.Tensor, comm: Comm, vals: torch.Tensor | 
             split.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "msort_sort_distributed_ws")
     split = split.reshape(comm.world + 1, comm.world)
     return (keys, vals, split) if return_split else (keys, vals)
+
+
+def msort_sort_distributed_out(in_keys: torch.Tensor, keys_out: torch.Tensor, comm: Comm,
+                               in_vals=None, vals_out=None, ws: torch.Tensor | None = None,
+                               stream=None, return_split: bool = False):
+    """Out-of-place collective sort: in_keys (unchanged) -> this rank's slice."""
+    _check_tensor(in_keys, "in_keys")
+    _check_tensor(keys_out, "keys_out")
+    n = in_keys.numel()
+    kd, vd = _dt(in_keys), _vdt(in_vals)
+    if ws is None:
+        ws = workspace(n, in_keys.dtype, in_vals is not None, world=comm.world,
+                       device=in_keys.device)
+    split = np.zeros((comm.world + 1) * comm.world, dtype=np.int64)
+    with torch.cuda.device(in_keys.device):
+        _check(lib.msort_sort_distributed_out_ws(
+            _ptr(in_keys), _ptr(in_vals), _ptr(keys_out), _ptr(vals_out), n, kd, vd, comm.handle,
+            _ptr(ws), ws.numel(), ctypes.c_void_p(_stream(stream)),
+            split.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+            "msort_sort_distributed_out_ws")
+    split = split.reshape(comm.world + 1, comm.world)
+    return (keys_out, vals_out, split) if return_split else (keys_out, vals_out)
 
 
 def msort_sort_distributed_emulated(keys: list, vals: list | None = None, stream=None):

@@ -1,6 +1,6 @@
 """Build libmsort.so (sm_100a) in-tree with nvcc; no JIT, no torch extension.
 
-    python -m paper_2211_16479_b200.build [--force]
+    python paper_2211_16479_b200/build.py [--force]
 
 Objects go to paper_2211_16479_b200/build/, the shared library to
 paper_2211_16479_b200/lib/libmsort.so (git-ignored; it travels to the GPU box

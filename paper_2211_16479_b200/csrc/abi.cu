@@ -13,8 +13,9 @@
 
 namespace msort {
 
-msort_status dist_nccl(void* keys, void* vals, size_t n, msort_dtype kd, msort_dtype vd,
-                       msort_comm_s* comm, void* ws, cudaStream_t s, int64_t* split_out);
+msort_status dist_nccl(const void* in_keys, const void* in_vals, void* keys, void* vals, size_t n,
+                       msort_dtype kd, msort_dtype vd, msort_comm_s* comm, void* ws,
+                       cudaStream_t s, int64_t* split_out);
 msort_status dist_emulated(void* const* keys, void* const* vals, const size_t* n, int world,
                            msort_dtype kd, msort_dtype vd, void* const* ws, cudaStream_t s,
                            int64_t* split_out);
@@ -193,7 +194,7 @@ static msort_status sort_alloc(void* keys, void* vals, size_t n, msort_dtype kd,
   size_t need = single_ws_bytes(n, kd, vd);
   void* ws = nullptr;
   MSORT_CUDA_TRY(cudaMallocAsync(&ws, need, s));
-  msort_status st = sort_single_dispatch(keys, vals, n, kd, vd, ws, need, s);
+  msort_status st = sort_single_dispatch(keys, vals, keys, vals, n, kd, vd, ws, need, s);
   cudaError_t e = cudaFreeAsync(ws, s);
   if (st != MSORT_SUCCESS) return st;
   if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
@@ -240,8 +241,39 @@ msort_status msort_sort_ws(void* keys, void* vals, size_t n, msort_dtype key_dty
   MSORT_TRY(check_device());
   MSORT_TRY(validate_ws(keys, vals, n, key_dtype, val_dtype, ws, ws_bytes,
                         single_ws_bytes(n, key_dtype, val_dtype)));
-  return sort_single_dispatch(keys, vals, n, key_dtype, val_dtype, ws, ws_bytes,
+  return sort_single_dispatch(keys, vals, keys, vals, n, key_dtype, val_dtype, ws, ws_bytes,
                               (cudaStream_t)stream);
+}
+
+static msort_status validate_out(const void* ik, const void* iv, void* ok, void* ov, size_t n,
+                                 msort_dtype kd, msort_dtype vd) {
+  MSORT_TRY(validate(ok, ov, n, kd, vd, false));
+  MSORT_TRY(validate(const_cast<void*>(ik), const_cast<void*>(iv), n, kd, vd, false));
+  const size_t wk = dtype_size(kd);
+  // the input may be the output (in place) but must not partially overlap it
+  if (ik != ok && n > 0 && overlaps(ik, n * wk, ok, n * wk)) {
+    set_error("input and output keys partially overlap");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  if (vd != MSORT_NONE && iv != ov && n > 0 && overlaps(iv, n * 4, ov, n * 4)) {
+    set_error("input and output vals partially overlap");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  return MSORT_SUCCESS;
+}
+
+msort_status msort_sort_out_ws(const void* in_keys, const void* in_vals, void* keys_out,
+                               void* vals_out, size_t n, msort_dtype key_dtype,
+                               msort_dtype val_dtype, void* ws, size_t ws_bytes,
+                               msort_stream_t stream) {
+  MSORT_TRY(validate_out(in_keys, in_vals, keys_out, vals_out, n, key_dtype, val_dtype));
+  if (n == 0) return MSORT_SUCCESS;
+  MSORT_TRY(check_device());
+  if (n >= 2)
+    MSORT_TRY(validate_ws(keys_out, vals_out, n, key_dtype, val_dtype, ws, ws_bytes,
+                          single_ws_bytes(n, key_dtype, val_dtype)));
+  return sort_single_dispatch(in_keys, in_vals, keys_out, vals_out, n, key_dtype, val_dtype, ws,
+                              ws_bytes, (cudaStream_t)stream);
 }
 
 msort_status msort_comm_unique_id(void* id_out) {
@@ -277,8 +309,30 @@ msort_status msort_sort_distributed_ws(void* keys, void* vals, size_t n_local,
   const int world = comm_world(comm);
   MSORT_TRY(validate_ws(keys, vals, n_local, key_dtype, val_dtype, ws, ws_bytes,
                         dist_ws_bytes(n_local, key_dtype, val_dtype, world)));
-  return dist_nccl(keys, vals, n_local, key_dtype, val_dtype, comm, ws, (cudaStream_t)stream,
-                   split_matrix_out);
+  return dist_nccl(keys, vals, keys, vals, n_local, key_dtype, val_dtype, comm, ws,
+                   (cudaStream_t)stream, split_matrix_out);
+}
+
+msort_status msort_sort_distributed_out_ws(const void* in_keys, const void* in_vals,
+                                           void* keys_out, void* vals_out, size_t n_local,
+                                           msort_dtype key_dtype, msort_dtype val_dtype,
+                                           msort_comm_t comm, void* ws, size_t ws_bytes,
+                                           msort_stream_t stream, int64_t* split_matrix_out) {
+  if (!comm) {
+    set_error("comm is NULL");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  MSORT_TRY(validate_out(in_keys, in_vals, keys_out, vals_out, n_local, key_dtype, val_dtype));
+  MSORT_TRY(check_device());
+  const int world = comm_world(comm);
+  MSORT_TRY(validate_ws(keys_out, vals_out, n_local, key_dtype, val_dtype, ws, ws_bytes,
+                        dist_ws_bytes(n_local, key_dtype, val_dtype, world)));
+  if (overlaps(ws, ws_bytes, in_keys, n_local * dtype_size(key_dtype))) {
+    set_error("workspace overlaps the input");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  return dist_nccl(in_keys, in_vals, keys_out, vals_out, n_local, key_dtype, val_dtype, comm, ws,
+                   (cudaStream_t)stream, split_matrix_out);
 }
 
 msort_status msort_sort_distributed(void* keys, void* vals, size_t n_local,
@@ -295,7 +349,7 @@ msort_status msort_sort_distributed(void* keys, void* vals, size_t n_local,
   size_t need = dist_ws_bytes(n_local, key_dtype, val_dtype, comm_world(comm));
   void* ws = nullptr;
   MSORT_CUDA_TRY(cudaMallocAsync(&ws, need, s));
-  msort_status st = dist_nccl(keys, vals, n_local, key_dtype, val_dtype, comm, ws, s,
+  msort_status st = dist_nccl(keys, vals, keys, vals, n_local, key_dtype, val_dtype, comm, ws, s,
                               split_matrix_out);
   cudaError_t e = cudaFreeAsync(ws, s);
   if (st != MSORT_SUCCESS) return st;

@@ -63,9 +63,11 @@ size_t single_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd);
 constexpr int kCandidates = 256;  // candidates per boundary per round (8 bits)
 size_t dist_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd, int world);
 
-// Single-GPU sort with explicit workspace (sort_single.cu).
-msort_status sort_single_dispatch(void* keys, void* vals, size_t n, msort_dtype kd,
-                                  msort_dtype vd, void* ws, size_t ws_bytes, cudaStream_t s);
+// Single-GPU sort with explicit workspace (sort_single.cu): sorts in_keys/
+// in_vals into keys/vals (the same pointers for an in-place sort).
+msort_status sort_single_dispatch(const void* in_keys, const void* in_vals, void* keys,
+                                  void* vals, size_t n, msort_dtype kd, msort_dtype vd, void* ws,
+                                  size_t ws_bytes, cudaStream_t s);
 
 // Stable merge of `runs` consecutive sorted runs (run r = [off[r], off[r+1]) of
 // src) into dst, ties to the lower run; used by the distributed k-way merge.

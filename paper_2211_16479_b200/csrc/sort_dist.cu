@@ -172,6 +172,7 @@ static DistWs carve(void* ws, size_t n, msort_dtype kd, msort_dtype vd, int worl
   const bool pairs = vd != MSORT_NONE;
   d.sort_ws = w;
   d.sort_ws_bytes = single_ws_bytes(n, kd, vd);
+  if (world <= 1) return d;  // one rank: the local sort is the whole job
   w += align_up(d.sort_ws_bytes, 256);
   d.rk = w;
   w += align_up(n * wk, 256);
@@ -189,6 +190,7 @@ static DistWs carve(void* ws, size_t n, msort_dtype kd, msort_dtype vd, int worl
 }
 
 size_t dist_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd, int world) {
+  if (world <= 1) return single_ws_bytes(n, kd, vd);
   size_t b = align_up(single_ws_bytes(n, kd, vd), 256);
   b += align_up(n * dtype_size(kd), 256);
   if (vd != MSORT_NONE) b += align_up(n * 4, 256);
@@ -198,7 +200,9 @@ size_t dist_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd, int world) {
 
 // ------------------------------------------------------------ the driver
 struct RankIO {
-  void* keys;
+  const void* in_keys;  // input shard (== keys for the in-place call)
+  const void* in_vals;
+  void* keys;  // output shard
   void* vals;
   size_t n;
   DistWs ws;
@@ -348,9 +352,8 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
   const int nb = p - 1;
   // D1: local sorts
   for (int l = 0; l < nloc; ++l)
-    if (io[l].n >= 2)
-      MSORT_TRY(sort_single_dispatch(io[l].keys, io[l].vals, io[l].n, kd, vd, io[l].ws.sort_ws,
-                                     io[l].ws.sort_ws_bytes, s));
+    MSORT_TRY(sort_single_dispatch(io[l].in_keys, io[l].in_vals, io[l].keys, io[l].vals, io[l].n,
+                                   kd, vd, io[l].ws.sort_ws, io[l].ws.sort_ws_bytes, s));
   std::vector<int64_t> S((size_t)(p + 1) * p);
   if (p == 1) {
     S[0] = 0, S[1] = (int64_t)io[0].n;
@@ -437,13 +440,16 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
   return MSORT_SUCCESS;
 }
 
-msort_status dist_nccl(void* keys, void* vals, size_t n, msort_dtype kd, msort_dtype vd,
-                       msort_comm_s* comm, void* ws, cudaStream_t s, int64_t* split_out) {
+msort_status dist_nccl(const void* in_keys, const void* in_vals, void* keys, void* vals, size_t n,
+                       msort_dtype kd, msort_dtype vd, msort_comm_s* comm, void* ws,
+                       cudaStream_t s, int64_t* split_out) {
   if (comm->world > kMaxWorld) {
     set_error("world too large");
     return MSORT_ERROR_NOT_SUPPORTED;
   }
-  RankIO io{keys, vd == MSORT_NONE ? nullptr : vals, n, carve(ws, n, kd, vd, comm->world)};
+  const bool pv = vd != MSORT_NONE;
+  RankIO io{in_keys, pv ? in_vals : nullptr, keys, pv ? vals : nullptr, n,
+            carve(ws, n, kd, vd, comm->world)};
   NcclColl C{comm, s};
   return dist_run(C, &io, 1, kd, vd, s, split_out);
 }
@@ -457,8 +463,10 @@ msort_status dist_emulated(void* const* keys, void* const* vals, const size_t* n
   }
   std::vector<RankIO> io(world);
   for (int r = 0; r < world; ++r)
-    io[r] = RankIO{keys[r], vd == MSORT_NONE || !vals ? nullptr : vals[r], n[r],
-                   carve(ws[r], n[r], kd, vd, world)};
+  {
+    void* v = vd == MSORT_NONE || !vals ? nullptr : vals[r];
+    io[r] = RankIO{keys[r], v, keys[r], v, n[r], carve(ws[r], n[r], kd, vd, world)};
+  }
   EmulColl C{world, s};
   return dist_run(C, io.data(), world, kd, vd, s, split_out);
 }

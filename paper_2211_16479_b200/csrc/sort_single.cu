@@ -241,9 +241,19 @@ struct Kernels {
     return MSORT_SUCCESS;
   }
 
-  static msort_status sort(K* keys, uint32_t* vals, size_t n, void* ws, size_t ws_bytes,
-                           cudaStream_t s) {
+  // Sort in_k/in_v into out_k/out_v (in == out: in place; K1 reads a whole
+  // tile into shared memory before writing it back, so that is safe).
+  static msort_status sort(const K* in_k, const uint32_t* in_v, K* keys, uint32_t* vals,
+                           size_t n, void* ws, size_t ws_bytes, cudaStream_t s) {
     MSORT_TRY(init());
+    if (n < 2) {
+      if (n == 1 && in_k != keys) {
+        MSORT_CUDA_TRY(cudaMemcpyAsync(keys, in_k, sizeof(K), cudaMemcpyDeviceToDevice, s));
+        if (PAIRS)
+          MSORT_CUDA_TRY(cudaMemcpyAsync(vals, in_v, 4, cudaMemcpyDeviceToDevice, s));
+      }
+      return MSORT_SUCCESS;
+    }
     const int64_t ntiles = (int64_t)((n + T - 1) / T);
     int passes = 0;
     while ((int64_t(1) << passes) < ntiles) ++passes;
@@ -264,7 +274,7 @@ struct Kernels {
     {
       LaunchScope ls(KC_TILE_SORT, s);
       k1_tile_sort<K, PAIRS, NT, VT>
-          <<<(unsigned)ntiles, NT, k1_smem, s>>>(keys, vals, bk[cur], bv[cur], (int64_t)n);
+          <<<(unsigned)ntiles, NT, k1_smem, s>>>(in_k, in_v, bk[cur], bv[cur], (int64_t)n);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
     for (int64_t L = T; L < (int64_t)n; L *= 2) {
@@ -340,21 +350,23 @@ struct Kernels {
 };
 
 template <class K>
-static msort_status sort_k(void* keys, void* vals, size_t n, void* ws, size_t ws_bytes,
-                           cudaStream_t s) {
+static msort_status sort_k(const void* ik, const void* iv, void* keys, void* vals, size_t n,
+                           void* ws, size_t ws_bytes, cudaStream_t s) {
   if (vals)
-    return Kernels<K, true>::sort((K*)keys, (uint32_t*)vals, n, ws, ws_bytes, s);
-  return Kernels<K, false>::sort((K*)keys, nullptr, n, ws, ws_bytes, s);
+    return Kernels<K, true>::sort((const K*)ik, (const uint32_t*)iv, (K*)keys, (uint32_t*)vals,
+                                  n, ws, ws_bytes, s);
+  return Kernels<K, false>::sort((const K*)ik, nullptr, (K*)keys, nullptr, n, ws, ws_bytes, s);
 }
 
-msort_status sort_single_dispatch(void* keys, void* vals, size_t n, msort_dtype kd,
-                                  msort_dtype vd, void* ws, size_t ws_bytes, cudaStream_t s) {
-  if (vd == MSORT_NONE) vals = nullptr;
+msort_status sort_single_dispatch(const void* in_keys, const void* in_vals, void* keys,
+                                  void* vals, size_t n, msort_dtype kd, msort_dtype vd, void* ws,
+                                  size_t ws_bytes, cudaStream_t s) {
+  if (vd == MSORT_NONE) vals = nullptr, in_vals = nullptr;
   switch (kd) {
-    case MSORT_INT32: return sort_k<int32_t>(keys, vals, n, ws, ws_bytes, s);
-    case MSORT_UINT32: return sort_k<uint32_t>(keys, vals, n, ws, ws_bytes, s);
-    case MSORT_INT64: return sort_k<int64_t>(keys, vals, n, ws, ws_bytes, s);
-    case MSORT_UINT64: return sort_k<uint64_t>(keys, vals, n, ws, ws_bytes, s);
+    case MSORT_INT32: return sort_k<int32_t>(in_keys, in_vals, keys, vals, n, ws, ws_bytes, s);
+    case MSORT_UINT32: return sort_k<uint32_t>(in_keys, in_vals, keys, vals, n, ws, ws_bytes, s);
+    case MSORT_INT64: return sort_k<int64_t>(in_keys, in_vals, keys, vals, n, ws, ws_bytes, s);
+    case MSORT_UINT64: return sort_k<uint64_t>(in_keys, in_vals, keys, vals, n, ws, ws_bytes, s);
     default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
   }
 }

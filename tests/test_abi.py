@@ -16,9 +16,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def ms():
-    from paper_2211_16479_b200.build import build
+    import __graft_entry__
 
-    build()
+    __graft_entry__.build()
     import paper_2211_16479_b200 as m
 
     return m
