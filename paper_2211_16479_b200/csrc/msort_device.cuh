@@ -89,27 +89,140 @@ __device__ __forceinline__ int64_t merge_path_global(const K* __restrict__ a, in
 // buffer s; `pos` records the source position of each output (for payload
 // gathers) when TRACK, and `src_idx` (if non-null) maps a position to an
 // original index carried from an earlier merge round.
+// Branch-free: one shared load per output, at a clamped index (<= lim), so
+// the caller only guarantees that s[0..lim] is addressable.
 template <class K, bool PAD, bool TRACK, int VT>
 __device__ __forceinline__ void serial_merge(const K* s, const int* src_idx, int ai, int aend,
-                                             int bi, int bend, K (&key)[VT], int (&pos)[VT]) {
-  K ak = ai < aend ? s[sidx<K, PAD>(ai)] : K(0);
-  K bk = bi < bend ? s[sidx<K, PAD>(bi)] : K(0);
+                                             int bi, int bend, int lim, K (&key)[VT],
+                                             int (&pos)[VT]) {
+  K ak = s[sidx<K, PAD>(min(ai, lim))];
+  K bk = s[sidx<K, PAD>(min(bi, lim))];
 #pragma unroll
   for (int k = 0; k < VT; ++k) {
-    bool takeB = (bi < bend) && ((ai >= aend) || (bk < ak));
+    const bool takeB = (bi < bend) && ((ai >= aend) || (bk < ak));
     key[k] = takeB ? bk : ak;
     if constexpr (TRACK) {
       int p = takeB ? bi : ai;
       pos[k] = src_idx ? src_idx[sidx<K, PAD>(p)] : p;
     }
-    if (takeB) {
-      ++bi;
-      if (bi < bend) bk = s[sidx<K, PAD>(bi)];
-    } else {
-      ++ai;
-      if (ai < aend) ak = s[sidx<K, PAD>(ai)];
+    ai += takeB ? 0 : 1;
+    bi += takeB ? 1 : 0;
+    if (k + 1 < VT) {
+      const K nv = s[sidx<K, PAD>(min(takeB ? bi : ai, lim))];
+      ak = takeB ? ak : nv;
+      bk = takeB ? nv : bk;
     }
   }
+}
+
+// ------------------------------------------- mbarrier + 1-D bulk copy (TMA)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// Global -> shared bulk copy (cp.async.bulk, SASS UBLKCP); dst/src 16-byte
+// aligned, bytes a multiple of 16; completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Shared -> global bulk copy (SASS UBLKCP); completion tracked per issuing
+// thread by bulk groups.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {  // sources of all but N groups read
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// Make this thread's generic-proxy shared-memory writes visible to the async
+// proxy (the bulk store engine).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// A window src[0, cnt) splits into a <16-byte head, a 16-byte aligned
+// interior (moved by one bulk copy) and a <16-byte tail (plain loads).
+template <class T>
+__device__ __forceinline__ void window_split(const T* src, int cnt, int& head, int& mid) {
+  const uintptr_t a = (uintptr_t)src;
+  const uintptr_t e = a + (uintptr_t)cnt * sizeof(T);
+  uintptr_t ia = (a + 15) & ~(uintptr_t)15;
+  uintptr_t ie = e & ~(uintptr_t)15;
+  if (ie < ia) ie = ia = e;  // too small for an aligned interior
+  head = (int)((ia - a) / sizeof(T));
+  mid = (int)((ie - ia) / sizeof(T));
+}
+template <class T>
+__device__ __forceinline__ uint32_t window_bulk_bytes(const T* src, int cnt) {
+  int head, mid;
+  window_split(src, cnt, head, mid);
+  return (uint32_t)mid * sizeof(T);
+}
+// Stage src[0, cnt) into shared memory at dst (same 16-byte phase as src, see
+// stage_offset): the leader issues the bulk copy of the interior (after it
+// armed `bar` with the expected bytes), every thread helps with head/tail.
+template <class T>
+__device__ __forceinline__ void stage_window(T* dst, const T* src, int cnt, uint64_t* bar,
+                                             bool leader, int tid, int nthreads) {
+  int head, mid;
+  window_split(src, cnt, head, mid);
+  const int tail = cnt - head - mid;
+  if (leader && mid > 0) bulk_g2s(dst + head, src + head, (uint32_t)(mid * sizeof(T)), bar);
+  for (int i = tid; i < head + tail; i += nthreads) {
+    int j = i < head ? i : head + mid + (i - head);
+    dst[j] = src[j];
+  }
+}
+// Element offset (0..16/sizeof(T)-1) at which to place a window starting at
+// src so that shared and global addresses share the same 16-byte phase.
+template <class T>
+__device__ __forceinline__ int stage_offset(const T* src) {
+  return (int)(((uintptr_t)src & 15) / sizeof(T));
 }
 
 // ------------------------------------------------------ register networks
@@ -123,21 +236,37 @@ __device__ __forceinline__ void cmp_swap(K& a, K& b) {
 
 // Batcher's odd-even merge sort network over N (power of two) registers.
 // Keys only: equal integers are indistinguishable, so any network is fine.
-template <int N, class K>
+// Sorts the first P (a power of two) of the N registers x.
+template <int P, int N, class K>
 __device__ __forceinline__ void batcher_sort(K (&x)[N]) {
+  static_assert(P <= N, "batcher_sort: P <= N");
 #pragma unroll
-  for (int p = 1; p < N; p <<= 1) {
+  for (int p = 1; p < P; p <<= 1) {
 #pragma unroll
     for (int k = p; k >= 1; k >>= 1) {
 #pragma unroll
-      for (int j = k % p; j + k < N; j += 2 * k) {
+      for (int j = k % p; j + k < P; j += 2 * k) {
 #pragma unroll
         for (int i = 0; i < k; ++i) {
-          if (i + j + k < N && (i + j) / (2 * p) == (i + j + k) / (2 * p))
+          if (i + j + k < P && (i + j) / (2 * p) == (i + j + k) / (2 * p))
             cmp_swap(x[i + j], x[i + j + k]);
         }
       }
     }
+  }
+}
+
+// Keys-only network for any N: Batcher on the largest power of two P <= N,
+// then each remaining element is inserted by a compare-exchange chain.
+template <int N, class K>
+__device__ __forceinline__ void keys_network(K (&x)[N]) {
+  constexpr int P = N >= 16 ? 16 : (N >= 8 ? 8 : (N >= 4 ? 4 : (N >= 2 ? 2 : 1)));
+  static_assert(N < 32, "keys_network: N < 32");
+  batcher_sort<P>(x);
+#pragma unroll
+  for (int m = P; m < N; ++m) {
+#pragma unroll
+    for (int i = m - 1; i >= 0; --i) cmp_swap(x[i], x[i + 1]);
   }
 }
 

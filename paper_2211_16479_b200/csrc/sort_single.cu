@@ -1,15 +1,19 @@
 // sort_single.cu -- single-GPU stable merge sort for sm_100a.
 //
-//   K1 k1_tile_sort     : each T-element tile sorted in registers + shared
-//                         memory (the base case of the recursion, P:77-84;
-//                         the chunk sort of the multiprocessing variant,
-//                         P:270-285; `SMALLEST_ARRAY_SIZE` of P:121 = T).
-//   K2 k2_partition     : merge-path co-rank of every output tile's first
-//                         diagonal inside its run pair (global binary search).
-//   K3 k3_merge_pass    : merges run pairs of length L into 2L (merge()),
-//                         one output tile per CTA, staged through shared memory.
-//   S4 placement        : K1's destination is picked from the parity of the
-//                         merge-pass count so that the last pass lands in keys.
+//   K1 k1_tile_sort   : each T-element tile sorted in registers + shared
+//                       memory: the base case of the recursion, the
+//                       chunk sort of the multiprocessing variant;
+//                       T plays `SMALLEST_ARRAY_SIZE` (reading R17).
+//   K3 k3_merge_pass  : one persistent, warp-specialised kernel per merge
+//                       level: merges run pairs of length L into 2L with the
+//                       stable merge() of P:107 (ties to the left run, R1).
+//                       Warp 0 stages windows with TMA bulk copies
+//                       (cp.async.bulk + mbarrier), warp 1 computes the
+//                       merge-path co-ranks (K2) of the CTA's tiles ahead of
+//                       use, warps 2.. merge from shared memory and write
+//                       through a shared buffer with TMA bulk stores.
+//   S4 placement      : K1's destination is picked from the parity of the
+//                       merge-pass count so that the last pass lands in keys.
 //
 // "P:n" = /root/reference/PAPER.md line n.
 #include <algorithm>
@@ -56,16 +60,17 @@ struct ExplicitPairs {  // arbitrary consecutive runs, pairs (2m, 2m+1)
 };
 
 // ----------------------------------------------------------------- K1
+// NT threads x VT items (VT odd: "blocked" shared accesses at stride VT are
+// bank-conflict free without padding).
 template <class K, bool PAIRS, int NT, int VT>
 __global__ void __launch_bounds__(NT)
     k1_tile_sort(const K* __restrict__ in_k, const uint32_t* __restrict__ in_v,
                  K* __restrict__ out_k, uint32_t* __restrict__ out_v, int64_t n) {
   constexpr int T = NT * VT;
-  constexpr int TP = padded_len<K, T>();
   extern __shared__ __align__(16) unsigned char smem[];
-  K* sk = reinterpret_cast<K*>(smem);
-  int* si = reinterpret_cast<int*>(sk + TP);      // PAIRS: original in-tile index
-  uint32_t* sv = reinterpret_cast<uint32_t*>(si + TP);  // PAIRS: payload staging
+  K* sk = reinterpret_cast<K*>(smem);                 // T keys
+  int* si = reinterpret_cast<int*>(sk + T);           // PAIRS: original in-tile index
+  uint32_t* sv = reinterpret_cast<uint32_t*>(si + T);  // PAIRS: payload staging
 
   const int tid = threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * T;
@@ -75,7 +80,7 @@ __global__ void __launch_bounds__(NT)
   // real elements, so the stable order keeps real keys first.
 #pragma unroll 4
   for (int i = tid; i < T; i += NT) {
-    sk[sidx<K, true>(i)] = i < cnt ? in_k[base + i] : KeyTraits<K>::max_key();
+    sk[i] = i < cnt ? in_k[base + i] : KeyTraits<K>::max_key();
     if constexpr (PAIRS) {
       if (i < cnt) sv[i] = in_v[base + i];
     }
@@ -86,12 +91,12 @@ __global__ void __launch_bounds__(NT)
   int idx[VT];
 #pragma unroll
   for (int k = 0; k < VT; ++k) {
-    key[k] = sk[sidx<K, true>(tid * VT + k)];
+    key[k] = sk[tid * VT + k];
     idx[k] = tid * VT + k;
   }
   // Per-thread register network.
   if constexpr (PAIRS) odd_even_transposition_sort<VT>(key, idx);
-  else batcher_sort<VT>(key);
+  else keys_network<VT>(key);
 
   // In-block merge rounds: runs of w -> 2w, merge path per thread.
 #pragma unroll 1
@@ -99,143 +104,284 @@ __global__ void __launch_bounds__(NT)
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < VT; ++k) {
-      sk[sidx<K, true>(tid * VT + k)] = key[k];
-      if constexpr (PAIRS) si[sidx<K, true>(tid * VT + k)] = idx[k];
+      sk[tid * VT + k] = key[k];
+      if constexpr (PAIRS) si[tid * VT + k] = idx[k];
     }
     __syncthreads();
     const int tpg = 2 * w / VT;  // threads per merge group
     const int g0 = (tid / tpg) * 2 * w;
     const int d = (tid % tpg) * VT;
-    int i = merge_path<K, true>(sk, g0, w, g0 + w, w, d);
-    serial_merge<K, true, PAIRS, VT>(sk, PAIRS ? si : nullptr, g0 + i, g0 + w, g0 + w + d - i,
-                                     g0 + 2 * w, key, idx);
+    int i = merge_path<K, false>(sk, g0, w, g0 + w, w, d);
+    serial_merge<K, false, PAIRS, VT>(sk, PAIRS ? si : nullptr, g0 + i, g0 + w, g0 + w + d - i,
+                                      g0 + 2 * w, T - 1, key, idx);
   }
 
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < VT; ++k) {
-    sk[sidx<K, true>(tid * VT + k)] = key[k];
-    if constexpr (PAIRS) si[sidx<K, true>(tid * VT + k)] = idx[k];
+    sk[tid * VT + k] = key[k];
+    if constexpr (PAIRS) si[tid * VT + k] = idx[k];
   }
   __syncthreads();
 #pragma unroll 4
   for (int i = tid; i < cnt; i += NT) {
-    out_k[base + i] = sk[sidx<K, true>(i)];
-    if constexpr (PAIRS) out_v[base + i] = sv[si[sidx<K, true>(i)]];
+    out_k[base + i] = sk[i];
+    if constexpr (PAIRS) out_v[base + i] = sv[si[i]];
   }
-}
-
-// ----------------------------------------------------------------- K2
-template <class K, class PM>
-__global__ void __launch_bounds__(256)
-    k2_partition(const K* __restrict__ src, PM pm, int64_t ntiles, int T,
-                 int64_t* __restrict__ part) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= ntiles) return;
-  int64_t A0, na, nb, dl;
-  pm.locate(q, T, A0, na, nb, dl);
-  part[q] = merge_path_global(src + A0, na, src + A0 + na, nb, dl);
 }
 
 // ----------------------------------------------------------------- K3
-template <class K, bool PAIRS, int NT, int VT, class PM>
-__global__ void __launch_bounds__(NT)
+struct TileMeta {
+  int64_t out;  // global output index of the tile's first element
+  int na, nb, offA, offB, offAv, offBv, tot, pad;
+};
+
+constexpr size_t align_up_c(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+template <class K, bool PAIRS, int NC, int VT, int S, int OB>
+struct K3Layout {
+  static constexpr int Tm = NC * VT;
+  static constexpr int EK = 16 / sizeof(K);
+  static constexpr int R = 4;                    // split ring: R batches of 32
+  static constexpr int SKE = Tm + 4 * EK;        // staged keys per stage
+  static constexpr int SVE = Tm + 16;            // staged vals per stage
+  static constexpr size_t bars = 0;              // full[S], empty[S], sfull[R], sempty[R]
+  static constexpr size_t meta = 128;
+  static constexpr size_t ring = meta + 48 * S;
+  static constexpr size_t stage_k = align_up_c(ring + 8 * 32 * R, 128);
+  static constexpr size_t stage_v = align_up_c(stage_k + (size_t)S * SKE * sizeof(K), 128);
+  static constexpr int OBK = Tm + 2 * EK;  // output tile + 16-byte phase slack
+  static constexpr int OBV = Tm + 8;
+  static constexpr size_t out_k =
+      align_up_c(stage_v + (PAIRS ? (size_t)S * SVE * 4 : 0), 128);
+  static constexpr size_t out_v = align_up_c(out_k + (size_t)OB * OBK * sizeof(K), 128);
+  static constexpr size_t bytes = align_up_c(out_v + (PAIRS ? (size_t)OB * OBV * 4 : 0), 128);
+};
+
+// Persistent merge pass.  CTA c owns the contiguous tiles [t0, t1); warp 0
+// = TMA producer, warp 1 = co-rank searcher, warps 2..2+NC/32 = mergers.
+template <class K, bool PAIRS, int NC, int VT, int S, int OB, class PM>
+__global__ void __launch_bounds__(NC + 64)
     k3_merge_pass(const K* __restrict__ src_k, const uint32_t* __restrict__ src_v,
-                  K* __restrict__ dst_k, uint32_t* __restrict__ dst_v, PM pm,
-                  const int64_t* __restrict__ part) {
-  constexpr int T = NT * VT;
-  constexpr int TP = padded_len<K, T>();
+                  K* __restrict__ dst_k, uint32_t* __restrict__ dst_v, PM pm, int64_t ntiles) {
+  using LY = K3Layout<K, PAIRS, NC, VT, S, OB>;
+  constexpr int Tm = LY::Tm, EK = LY::EK, R = LY::R;
   extern __shared__ __align__(16) unsigned char smem[];
-  K* sin = reinterpret_cast<K*>(smem);              // staged A|B window (T)
-  K* sout = sin + T;                                // padded output (TP)
-  int* spos = reinterpret_cast<int*>(sout + TP);    // PAIRS: source position
-  uint32_t* sv = reinterpret_cast<uint32_t*>(spos + TP);  // PAIRS: staged payload
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + LY::bars);
+  uint64_t* empty = full + S;
+  uint64_t* sfull = empty + S;
+  uint64_t* sempty = sfull + R;
+  TileMeta* meta = reinterpret_cast<TileMeta*>(smem + LY::meta);
+  int64_t* ring = reinterpret_cast<int64_t*>(smem + LY::ring);
+  K* stk = reinterpret_cast<K*>(smem + LY::stage_k);
+  uint32_t* stv = reinterpret_cast<uint32_t*>(smem + LY::stage_v);
+  K* obk = reinterpret_cast<K*>(smem + LY::out_k);
+  uint32_t* obv = reinterpret_cast<uint32_t*>(smem + LY::out_v);
 
-  const int tid = threadIdx.x;
-  const int64_t q = blockIdx.x;
-  int64_t A0, na_all, nb_all, d0;
-  pm.locate(q, T, A0, na_all, nb_all, d0);
-  const int64_t tot_all = na_all + nb_all;
-  const int64_t d1 = min(d0 + T, tot_all);
-  const int64_t i0 = part[q];
-  const int64_t i1 = d1 == tot_all ? na_all : part[q + 1];
-  const int64_t j0 = d0 - i0, j1 = d1 - i1;
-  const int na = (int)(i1 - i0), nb = (int)(j1 - j0), tot = na + nb;
-  const K* a = src_k + A0 + i0;
-  const K* b = src_k + A0 + na_all + j0;
-
-#pragma unroll 4
-  for (int i = tid; i < tot; i += NT) {
-    sin[i] = i < na ? a[i] : b[i - na];
-    if constexpr (PAIRS) sv[i] = i < na ? src_v[A0 + i0 + i] : src_v[A0 + na_all + j0 + i - na];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // contiguous tile range of this CTA
+  const int64_t G = gridDim.x, per = ntiles / G, rem = ntiles % G, c = blockIdx.x;
+  const int64_t t0 = c * per + min(c, rem);
+  const int64_t cnt = per + (c < rem ? 1 : 0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 32), mbar_init(&empty[s], NC / 32);
+    for (int r = 0; r < R; ++r) mbar_init(&sfull[r], 32), mbar_init(&sempty[r], 1);
+    fence_mbar_init();
   }
   __syncthreads();
+  if (cnt == 0) return;
+  const int64_t nsplit = cnt + 1;  // co-ranks of local diagonals 0..cnt
+  const int64_t nbatch = (nsplit + 31) / 32;
 
-  K key[VT];
-  int pos[VT];
-  const int d = tid * VT;
-  if (d < tot) {
-    int i = merge_path<K, false>(sin, 0, na, na, nb, d);
-    serial_merge<K, false, PAIRS, VT>(sin, nullptr, i, na, na + d - i, tot, key, pos);
-  }
-#pragma unroll
-  for (int k = 0; k < VT; ++k) {
-    if (d + k < tot) {
-      sout[sidx<K, true>(d + k)] = key[k];
-      if constexpr (PAIRS) spos[sidx<K, true>(d + k)] = pos[k];
+  if (warp == 1) {
+    // ------------------------------------------------ co-rank searcher (K2)
+    for (int64_t b = 0; b < nbatch; ++b) {
+      const int r = (int)(b % R);
+      const uint32_t u = (uint32_t)(b / R);
+      mbar_wait(&sempty[r], (u & 1) ^ 1);
+      const int64_t j = b * 32 + lane;
+      int64_t v = 0;
+      if (j < nsplit && t0 + j < ntiles) {
+        int64_t A0, na, nb, dl;
+        pm.locate(t0 + j, Tm, A0, na, nb, dl);
+        v = merge_path_global(src_k + A0, na, src_k + A0 + na, nb, dl);
+      }
+      ring[r * 32 + lane] = v;
+      mbar_arrive(&sfull[r]);
     }
-  }
-  __syncthreads();
-  K* out = dst_k + A0 + d0;
-#pragma unroll 4
-  for (int i = tid; i < tot; i += NT) {
-    out[i] = sout[sidx<K, true>(i)];
-    if constexpr (PAIRS) dst_v[A0 + d0 + i] = sv[spos[sidx<K, true>(i)]];
+  } else if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    for (int64_t k = 0; k < cnt; ++k) {
+      const int64_t q = t0 + k;
+      const int s = (int)(k % S);
+      // co-ranks of diagonals k and k+1 (local), possibly in two batches
+      const int64_t b0 = k / 32, b1 = (k + 1) / 32;
+      mbar_wait(&sfull[b0 % R], (uint32_t)((b0 / R) & 1));
+      if (b1 != b0 && b1 < nbatch) mbar_wait(&sfull[b1 % R], (uint32_t)((b1 / R) & 1));
+      int64_t A0, na_all, nb_all, d0;
+      pm.locate(q, Tm, A0, na_all, nb_all, d0);
+      const int64_t tot_all = na_all + nb_all;
+      const int64_t d1 = min(d0 + Tm, tot_all);
+      const int64_t i0 = ring[(b0 % R) * 32 + (k % 32)];
+      const int64_t i1 = d1 == tot_all ? na_all : ring[(b1 % R) * 32 + ((k + 1) % 32)];
+      __syncwarp();
+      if (k % 32 == 31 && lane == 0) mbar_arrive(&sempty[b0 % R]);  // batch b0 consumed
+      const int64_t j0 = d0 - i0, j1 = d1 - i1;
+      const int na = (int)(i1 - i0), nb = (int)(j1 - j0);
+      const K* a = src_k + A0 + i0;
+      const K* bp = src_k + A0 + na_all + j0;
+      const int offA = stage_offset(a);
+      const int offB = (offA + na + EK - 1) / EK * EK + stage_offset(bp);
+      const uint32_t* av = nullptr;
+      const uint32_t* bv = nullptr;
+      int offAv = 0, offBv = 0;
+      if constexpr (PAIRS) {
+        av = src_v + A0 + i0;
+        bv = src_v + A0 + na_all + j0;
+        offAv = stage_offset(av);
+        offBv = (offAv + na + 3) / 4 * 4 + stage_offset(bv);
+      }
+      mbar_wait(&empty[s], (uint32_t)(((k / S) & 1) ^ 1));
+      K* sk = stk + (size_t)s * LY::SKE;
+      uint32_t* sv = stv + (size_t)s * LY::SVE;
+      if (lane == 0) {
+        meta[s] = TileMeta{A0 + d0, na, nb, offA, offB, offAv, offBv, na + nb, 0};
+        uint32_t tx = window_bulk_bytes(a, na) + window_bulk_bytes(bp, nb);
+        if constexpr (PAIRS) tx += window_bulk_bytes(av, na) + window_bulk_bytes(bv, nb);
+        mbar_expect_tx(&full[s], tx);  // before the copies that complete it
+      }
+      stage_window(sk + offA, a, na, &full[s], lane == 0, lane, 32);
+      stage_window(sk + offB, bp, nb, &full[s], lane == 0, lane, 32);
+      if constexpr (PAIRS) {
+        stage_window(sv + offAv, av, na, &full[s], lane == 0, lane, 32);
+        stage_window(sv + offBv, bv, nb, &full[s], lane == 0, lane, 32);
+      }
+      mbar_arrive(&full[s]);  // all 32 lanes: their head/tail stores are released
+    }
+  } else {
+    // ------------------------------------------------------------ mergers
+    const int ct = threadIdx.x - 64;  // 0..NC-1
+    for (int64_t k = 0; k < cnt; ++k) {
+      const int s = (int)(k % S);
+      const int ob = OB == 1 ? 0 : (int)(k % OB);
+      mbar_wait(&full[s], (uint32_t)((k / S) & 1));
+      const TileMeta m = meta[s];
+      const K* sk = stk + (size_t)s * LY::SKE;
+      const uint32_t* sv = stv + (size_t)s * LY::SVE;
+      K key[VT];
+      int pos[VT];
+      const int d = ct * VT;
+      if (d < m.tot) {
+        int i = merge_path<K, false>(sk, m.offA, m.na, m.offB, m.nb, d);
+        serial_merge<K, false, PAIRS, VT>(sk, nullptr, m.offA + i, m.offA + m.na,
+                                          m.offB + d - i, m.offB + m.nb, LY::SKE - 1, key, pos);
+      }
+      if (ct == 0) bulk_wait_read<OB - 1>();  // store from this buffer has read it
+      named_bar_sync(1, NC);                   // output buffer ob is free
+      // The output tile keeps its global 16-byte phase in shared memory so
+      // the aligned middle leaves by one bulk store (TMA, cp.async.bulk).
+      K* gk = dst_k + m.out;
+      const int phk = stage_offset(gk);
+      K* ok = obk + (size_t)ob * LY::OBK;
+      uint32_t* gv = nullptr;
+      int phv = 0;
+      uint32_t* ovb = obv + (size_t)ob * LY::OBV;
+      if constexpr (PAIRS) {
+        gv = dst_v + m.out;
+        phv = stage_offset(gv);
+      }
+#pragma unroll
+      for (int t = 0; t < VT; ++t) {
+        if (d + t < m.tot) {
+          ok[phk + d + t] = key[t];
+          if constexpr (PAIRS) {
+            const int p = pos[t];
+            ovb[phv + d + t] = sv[p < m.offB ? m.offAv + (p - m.offA) : m.offBv + (p - m.offB)];
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // stage s fully consumed
+      named_bar_sync(1, NC);                  // output tile complete in shared memory
+      int hk, mk;
+      window_split(gk, m.tot, hk, mk);
+      int hv = 0, mv = 0;
+      if constexpr (PAIRS) window_split(gv, m.tot, hv, mv);
+      if (ct == 0) {
+        if (mk) bulk_s2g(gk + hk, ok + phk + hk, (uint32_t)(mk * sizeof(K)));
+        if constexpr (PAIRS)
+          if (mv) bulk_s2g(gv + hv, ovb + phv + hv, (uint32_t)(mv * 4));
+        bulk_commit();
+      }
+      for (int i = ct; i < m.tot - mk; i += NC) {
+        const int j = i < hk ? i : i + mk;
+        gk[j] = ok[phk + j];
+      }
+      if constexpr (PAIRS)
+        for (int i = ct; i < m.tot - mv; i += NC) {
+          const int j = i < hv ? i : i + mv;
+          gv[j] = ovb[phv + j];
+        }
+    }
+    if (ct == 0) bulk_wait_all();
   }
 }
 
 // ------------------------------------------------------------ host driver
 template <class K, bool PAIRS>
 struct Kernels {
-  using G = Geometry<K, PAIRS>;
-  static constexpr int NT = G::NT, VT = G::VT, T = G::T;
-  static constexpr int TP = padded_len<K, T>();
-  static constexpr size_t k1_smem =
-      TP * sizeof(K) + (PAIRS ? TP * sizeof(int) + T * sizeof(uint32_t) : 0);
-  static constexpr size_t k3_smem =
-      (T + TP) * sizeof(K) + (PAIRS ? TP * sizeof(int) + T * sizeof(uint32_t) : 0);
+  static constexpr int VT = 17;  // odd: conflict-free blocked shared accesses
+  static constexpr int NT1 = 512;
+  static constexpr int T = NT1 * VT;  // tile sort size
+  static constexpr int NC = 256;      // merging threads per K3 CTA
+  static constexpr int Tm = NC * VT;  // merge output tile (T = 2 Tm)
+  static constexpr int S = 2;
+  static constexpr int OB = (sizeof(K) == 4 && !PAIRS) ? 2 : 1;
+  using LY = K3Layout<K, PAIRS, NC, VT, S, OB>;
+  static constexpr size_t k1_smem = (size_t)T * sizeof(K) + (PAIRS ? (size_t)T * 8 : 0);
+  static constexpr size_t k3_smem = LY::bytes;
+  static_assert(T % Tm == 0, "pair boundaries must be tile boundaries");
+
+  static int& grid3(int dev) {
+    static int g[64] = {};
+    return g[dev & 63];
+  }
 
   static msort_status init() {
-    static bool done = false;
-    static msort_status st = MSORT_SUCCESS;
-    if (done) return st;
-    cudaError_t e = cudaFuncSetAttribute(k1_tile_sort<K, PAIRS, NT, VT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)k1_smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k3_merge_pass<K, PAIRS, NT, VT, UniformPairs>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3_smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k3_merge_pass<K, PAIRS, NT, VT, ExplicitPairs>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3_smem);
-    st = e == cudaSuccess ? MSORT_SUCCESS : cuda_fail(e, "cudaFuncSetAttribute");
-    done = true;
-    return st;
+    int dev = 0;
+    MSORT_CUDA_TRY(cudaGetDevice(&dev));
+    if (grid3(dev)) return MSORT_SUCCESS;
+    MSORT_CUDA_TRY(cudaFuncSetAttribute(k1_tile_sort<K, PAIRS, NT1, VT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)k1_smem));
+    auto ku = k3_merge_pass<K, PAIRS, NC, VT, S, OB, UniformPairs>;
+    auto ke = k3_merge_pass<K, PAIRS, NC, VT, S, OB, ExplicitPairs>;
+    MSORT_CUDA_TRY(cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)k3_smem));
+    MSORT_CUDA_TRY(cudaFuncSetAttribute(ke, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)k3_smem));
+    int sms = 0, occ = 0;
+    MSORT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    MSORT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ku, NC + 64, k3_smem));
+    if (occ < 1) {
+      set_error("merge pass kernel does not fit on an SM");
+      return MSORT_ERROR_NOT_SUPPORTED;
+    }
+    grid3(dev) = sms * occ;
+    return MSORT_SUCCESS;
   }
 
   template <class PM>
   static msort_status merge_pass(const K* sk, const uint32_t* sv, K* dk, uint32_t* dv,
-                                 const PM& pm, int64_t ntiles, int64_t* part, cudaStream_t s,
-                                 KernelClass kc) {
-    {
-      LaunchScope ls(KC_PARTITION, s);
-      unsigned g = (unsigned)((ntiles + 255) / 256);
-      k2_partition<K, PM><<<g, 256, 0, s>>>(sk, pm, ntiles, T, part);
-    }
+                                 const PM& pm, int64_t ntiles, cudaStream_t s, KernelClass kc) {
+    int dev = 0;
+    MSORT_CUDA_TRY(cudaGetDevice(&dev));
+    const int64_t grid = std::min<int64_t>(grid3(dev), ntiles);
     {
       LaunchScope ls(kc, s);
-      k3_merge_pass<K, PAIRS, NT, VT, PM>
-          <<<(unsigned)ntiles, NT, k3_smem, s>>>(sk, sv, dk, dv, pm, part);
+      k3_merge_pass<K, PAIRS, NC, VT, S, OB, PM>
+          <<<(unsigned)grid, NC + 64, k3_smem, s>>>(sk, sv, dk, dv, pm, ntiles);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
     return MSORT_SUCCESS;
@@ -261,11 +407,7 @@ struct Kernels {
     K* wk = reinterpret_cast<K*>(w);
     w += align_up(n * sizeof(K), 256);
     uint32_t* wv = nullptr;
-    if (PAIRS) {
-      wv = reinterpret_cast<uint32_t*>(w);
-      w += align_up(n * sizeof(uint32_t), 256);
-    }
-    int64_t* part = reinterpret_cast<int64_t*>(w);
+    if (PAIRS) wv = reinterpret_cast<uint32_t*>(w);
     (void)ws_bytes;
 
     K* bk[2] = {keys, wk};
@@ -273,14 +415,14 @@ struct Kernels {
     int cur = passes % 2;  // S4: pick K1's destination so the last pass lands in keys
     {
       LaunchScope ls(KC_TILE_SORT, s);
-      k1_tile_sort<K, PAIRS, NT, VT>
-          <<<(unsigned)ntiles, NT, k1_smem, s>>>(in_k, in_v, bk[cur], bv[cur], (int64_t)n);
+      k1_tile_sort<K, PAIRS, NT1, VT>
+          <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, in_v, bk[cur], bv[cur], (int64_t)n);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
+    const int64_t mtiles = (int64_t)((n + Tm - 1) / Tm);
     for (int64_t L = T; L < (int64_t)n; L *= 2) {
       UniformPairs pm{(int64_t)n, L};
-      MSORT_TRY(merge_pass(bk[cur], bv[cur], bk[cur ^ 1], bv[cur ^ 1], pm, ntiles, part, s,
-                           KC_MERGE));
+      MSORT_TRY(merge_pass(bk[cur], bv[cur], bk[cur ^ 1], bv[cur ^ 1], pm, mtiles, s, KC_MERGE));
       cur ^= 1;
     }
     return MSORT_SUCCESS;
@@ -290,8 +432,7 @@ struct Kernels {
   // pairwise merges (ties to the lower run: merge() left-first at every
   // round keeps the lower run on the left).
   static msort_status kway(K* src_k, uint32_t* src_v, K* tmp_k, uint32_t* tmp_v, K* dst_k,
-                           uint32_t* dst_v, const int64_t* off_in, int runs, int64_t* part,
-                           cudaStream_t s) {
+                           uint32_t* dst_v, const int64_t* off_in, int runs, cudaStream_t s) {
     MSORT_TRY(init());
     const int64_t n = off_in[runs] - off_in[0];
     if (runs <= 1 || n == 0) {
@@ -316,7 +457,6 @@ struct Kernels {
     K* ck = src_k + off_in[0];
     uint32_t* cv = PAIRS ? src_v + off_in[0] : nullptr;
     for (int round = 0; round < rounds; ++round) {
-      const bool last = round == rounds - 1;
       // rounds-1-round remaining after this one: alternate so the last hits dst
       const bool to_dst = ((rounds - 1 - round) % 2) == 0;
       K* nk = to_dst ? dst_k : tmp_k;
@@ -331,19 +471,17 @@ struct Kernels {
         pm.off[2 * m] = a;
         pm.off[2 * m + 1] = bmid;
         pm.off[2 * m + 2] = e;
-        tiles += (e - a + T - 1) / T;
+        tiles += (e - a + Tm - 1) / Tm;
       }
       pm.first_tile[pm.npairs] = tiles;
-      // skip empty pairs in the tile map: first_tile is non-decreasing and
-      // locate() takes the last pair whose first tile <= q, which is non-empty
-      if (tiles > 0) MSORT_TRY(merge_pass(ck, cv, nk, nv, pm, tiles, part, s, KC_KWAY));
-      // new runs: pair outputs
+      // empty pairs own no tiles; locate() picks the last pair whose first
+      // tile <= q, which is never an empty one
+      if (tiles > 0) MSORT_TRY(merge_pass(ck, cv, nk, nv, pm, tiles, s, KC_KWAY));
       int nr = pm.npairs;
       for (int m = 0; m <= nr; ++m) off[m] = off[std::min(2 * m, runs)];
       runs = nr;
       ck = nk;
       cv = nv;
-      (void)last;
     }
     return MSORT_SUCCESS;
   }
@@ -373,28 +511,28 @@ msort_status sort_single_dispatch(const void* in_keys, const void* in_vals, void
 
 template <class K>
 static msort_status kway_k(void* sk, void* sv, void* tk, void* tv, void* dk, void* dv,
-                           const int64_t* off, int runs, void* part, cudaStream_t s) {
+                           const int64_t* off, int runs, cudaStream_t s) {
   if (sv)
     return Kernels<K, true>::kway((K*)sk, (uint32_t*)sv, (K*)tk, (uint32_t*)tv, (K*)dk,
-                                  (uint32_t*)dv, off, runs, (int64_t*)part, s);
-  return Kernels<K, false>::kway((K*)sk, nullptr, (K*)tk, nullptr, (K*)dk, nullptr, off, runs,
-                                 (int64_t*)part, s);
+                                  (uint32_t*)dv, off, runs, s);
+  return Kernels<K, false>::kway((K*)sk, nullptr, (K*)tk, nullptr, (K*)dk, nullptr, off, runs, s);
 }
 
 msort_status kway_merge_dispatch(void* src_k, void* src_v, void* tmp_k, void* tmp_v,
                                  void* dst_k, void* dst_v, const int64_t* off_host, int runs,
                                  msort_dtype kd, msort_dtype vd, void* part_ws,
                                  cudaStream_t s) {
+  (void)part_ws;
   if (vd == MSORT_NONE) src_v = tmp_v = dst_v = nullptr;
   switch (kd) {
     case MSORT_INT32:
-      return kway_k<int32_t>(src_k, src_v, tmp_k, tmp_v, dst_k, dst_v, off_host, runs, part_ws, s);
+      return kway_k<int32_t>(src_k, src_v, tmp_k, tmp_v, dst_k, dst_v, off_host, runs, s);
     case MSORT_UINT32:
-      return kway_k<uint32_t>(src_k, src_v, tmp_k, tmp_v, dst_k, dst_v, off_host, runs, part_ws, s);
+      return kway_k<uint32_t>(src_k, src_v, tmp_k, tmp_v, dst_k, dst_v, off_host, runs, s);
     case MSORT_INT64:
-      return kway_k<int64_t>(src_k, src_v, tmp_k, tmp_v, dst_k, dst_v, off_host, runs, part_ws, s);
+      return kway_k<int64_t>(src_k, src_v, tmp_k, tmp_v, dst_k, dst_v, off_host, runs, s);
     case MSORT_UINT64:
-      return kway_k<uint64_t>(src_k, src_v, tmp_k, tmp_v, dst_k, dst_v, off_host, runs, part_ws, s);
+      return kway_k<uint64_t>(src_k, src_v, tmp_k, tmp_v, dst_k, dst_v, off_host, runs, s);
     default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
   }
 }
@@ -403,9 +541,9 @@ int tile_size_for(msort_dtype kd, msort_dtype vd) {
   bool p = vd != MSORT_NONE;
   switch (kd) {
     case MSORT_INT32:
-    case MSORT_UINT32: return p ? Geometry<int32_t, true>::T : Geometry<int32_t, false>::T;
+    case MSORT_UINT32: return p ? Kernels<int32_t, true>::T : Kernels<int32_t, false>::T;
     case MSORT_INT64:
-    case MSORT_UINT64: return p ? Geometry<int64_t, true>::T : Geometry<int64_t, false>::T;
+    case MSORT_UINT64: return p ? Kernels<int64_t, true>::T : Kernels<int64_t, false>::T;
     default: return 0;
   }
 }
