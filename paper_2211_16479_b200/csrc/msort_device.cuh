@@ -115,6 +115,33 @@ __device__ __forceinline__ void serial_merge(const K* s, const int* src_idx, int
   }
 }
 
+// As serial_merge (unpadded, positions tracked as buffer indices), with a
+// check-free fast path when neither run can run out within VT steps --
+// the common case -- and the checked loop otherwise.
+template <class K, bool TRACK, int VT>
+__device__ __forceinline__ void serial_merge_fast(const K* s, int ai, int aend, int bi, int bend,
+                                                  int lim, K (&key)[VT], int (&pos)[VT]) {
+  if (ai + VT <= aend && bi + VT <= bend) {
+    K ak = s[ai];
+    K bk = s[bi];
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+      const bool takeB = bk < ak;
+      key[k] = takeB ? bk : ak;
+      if constexpr (TRACK) pos[k] = takeB ? bi : ai;
+      ai += takeB ? 0 : 1;
+      bi += takeB ? 1 : 0;
+      if (k + 1 < VT) {
+        const K nv = s[takeB ? bi : ai];
+        ak = takeB ? ak : nv;
+        bk = takeB ? nv : bk;
+      }
+    }
+  } else {
+    serial_merge<K, false, TRACK, VT>(s, nullptr, ai, aend, bi, bend, lim, key, pos);
+  }
+}
+
 // ------------------------------------------- mbarrier + 1-D bulk copy (TMA)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

@@ -138,33 +138,32 @@ struct TileMeta {
 
 constexpr size_t align_up_c(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-template <class K, bool PAIRS, int NC, int VT, int S, int OB>
+// Shared memory of one K3 CTA: barriers, tile metadata, the co-rank ring and
+// S stages.  A stage holds the staged A|B window of one output tile and is
+// then overwritten in place by that tile's merged output, which leaves by a
+// bulk store before the stage is handed back to the producer.
+template <class K, bool PAIRS, int NC, int VT, int S>
 struct K3Layout {
   static constexpr int Tm = NC * VT;
   static constexpr int EK = 16 / sizeof(K);
-  static constexpr int R = 4;                    // split ring: R batches of 32
-  static constexpr int SKE = Tm + 4 * EK;        // staged keys per stage
-  static constexpr int SVE = Tm + 16;            // staged vals per stage
-  static constexpr size_t bars = 0;              // full[S], empty[S], sfull[R], sempty[R]
+  static constexpr int R = 4;              // co-rank ring: R batches of 32
+  static constexpr int SKE = Tm + 4 * EK;  // keys per stage (windows + phase slack)
+  static constexpr int SVE = Tm + 16;      // payloads per stage
+  static constexpr size_t bars = 0;        // full[S], empty[S], sfull[R], sempty[R]
   static constexpr size_t meta = 128;
   static constexpr size_t ring = meta + 48 * S;
   static constexpr size_t stage_k = align_up_c(ring + 8 * 32 * R, 128);
   static constexpr size_t stage_v = align_up_c(stage_k + (size_t)S * SKE * sizeof(K), 128);
-  static constexpr int OBK = Tm + 2 * EK;  // output tile + 16-byte phase slack
-  static constexpr int OBV = Tm + 8;
-  static constexpr size_t out_k =
-      align_up_c(stage_v + (PAIRS ? (size_t)S * SVE * 4 : 0), 128);
-  static constexpr size_t out_v = align_up_c(out_k + (size_t)OB * OBK * sizeof(K), 128);
-  static constexpr size_t bytes = align_up_c(out_v + (PAIRS ? (size_t)OB * OBV * 4 : 0), 128);
+  static constexpr size_t bytes = align_up_c(stage_v + (PAIRS ? (size_t)S * SVE * 4 : 0), 128);
 };
 
-// Persistent merge pass.  CTA c owns the contiguous tiles [t0, t1); warp 0
-// = TMA producer, warp 1 = co-rank searcher, warps 2..2+NC/32 = mergers.
-template <class K, bool PAIRS, int NC, int VT, int S, int OB, class PM>
-__global__ void __launch_bounds__(NC + 64)
+// Persistent merge pass.  CTA c owns the contiguous tiles [t0, t0+cnt);
+// warp 0 = TMA producer, warp 1 = co-rank searcher (K2), warps 2.. = mergers.
+template <class K, bool PAIRS, int NC, int VT, int S, int MINB, class PM>
+__global__ void __launch_bounds__(NC + 64, MINB)
     k3_merge_pass(const K* __restrict__ src_k, const uint32_t* __restrict__ src_v,
                   K* __restrict__ dst_k, uint32_t* __restrict__ dst_v, PM pm, int64_t ntiles) {
-  using LY = K3Layout<K, PAIRS, NC, VT, S, OB>;
+  using LY = K3Layout<K, PAIRS, NC, VT, S>;
   constexpr int Tm = LY::Tm, EK = LY::EK, R = LY::R;
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + LY::bars);
@@ -175,8 +174,6 @@ __global__ void __launch_bounds__(NC + 64)
   int64_t* ring = reinterpret_cast<int64_t*>(smem + LY::ring);
   K* stk = reinterpret_cast<K*>(smem + LY::stage_k);
   uint32_t* stv = reinterpret_cast<uint32_t*>(smem + LY::stage_v);
-  K* obk = reinterpret_cast<K*>(smem + LY::out_k);
-  uint32_t* obv = reinterpret_cast<uint32_t*>(smem + LY::out_v);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // contiguous tile range of this CTA
@@ -184,7 +181,7 @@ __global__ void __launch_bounds__(NC + 64)
   const int64_t t0 = c * per + min(c, rem);
   const int64_t cnt = per + (c < rem ? 1 : 0);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&full[s], 32), mbar_init(&empty[s], NC / 32);
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 32), mbar_init(&empty[s], 1);
     for (int r = 0; r < R; ++r) mbar_init(&sfull[r], 32), mbar_init(&sempty[r], 1);
     fence_mbar_init();
   }
@@ -217,7 +214,7 @@ __global__ void __launch_bounds__(NC + 64)
       // co-ranks of diagonals k and k+1 (local), possibly in two batches
       const int64_t b0 = k / 32, b1 = (k + 1) / 32;
       mbar_wait(&sfull[b0 % R], (uint32_t)((b0 / R) & 1));
-      if (b1 != b0 && b1 < nbatch) mbar_wait(&sfull[b1 % R], (uint32_t)((b1 / R) & 1));
+      if (b1 != b0) mbar_wait(&sfull[b1 % R], (uint32_t)((b1 / R) & 1));
       int64_t A0, na_all, nb_all, d0;
       pm.locate(q, Tm, A0, na_all, nb_all, d0);
       const int64_t tot_all = na_all + nb_all;
@@ -261,31 +258,42 @@ __global__ void __launch_bounds__(NC + 64)
   } else {
     // ------------------------------------------------------------ mergers
     const int ct = threadIdx.x - 64;  // 0..NC-1
+    int prev_s = -1;
     for (int64_t k = 0; k < cnt; ++k) {
       const int s = (int)(k % S);
-      const int ob = OB == 1 ? 0 : (int)(k % OB);
       mbar_wait(&full[s], (uint32_t)((k / S) & 1));
       const TileMeta m = meta[s];
-      const K* sk = stk + (size_t)s * LY::SKE;
-      const uint32_t* sv = stv + (size_t)s * LY::SVE;
+      K* sk = stk + (size_t)s * LY::SKE;
+      uint32_t* sv = stv + (size_t)s * LY::SVE;
       K key[VT];
       int pos[VT];
       const int d = ct * VT;
       if (d < m.tot) {
         int i = merge_path<K, false>(sk, m.offA, m.na, m.offB, m.nb, d);
-        serial_merge<K, false, PAIRS, VT>(sk, nullptr, m.offA + i, m.offA + m.na,
-                                          m.offB + d - i, m.offB + m.nb, LY::SKE - 1, key, pos);
+        serial_merge_fast<K, PAIRS, VT>(sk, m.offA + i, m.offA + m.na, m.offB + d - i,
+                                        m.offB + m.nb, LY::SKE - 1, key, pos);
       }
-      if (ct == 0) bulk_wait_read<OB - 1>();  // store from this buffer has read it
-      named_bar_sync(1, NC);                   // output buffer ob is free
-      // The output tile keeps its global 16-byte phase in shared memory so
-      // the aligned middle leaves by one bulk store (TMA, cp.async.bulk).
+      uint32_t val[PAIRS ? VT : 1];
+      if constexpr (PAIRS) {
+#pragma unroll
+        for (int t = 0; t < VT; ++t) {
+          const int p = pos[t];
+          val[t] = sv[p < m.offB ? m.offAv + (p - m.offA) : m.offBv + (p - m.offB)];
+        }
+      }
+      // everyone is done reading stage s (so it can be overwritten) and with
+      // the previous tile's head/tail stores (so that stage can be recycled)
+      named_bar_sync(1, NC);
+      if (ct == 0 && prev_s >= 0) {
+        bulk_wait_read<0>();         // the previous tile's bulk store has read it
+        mbar_arrive(&empty[prev_s]);  // ... so it goes back to the producer
+      }
+      // The output keeps its global 16-byte phase so the aligned middle leaves
+      // by one bulk store (TMA, cp.async.bulk.global.shared).
       K* gk = dst_k + m.out;
       const int phk = stage_offset(gk);
-      K* ok = obk + (size_t)ob * LY::OBK;
       uint32_t* gv = nullptr;
       int phv = 0;
-      uint32_t* ovb = obv + (size_t)ob * LY::OBV;
       if constexpr (PAIRS) {
         gv = dst_v + m.out;
         phv = stage_offset(gv);
@@ -293,36 +301,32 @@ __global__ void __launch_bounds__(NC + 64)
 #pragma unroll
       for (int t = 0; t < VT; ++t) {
         if (d + t < m.tot) {
-          ok[phk + d + t] = key[t];
-          if constexpr (PAIRS) {
-            const int p = pos[t];
-            ovb[phv + d + t] = sv[p < m.offB ? m.offAv + (p - m.offA) : m.offBv + (p - m.offB)];
-          }
+          sk[phk + d + t] = key[t];
+          if constexpr (PAIRS) sv[phv + d + t] = val[t];
         }
       }
       fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);  // stage s fully consumed
-      named_bar_sync(1, NC);                  // output tile complete in shared memory
+      named_bar_sync(1, NC);  // output tile complete in shared memory
       int hk, mk;
       window_split(gk, m.tot, hk, mk);
       int hv = 0, mv = 0;
       if constexpr (PAIRS) window_split(gv, m.tot, hv, mv);
       if (ct == 0) {
-        if (mk) bulk_s2g(gk + hk, ok + phk + hk, (uint32_t)(mk * sizeof(K)));
+        if (mk) bulk_s2g(gk + hk, sk + phk + hk, (uint32_t)(mk * sizeof(K)));
         if constexpr (PAIRS)
-          if (mv) bulk_s2g(gv + hv, ovb + phv + hv, (uint32_t)(mv * 4));
+          if (mv) bulk_s2g(gv + hv, sv + phv + hv, (uint32_t)(mv * 4));
         bulk_commit();
       }
       for (int i = ct; i < m.tot - mk; i += NC) {
         const int j = i < hk ? i : i + mk;
-        gk[j] = ok[phk + j];
+        gk[j] = sk[phk + j];
       }
       if constexpr (PAIRS)
         for (int i = ct; i < m.tot - mv; i += NC) {
           const int j = i < hv ? i : i + mv;
-          gv[j] = ovb[phv + j];
+          gv[j] = sv[phv + j];
         }
+      prev_s = s;
     }
     if (ct == 0) bulk_wait_all();
   }
@@ -336,9 +340,11 @@ struct Kernels {
   static constexpr int T = NT1 * VT;  // tile sort size
   static constexpr int NC = 256;      // merging threads per K3 CTA
   static constexpr int Tm = NC * VT;  // merge output tile (T = 2 Tm)
-  static constexpr int S = 2;
-  static constexpr int OB = (sizeof(K) == 4 && !PAIRS) ? 2 : 1;
-  using LY = K3Layout<K, PAIRS, NC, VT, S, OB>;
+  static constexpr int S = 3;
+  using LY = K3Layout<K, PAIRS, NC, VT, S>;
+  // CTAs per SM the register budget is tuned for (shared memory allows 4 for
+  // 4-byte keys without payload, 2-3 otherwise)
+  static constexpr int MINB = (sizeof(K) == 4 && !PAIRS) ? 4 : 2;
   static constexpr size_t k1_smem = (size_t)T * sizeof(K) + (PAIRS ? (size_t)T * 8 : 0);
   static constexpr size_t k3_smem = LY::bytes;
   static_assert(T % Tm == 0, "pair boundaries must be tile boundaries");
@@ -355,8 +361,8 @@ struct Kernels {
     MSORT_CUDA_TRY(cudaFuncSetAttribute(k1_tile_sort<K, PAIRS, NT1, VT>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)k1_smem));
-    auto ku = k3_merge_pass<K, PAIRS, NC, VT, S, OB, UniformPairs>;
-    auto ke = k3_merge_pass<K, PAIRS, NC, VT, S, OB, ExplicitPairs>;
+    auto ku = k3_merge_pass<K, PAIRS, NC, VT, S, MINB, UniformPairs>;
+    auto ke = k3_merge_pass<K, PAIRS, NC, VT, S, MINB, ExplicitPairs>;
     MSORT_CUDA_TRY(cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)k3_smem));
     MSORT_CUDA_TRY(cudaFuncSetAttribute(ke, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -380,7 +386,7 @@ struct Kernels {
     const int64_t grid = std::min<int64_t>(grid3(dev), ntiles);
     {
       LaunchScope ls(kc, s);
-      k3_merge_pass<K, PAIRS, NC, VT, S, OB, PM>
+      k3_merge_pass<K, PAIRS, NC, VT, S, MINB, PM>
           <<<(unsigned)grid, NC + 64, k3_smem, s>>>(sk, sv, dk, dv, pm, ntiles);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
