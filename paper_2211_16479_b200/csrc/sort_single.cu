@@ -277,8 +277,10 @@ __global__ void __launch_bounds__(NC + 64, MINB)
       if constexpr (PAIRS) {
 #pragma unroll
         for (int t = 0; t < VT; ++t) {
-          const int p = pos[t];
-          val[t] = sv[p < m.offB ? m.offAv + (p - m.offA) : m.offBv + (p - m.offB)];
+          if (d + t < m.tot) {
+            const int p = pos[t];
+            val[t] = sv[p < m.offB ? m.offAv + (p - m.offA) : m.offBv + (p - m.offB)];
+          }
         }
       }
       // everyone is done reading stage s (so it can be overwritten) and with
