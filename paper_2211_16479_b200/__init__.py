@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libmsort.so")
+LIB_PATH = os.environ.get("MSORT_LIB") or os.path.join(_PKG, "lib", "libmsort.so")
 
 MSORT_INT32, MSORT_UINT32, MSORT_INT64, MSORT_UINT64, MSORT_NONE = 0, 1, 2, 3, 255
 MSORT_PROFILE_CLASSES = 6

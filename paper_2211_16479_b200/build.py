@@ -55,17 +55,22 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Build the library.  `defines` (e.g. ["MSORT_K3_NC=256"]) and `out`
+    produce tuning variants at another path (loaded via MSORT_LIB)."""
+    lib_path = out or LIB
+    if not force and not defines and out is None and up_to_date():
         return LIB
-    os.makedirs(BUILD, exist_ok=True)
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    bdir = BUILD if not defines else os.path.join(BUILD, "v_" + "_".join(defines).replace("=", ""))
+    os.makedirs(bdir, exist_ok=True)
+    os.makedirs(os.path.dirname(lib_path), exist_ok=True)
     inc, libdir = nccl_dirs()
     incs = ["-I", os.path.join(ROOT, "include"), "-I", inc]
+    dflags = [f"-D{d}" for d in defines]
 
     def compile_one(src):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, *incs, "-c", src, "-o", obj]
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *NVCC_FLAGS, *dflags, *incs, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
@@ -77,15 +82,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, _sources()))
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", libdir, "-l:libnccl.so.2",
            "-Xlinker", f"-rpath={libdir}", "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("-D", action="append", default=[], help="NAME=VALUE define (variant build)")
+    ap.add_argument("--out", default=None, help="output .so for a variant build")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, defines=tuple(a.D), out=a.out))

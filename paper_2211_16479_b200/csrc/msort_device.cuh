@@ -142,6 +142,44 @@ __device__ __forceinline__ void serial_merge_fast(const K* s, int ai, int aend, 
   }
 }
 
+// 2H outputs of one thread merged as two independent chains: the front chain
+// produces outputs 0..H-1 from the co-rank at the thread's first diagonal
+// (ai0, bi0) upwards, the back chain outputs 2H-1..H from the co-rank at its
+// last diagonal (ai1, bi1) downwards.  Forward, ties take A (R1);
+// backward the LAST of equal keys is the B one, so ties take B.  Two
+// dependency chains halve the latency of a thread's merge.  Requires that
+// no run can run out: ai0+H <= aend, bi0+H <= bend, ai1-H >= a_lo,
+// bi1-H >= b_lo (the caller checks, else uses serial_merge).
+template <class K, bool TRACK, int H>
+__device__ __forceinline__ void dual_merge(const K* s, int ai, int bi, int ai1, int bi1,
+                                           K (&key)[2 * H], int (&pos)[2 * H]) {
+  K ak = s[ai], bk = s[bi];
+  K ak1 = s[ai1 - 1], bk1 = s[bi1 - 1];
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    const bool takeB = bk < ak;
+    const bool takeB1 = bk1 >= ak1;
+    key[k] = takeB ? bk : ak;
+    key[2 * H - 1 - k] = takeB1 ? bk1 : ak1;
+    if constexpr (TRACK) {
+      pos[k] = takeB ? bi : ai;
+      pos[2 * H - 1 - k] = takeB1 ? bi1 - 1 : ai1 - 1;
+    }
+    ai += takeB ? 0 : 1;
+    bi += takeB ? 1 : 0;
+    ai1 -= takeB1 ? 0 : 1;
+    bi1 -= takeB1 ? 1 : 0;
+    if (k + 1 < H) {
+      const K nv = s[takeB ? bi : ai];
+      ak = takeB ? ak : nv;
+      bk = takeB ? nv : bk;
+      const K nv1 = s[(takeB1 ? bi1 : ai1) - 1];
+      ak1 = takeB1 ? ak1 : nv1;
+      bk1 = takeB1 ? nv1 : bk1;
+    }
+  }
+}
+
 // ------------------------------------------- mbarrier + 1-D bulk copy (TMA)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

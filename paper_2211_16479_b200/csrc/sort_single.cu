@@ -152,7 +152,8 @@ struct K3Layout {
   static constexpr size_t bars = 0;        // full[S], empty[S], sfull[R], sempty[R]
   static constexpr size_t meta = 128;
   static constexpr size_t ring = meta + 48 * S;
-  static constexpr size_t stage_k = align_up_c(ring + 8 * 32 * R, 128);
+  static constexpr size_t corank = ring + 8 * 32 * R;  // NC+1 ints: per-thread co-ranks
+  static constexpr size_t stage_k = align_up_c(corank + 4 * (NC + 1), 128);
   static constexpr size_t stage_v = align_up_c(stage_k + (size_t)S * SKE * sizeof(K), 128);
   static constexpr size_t bytes = align_up_c(stage_v + (PAIRS ? (size_t)S * SVE * 4 : 0), 128);
 };
@@ -174,6 +175,9 @@ __global__ void __launch_bounds__(NC + 64, MINB)
   int64_t* ring = reinterpret_cast<int64_t*>(smem + LY::ring);
   K* stk = reinterpret_cast<K*>(smem + LY::stage_k);
   uint32_t* stv = reinterpret_cast<uint32_t*>(smem + LY::stage_v);
+  int* corank = reinterpret_cast<int*>(smem + LY::corank);
+  constexpr bool DUAL = (VT % 2) == 0;  // even: two chains per thread
+  constexpr int H = VT / 2;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // contiguous tile range of this CTA
@@ -268,10 +272,28 @@ __global__ void __launch_bounds__(NC + 64, MINB)
       K key[VT];
       int pos[VT];
       const int d = ct * VT;
-      if (d < m.tot) {
+      const int aend = m.offA + m.na, bend = m.offB + m.nb;
+      if constexpr (DUAL) {
+        // co-rank of my first diagonal; the one of my last comes from the
+        // next thread through shared memory
+        const int i0 = d < m.tot ? merge_path<K, false>(sk, m.offA, m.na, m.offB, m.nb, d) : 0;
+        corank[ct] = i0;
+        named_bar_sync(1, NC);
+        const int d1 = min(d + VT, m.tot);
+        const int i1 = d + VT < m.tot ? corank[ct + 1] : m.na;
+        const int ai0 = m.offA + i0, bi0 = m.offB + d - i0;
+        const int ai1 = m.offA + i1, bi1 = m.offB + d1 - i1;
+        if (d1 - d == VT && ai0 + H <= aend && bi0 + H <= bend && ai1 - H >= m.offA &&
+            bi1 - H >= m.offB) {
+          dual_merge<K, PAIRS, H>(sk, ai0, bi0, ai1, bi1, key, pos);
+        } else if (d < m.tot) {
+          serial_merge<K, false, PAIRS, VT>(sk, nullptr, ai0, aend, bi0, bend, LY::SKE - 1, key,
+                                            pos);
+        }
+      } else if (d < m.tot) {
         int i = merge_path<K, false>(sk, m.offA, m.na, m.offB, m.nb, d);
-        serial_merge_fast<K, PAIRS, VT>(sk, m.offA + i, m.offA + m.na, m.offB + d - i,
-                                        m.offB + m.nb, LY::SKE - 1, key, pos);
+        serial_merge_fast<K, PAIRS, VT>(sk, m.offA + i, aend, m.offB + d - i, bend,
+                                        LY::SKE - 1, key, pos);
       }
       uint32_t val[PAIRS ? VT : 1];
       if constexpr (PAIRS) {
@@ -335,21 +357,29 @@ __global__ void __launch_bounds__(NC + 64, MINB)
 }
 
 // ------------------------------------------------------------ host driver
+#ifndef MSORT_K3_NC
+#define MSORT_K3_NC 128  // merging threads per K3 CTA
+#endif
+#ifndef MSORT_K3_VT
+#define MSORT_K3_VT 34  // outputs per merging thread (even: two chains)
+#endif
+
 template <class K, bool PAIRS>
 struct Kernels {
   static constexpr int VT = 17;  // odd: conflict-free blocked shared accesses
   static constexpr int NT1 = 512;
   static constexpr int T = NT1 * VT;  // tile sort size
-  static constexpr int NC = 256;      // merging threads per K3 CTA
-  static constexpr int Tm = NC * VT;  // merge output tile (T = 2 Tm)
+  static constexpr int NC = MSORT_K3_NC;
+  static constexpr int VT3 = MSORT_K3_VT;
+  static constexpr int Tm = NC * VT3;  // merge output tile (divides 2T)
   static constexpr int S = 3;
-  using LY = K3Layout<K, PAIRS, NC, VT, S>;
+  using LY = K3Layout<K, PAIRS, NC, VT3, S>;
   // CTAs per SM the register budget is tuned for (shared memory allows 4 for
   // 4-byte keys without payload, 2-3 otherwise)
   static constexpr int MINB = (sizeof(K) == 4 && !PAIRS) ? 4 : 2;
   static constexpr size_t k1_smem = (size_t)T * sizeof(K) + (PAIRS ? (size_t)T * 8 : 0);
   static constexpr size_t k3_smem = LY::bytes;
-  static_assert(T % Tm == 0, "pair boundaries must be tile boundaries");
+  static_assert((2 * T) % Tm == 0, "pair boundaries must be tile boundaries");
 
   static int& grid3(int dev) {
     static int g[64] = {};
@@ -363,8 +393,8 @@ struct Kernels {
     MSORT_CUDA_TRY(cudaFuncSetAttribute(k1_tile_sort<K, PAIRS, NT1, VT>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)k1_smem));
-    auto ku = k3_merge_pass<K, PAIRS, NC, VT, S, MINB, UniformPairs>;
-    auto ke = k3_merge_pass<K, PAIRS, NC, VT, S, MINB, ExplicitPairs>;
+    auto ku = k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, UniformPairs>;
+    auto ke = k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, ExplicitPairs>;
     MSORT_CUDA_TRY(cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)k3_smem));
     MSORT_CUDA_TRY(cudaFuncSetAttribute(ke, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -388,7 +418,7 @@ struct Kernels {
     const int64_t grid = std::min<int64_t>(grid3(dev), ntiles);
     {
       LaunchScope ls(kc, s);
-      k3_merge_pass<K, PAIRS, NC, VT, S, MINB, PM>
+      k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, PM>
           <<<(unsigned)grid, NC + 64, k3_smem, s>>>(sk, sv, dk, dv, pm, ntiles);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
