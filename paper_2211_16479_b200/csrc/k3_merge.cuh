@@ -1,0 +1,377 @@
+// k3_merge.cuh -- K3, the global merge pass (SURVEY.md §8(a) S2+S3).
+//
+// One persistent, warp-specialised launch per merge level merges run pairs
+// (A, B) into one run with the stable merge() of P:107 (ties take the left
+// run, R1).  The output of a level is cut into tiles of Tm
+// elements; tile q covers diagonals [q*Tm, (q+1)*Tm) of its pair and needs
+// the merge-path co-rank
+//     i(d) = min{ i : i = min(d, |A|) or A[i] > B[d-1-i] }
+// at its two boundary diagonals (K2).
+//
+// Work is handed out dynamically in chunks of CH consecutive tiles through a
+// global atomic counter, so CTAs that run faster take more chunks (the
+// static split left ~20% of the SMs idle at the end of a level).  Roles:
+//   warp 1      co-rank searcher: grabs the next chunk and binary-searches its
+//               CH+1 boundary co-ranks in global memory (one lane each) into a
+//               ring of R chunk descriptors guarded by mbarriers;
+//   warp 0      TMA producer: stages A[i0,i1) and B[j0,j1) of each tile into an
+//               S-stage shared ring with cp.async.bulk (UBLKCP) + mbarrier;
+//   warps 2..   mergers: per thread a merge-path search in shared memory and
+//               a branch-free serial merge of VT outputs; the output overwrites
+//               the consumed stage and leaves by one bulk store.
+// At start every warp helps with the first chunk's co-ranks (32-way
+// cooperative searches: 6 dependent rounds instead of 28), so the first tile
+// starts after ~1/4 of a binary-search latency.
+#pragma once
+
+#include "msort_device.cuh"
+
+namespace msort {
+
+struct TileMeta {
+  int64_t out;  // global output index of the tile's first element (-1: stop)
+  int na, nb, offA, offB, offAv, offBv, tot, pad;
+};
+
+constexpr size_t align_up_c(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+constexpr int kChunk = 8;  // tiles per dynamically scheduled chunk
+
+struct ChunkDesc {
+  int64_t q0;  // first tile
+  int cnt;     // tiles in the chunk (0: no more work)
+  int pad;
+  int64_t co[kChunk + 1];  // co-ranks of its boundary diagonals
+};
+
+template <class K, bool PAIRS, int NC, int VT, int S>
+struct K3Layout {
+  static constexpr int Tm = NC * VT;
+  static constexpr int EK = 16 / sizeof(K);
+  static constexpr int R = 4;              // chunk ring
+  static constexpr int SKE = Tm + 4 * EK;  // keys per stage (windows + phase slack)
+  static constexpr int SVE = Tm + 16;      // payloads per stage
+  static constexpr size_t bars = 0;        // full[S], empty[S], sfull[R], sempty[R]
+  static constexpr size_t meta = 128;
+  static constexpr size_t ring = align_up_c(meta + sizeof(TileMeta) * S, 16);
+  static constexpr size_t corank = ring + sizeof(ChunkDesc) * R;  // NC+1 ints
+  static constexpr size_t misc = align_up_c(corank + 4 * (NC + 1), 16);
+  static constexpr size_t stage_k = align_up_c(misc + 16, 128);
+  static constexpr size_t stage_v = align_up_c(stage_k + (size_t)S * SKE * sizeof(K), 128);
+  static constexpr size_t bytes = align_up_c(stage_v + (PAIRS ? (size_t)S * SVE * 4 : 0), 128);
+};
+
+#ifdef MSORT_K3_TRACE
+// Tuning builds only (-DMSORT_K3_TRACE): per-CTA timeline of the last K3 launch.
+__device__ unsigned long long g_k3_trace[4096 * 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define K3_TRACE(slot, v) g_k3_trace[(blockIdx.x & 4095) * 8 + (slot)] = (v)
+#else
+#define K3_TRACE(slot, v) ((void)0)
+#endif
+
+// Co-rank of tile q's first diagonal by one warp: each round probes 32
+// evenly spaced candidates of [lo, hi) and keeps the bucket holding the
+// first one where the (monotone) predicate A[i] > B[d-1-i] turns true.
+template <class K, class PM>
+__device__ __forceinline__ int64_t corank_warp(const K* __restrict__ src, const PM& pm, int64_t q,
+                                               int T, int lane) {
+  int64_t A0, na, nb, dl;
+  pm.locate(q, T, A0, na, nb, dl);
+  const K* a = src + A0;
+  const K* b = a + na;
+  int64_t lo = dl - nb > 0 ? dl - nb : 0;
+  int64_t hi = dl < na ? dl : na;
+  while (hi > lo) {
+    const int64_t span = hi - lo;
+    const int64_t step = (span + 31) >> 5;
+    const int64_t off = step * (lane + 1);
+    const int64_t p = lo + (off < span ? off : span) - 1;
+    const bool pred = __ldg(a + p) > __ldg(b + (dl - 1 - p));
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (m == 0) {
+      lo = hi;
+    } else {
+      const int f = __ffs(m) - 1;
+      const int64_t pf = __shfl_sync(0xffffffffu, p, f);
+      const int64_t pp = __shfl_sync(0xffffffffu, p, f > 0 ? f - 1 : 0);
+      hi = pf;
+      if (f > 0) lo = pp + 1;
+    }
+  }
+  return lo;
+}
+
+template <class K, bool PAIRS, int NC, int VT, int S, int MINB, class PM>
+__global__ void __launch_bounds__(NC + 64, MINB)
+    k3_merge_pass(const K* __restrict__ src_k, const uint32_t* __restrict__ src_v,
+                  K* __restrict__ dst_k, uint32_t* __restrict__ dst_v, PM pm, int64_t ntiles,
+                  unsigned long long* __restrict__ ctr, unsigned long long base) {
+  using LY = K3Layout<K, PAIRS, NC, VT, S>;
+  constexpr int Tm = LY::Tm, EK = LY::EK, R = LY::R, CH = kChunk;
+  constexpr int NW = (NC + 64) / 32;  // warps per CTA
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + LY::bars);
+  uint64_t* empty = full + S;
+  uint64_t* sfull = empty + S;
+  uint64_t* sempty = sfull + R;
+  TileMeta* meta = reinterpret_cast<TileMeta*>(smem + LY::meta);
+  ChunkDesc* ring = reinterpret_cast<ChunkDesc*>(smem + LY::ring);
+  int* corank = reinterpret_cast<int*>(smem + LY::corank);
+  int64_t* first_chunk = reinterpret_cast<int64_t*>(smem + LY::misc);
+  K* stk = reinterpret_cast<K*>(smem + LY::stage_k);
+  uint32_t* stv = reinterpret_cast<uint32_t*>(smem + LY::stage_v);
+  constexpr bool DUAL = (VT % 2) == 0;  // even: two chains per thread
+  constexpr int H = VT / 2;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nchunks = (ntiles + CH - 1) / CH;
+#ifdef MSORT_K3_TRACE
+  const unsigned long long t_start = gtimer();
+  unsigned long long t_wait = 0;
+  int64_t ntile_done = 0;
+  if (threadIdx.x == 0) K3_TRACE(0, t_start);
+#endif
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 32), mbar_init(&empty[s], 1);
+    for (int r = 0; r < R; ++r) mbar_init(&sfull[r], 32), mbar_init(&sempty[r], 1);
+    fence_mbar_init();
+    *first_chunk = (int64_t)(atomicAdd(ctr, 1ull) - base);
+  }
+  __syncthreads();
+  {
+    // the first chunk's co-ranks, one cooperative search per warp
+    const int64_t c = *first_chunk;
+    if (c >= nchunks) return;  // no work for this CTA (uniform)
+    const int64_t q0 = c * CH;
+    const int cnt = (int)min((int64_t)CH, ntiles - q0);
+    for (int w = warp; w <= cnt; w += NW) {
+      const int64_t q = q0 + w;
+      const int64_t v = q < ntiles ? corank_warp(src_k, pm, q, Tm, lane) : 0;
+      if (lane == 0) ring[0].co[w] = v;
+    }
+    if (threadIdx.x == 0) ring[0].q0 = q0, ring[0].cnt = cnt;
+  }
+  __syncthreads();
+#ifdef MSORT_K3_TRACE
+  if (threadIdx.x == 0) K3_TRACE(1, gtimer() - t_start);
+#endif
+
+  if (warp == 1) {
+    // ------------------------------------------------ co-rank searcher (K2)
+    mbar_arrive(&sfull[0]);  // slot 0 was filled cooperatively above
+    for (int64_t b = 1;; ++b) {
+      const int r = (int)(b % R);
+      const uint32_t u = (uint32_t)(b / R);
+      mbar_wait(&sempty[r], (u & 1) ^ 1);
+      int64_t c = 0;
+      if (lane == 0) c = (int64_t)(atomicAdd(ctr, 1ull) - base);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (c >= nchunks) {
+        if (lane == 0) ring[r].cnt = 0;
+        mbar_arrive(&sfull[r]);
+        break;
+      }
+      const int64_t q0 = c * CH;
+      const int cnt = (int)min((int64_t)CH, ntiles - q0);
+      if (lane <= cnt) {
+        const int64_t q = q0 + lane;
+        int64_t v = 0;
+        if (q < ntiles) {
+          int64_t A0, na, nb, dl;
+          pm.locate(q, Tm, A0, na, nb, dl);
+          v = merge_path_global(src_k + A0, na, src_k + A0 + na, nb, dl);
+        }
+        ring[r].co[lane] = v;
+      }
+      if (lane == 0) ring[r].q0 = q0, ring[r].cnt = cnt;
+      mbar_arrive(&sfull[r]);
+    }
+  } else if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    int64_t k = 0;  // tiles issued by this CTA
+    for (int64_t b = 0;; ++b) {
+      const int r = (int)(b % R);
+      mbar_wait(&sfull[r], (uint32_t)((b / R) & 1));
+      const ChunkDesc& cd = ring[r];
+      const int ccnt = cd.cnt;
+      if (ccnt == 0) {
+        // no more chunks: tell the mergers to stop
+        const int s = (int)(k % S);
+        mbar_wait(&empty[s], (uint32_t)(((k / S) & 1) ^ 1));
+        if (lane == 0) meta[s].out = -1;
+        mbar_arrive(&full[s]);
+        break;
+      }
+      for (int j = 0; j < ccnt; ++j, ++k) {
+        const int64_t q = cd.q0 + j;
+        const int s = (int)(k % S);
+        int64_t A0, na_all, nb_all, d0;
+        pm.locate(q, Tm, A0, na_all, nb_all, d0);
+        const int64_t tot_all = na_all + nb_all;
+        const int64_t d1 = min(d0 + Tm, tot_all);
+        const int64_t i0 = cd.co[j];
+        const int64_t i1 = d1 == tot_all ? na_all : cd.co[j + 1];
+        const int64_t j0 = d0 - i0, j1 = d1 - i1;
+        const int na = (int)(i1 - i0), nb = (int)(j1 - j0);
+        const K* a = src_k + A0 + i0;
+        const K* bp = src_k + A0 + na_all + j0;
+        const int offA = stage_offset(a);
+        const int offB = (offA + na + EK - 1) / EK * EK + stage_offset(bp);
+        const uint32_t* av = nullptr;
+        const uint32_t* bv = nullptr;
+        int offAv = 0, offBv = 0;
+        if constexpr (PAIRS) {
+          av = src_v + A0 + i0;
+          bv = src_v + A0 + na_all + j0;
+          offAv = stage_offset(av);
+          offBv = (offAv + na + 3) / 4 * 4 + stage_offset(bv);
+        }
+        if (j + 1 == ccnt) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sempty[r]);  // chunk descriptor consumed
+        }
+#ifdef MSORT_K3_TRACE
+        const unsigned long long tw0 = gtimer();
+#endif
+        mbar_wait(&empty[s], (uint32_t)(((k / S) & 1) ^ 1));
+#ifdef MSORT_K3_TRACE
+        t_wait += gtimer() - tw0;
+        if (k == 0 && lane == 0) K3_TRACE(2, gtimer() - t_start);
+#endif
+        K* sk = stk + (size_t)s * LY::SKE;
+        uint32_t* sv = stv + (size_t)s * LY::SVE;
+        if (lane == 0) {
+          meta[s] = TileMeta{A0 + d0, na, nb, offA, offB, offAv, offBv, na + nb, 0};
+          uint32_t tx = window_bulk_bytes(a, na) + window_bulk_bytes(bp, nb);
+          if constexpr (PAIRS) tx += window_bulk_bytes(av, na) + window_bulk_bytes(bv, nb);
+          mbar_expect_tx(&full[s], tx);  // before the copies that complete it
+        }
+        stage_window(sk + offA, a, na, &full[s], lane == 0, lane, 32);
+        stage_window(sk + offB, bp, nb, &full[s], lane == 0, lane, 32);
+        if constexpr (PAIRS) {
+          stage_window(sv + offAv, av, na, &full[s], lane == 0, lane, 32);
+          stage_window(sv + offBv, bv, nb, &full[s], lane == 0, lane, 32);
+        }
+        mbar_arrive(&full[s]);  // all 32 lanes: their head/tail stores are released
+      }
+    }
+#ifdef MSORT_K3_TRACE
+    if (lane == 0) K3_TRACE(7, t_wait);
+#endif
+  } else {
+    // ------------------------------------------------------------ mergers
+    const int ct = threadIdx.x - 64;  // 0..NC-1
+    int prev_s = -1;
+    for (int64_t k = 0;; ++k) {
+      const int s = (int)(k % S);
+#ifdef MSORT_K3_TRACE
+      const unsigned long long tw0 = gtimer();
+#endif
+      mbar_wait(&full[s], (uint32_t)((k / S) & 1));
+#ifdef MSORT_K3_TRACE
+      t_wait += gtimer() - tw0;
+      if (k == 0 && ct == 0) K3_TRACE(3, gtimer() - t_start);
+#endif
+      const TileMeta m = meta[s];
+      if (m.out < 0) break;
+      K* sk = stk + (size_t)s * LY::SKE;
+      uint32_t* sv = stv + (size_t)s * LY::SVE;
+      K key[VT];
+      int pos[VT];
+      const int d = ct * VT;
+      const int aend = m.offA + m.na, bend = m.offB + m.nb;
+      if constexpr (DUAL) {
+        // co-rank of my first diagonal; the one of my last comes from the
+        // next thread through shared memory
+        const int i0 = d < m.tot ? merge_path<K, false>(sk, m.offA, m.na, m.offB, m.nb, d) : 0;
+        corank[ct] = i0;
+        named_bar_sync(1, NC);
+        const int d1 = min(d + VT, m.tot);
+        const int i1 = d + VT < m.tot ? corank[ct + 1] : m.na;
+        const int ai0 = m.offA + i0, bi0 = m.offB + d - i0;
+        const int ai1 = m.offA + i1, bi1 = m.offB + d1 - i1;
+        if (d1 - d == VT && ai0 + H <= aend && bi0 + H <= bend && ai1 - H >= m.offA &&
+            bi1 - H >= m.offB) {
+          dual_merge<K, PAIRS, H>(sk, ai0, bi0, ai1, bi1, key, pos);
+        } else if (d < m.tot) {
+          serial_merge<K, false, PAIRS, VT>(sk, nullptr, ai0, aend, bi0, bend, LY::SKE - 1, key,
+                                            pos);
+        }
+      } else if (d < m.tot) {
+        int i = merge_path<K, false>(sk, m.offA, m.na, m.offB, m.nb, d);
+        serial_merge_fast<K, PAIRS, VT>(sk, m.offA + i, aend, m.offB + d - i, bend,
+                                        LY::SKE - 1, key, pos);
+      }
+      uint32_t val[PAIRS ? VT : 1];
+      if constexpr (PAIRS) {
+#pragma unroll
+        for (int t = 0; t < VT; ++t) {
+          if (d + t < m.tot) {
+            const int p = pos[t];
+            val[t] = sv[p < m.offB ? m.offAv + (p - m.offA) : m.offBv + (p - m.offB)];
+          }
+        }
+      }
+      // everyone is done reading stage s (so it can be overwritten) and with
+      // the previous tile's head/tail stores (so that stage can be recycled)
+      named_bar_sync(1, NC);
+      if (ct == 0 && prev_s >= 0) {
+        bulk_wait_read<0>();         // the previous tile's bulk store has read it
+        mbar_arrive(&empty[prev_s]);  // ... so it goes back to the producer
+      }
+      // The output keeps its global 16-byte phase so the aligned middle leaves
+      // by one bulk store (TMA, cp.async.bulk.global.shared).
+      K* gk = dst_k + m.out;
+      const int phk = stage_offset(gk);
+      uint32_t* gv = nullptr;
+      int phv = 0;
+      if constexpr (PAIRS) {
+        gv = dst_v + m.out;
+        phv = stage_offset(gv);
+      }
+#pragma unroll
+      for (int t = 0; t < VT; ++t) {
+        if (d + t < m.tot) {
+          sk[phk + d + t] = key[t];
+          if constexpr (PAIRS) sv[phv + d + t] = val[t];
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, NC);  // output tile complete in shared memory
+      int hk, mk;
+      window_split(gk, m.tot, hk, mk);
+      int hv = 0, mv = 0;
+      if constexpr (PAIRS) window_split(gv, m.tot, hv, mv);
+      if (ct == 0) {
+        if (mk) bulk_s2g(gk + hk, sk + phk + hk, (uint32_t)(mk * sizeof(K)));
+        if constexpr (PAIRS)
+          if (mv) bulk_s2g(gv + hv, sv + phv + hv, (uint32_t)(mv * 4));
+        bulk_commit();
+      }
+      for (int i = ct; i < m.tot - mk; i += NC) {
+        const int j = i < hk ? i : i + mk;
+        gk[j] = sk[phk + j];
+      }
+      if constexpr (PAIRS)
+        for (int i = ct; i < m.tot - mv; i += NC) {
+          const int j = i < hv ? i : i + mv;
+          gv[j] = sv[phv + j];
+        }
+      prev_s = s;
+#ifdef MSORT_K3_TRACE
+      ++ntile_done;
+#endif
+    }
+    if (ct == 0) bulk_wait_all();
+#ifdef MSORT_K3_TRACE
+    if (ct == 0) K3_TRACE(4, gtimer() - t_start), K3_TRACE(6, t_wait), K3_TRACE(5, ntile_done);
+#endif
+  }
+}
+
+}  // namespace msort
