@@ -36,6 +36,7 @@ struct TileMeta {
 constexpr size_t align_up_c(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 constexpr int kChunk = 8;  // tiles per dynamically scheduled chunk
+constexpr int kGrab = 3;   // chunks taken per atomic (the searcher fills 3 ring slots per round)
 
 struct ChunkDesc {
   int64_t q0;  // first tile
@@ -48,7 +49,7 @@ template <class K, bool PAIRS, int NC, int VT, int S>
 struct K3Layout {
   static constexpr int Tm = NC * VT;
   static constexpr int EK = 16 / sizeof(K);
-  static constexpr int R = 4;              // chunk ring
+  static constexpr int R = 2 * kGrab;      // chunk ring: two searcher rounds
   static constexpr int SKE = Tm + 4 * EK;  // keys per stage (windows + phase slack)
   static constexpr int SVE = Tm + 16;      // payloads per stage
   static constexpr size_t bars = 0;        // full[S], empty[S], sfull[R], sempty[R]
@@ -140,11 +141,15 @@ __global__ void __launch_bounds__(NC + 64, MINB)
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 32), mbar_init(&empty[s], 1);
     for (int r = 0; r < R; ++r) mbar_init(&sfull[r], 32), mbar_init(&sempty[r], 1);
     fence_mbar_init();
-    *first_chunk = (int64_t)(atomicAdd(ctr, 1ull) - base);
+    *first_chunk = (int64_t)(atomicAdd(ctr, (unsigned long long)kGrab) - base);
   }
   __syncthreads();
+#ifdef MSORT_K3_TRACE
+  if (threadIdx.x == 0) K3_TRACE(2, gtimer() - t_start);
+#endif
   {
-    // the first chunk's co-ranks, one cooperative search per warp
+    // the first chunk's co-ranks, one cooperative search per warp; the other
+    // kGrab-1 chunks of this grab go to the searcher
     const int64_t c = *first_chunk;
     if (c >= nchunks) return;  // no work for this CTA (uniform)
     const int64_t q0 = c * CH;
@@ -163,33 +168,54 @@ __global__ void __launch_bounds__(NC + 64, MINB)
 
   if (warp == 1) {
     // ------------------------------------------------ co-rank searcher (K2)
-    mbar_arrive(&sfull[0]);  // slot 0 was filled cooperatively above
-    for (int64_t b = 1;; ++b) {
-      const int r = (int)(b % R);
-      const uint32_t u = (uint32_t)(b / R);
-      mbar_wait(&sempty[r], (u & 1) ^ 1);
-      int64_t c = 0;
-      if (lane == 0) c = (int64_t)(atomicAdd(ctr, 1ull) - base);
-      c = __shfl_sync(0xffffffffu, c, 0);
-      if (c >= nchunks) {
-        if (lane == 0) ring[r].cnt = 0;
-        mbar_arrive(&sfull[r]);
-        break;
+    // Round g fills ring slots kGrab*g .. kGrab*g+kGrab-1 (mod R) with the
+    // chunks of one grab; lanes 9m..9m+8 search chunk m's CH+1 co-ranks.
+    static_assert(kGrab * (kChunk + 1) <= 32, "one lane per co-rank");
+    mbar_arrive(&sfull[0]);  // slot 0 (first chunk of grab 0) was filled above
+    int64_t c0 = *first_chunk;
+    bool done = false;
+    for (int64_t g = 0; !done; ++g) {
+      if (g > 0) {
+        int64_t c = 0;
+        if (lane == 0) c = (int64_t)(atomicAdd(ctr, (unsigned long long)kGrab) - base);
+        c0 = __shfl_sync(0xffffffffu, c, 0);
       }
-      const int64_t q0 = c * CH;
-      const int cnt = (int)min((int64_t)CH, ntiles - q0);
-      if (lane <= cnt) {
-        const int64_t q = q0 + lane;
-        int64_t v = 0;
+      const int m = lane / (CH + 1), j = lane % (CH + 1);
+      for (int mm = (g == 0 ? 1 : 0); mm < kGrab; ++mm) {
+        const int64_t b = g * kGrab + mm;  // ring use index
+        const int r = (int)(b % R);
+        mbar_wait(&sempty[r], (uint32_t)(((b / R) & 1) ^ 1));
+      }
+      // every lane searches its co-rank (if any) of this grab
+      int64_t v = 0;
+      const int64_t cm = c0 + m;
+      const bool mine = m < kGrab && !(g == 0 && m == 0) && cm < nchunks;
+      int cntm = 0;
+      if (m < kGrab && cm < nchunks) cntm = (int)min((int64_t)CH, ntiles - cm * CH);
+      if (mine && j <= cntm) {
+        const int64_t q = cm * CH + j;
         if (q < ntiles) {
           int64_t A0, na, nb, dl;
           pm.locate(q, Tm, A0, na, nb, dl);
           v = merge_path_global(src_k + A0, na, src_k + A0 + na, nb, dl);
         }
-        ring[r].co[lane] = v;
       }
-      if (lane == 0) ring[r].q0 = q0, ring[r].cnt = cnt;
-      mbar_arrive(&sfull[r]);
+      for (int mm = (g == 0 ? 1 : 0); mm < kGrab; ++mm) {
+        const int r = (int)((g * kGrab + mm) % R);
+        const int64_t cmm = c0 + mm;
+        if (m == mm && mine && j <= cntm) ring[r].co[j] = v;
+        if (lane == 0) {
+          if (cmm < nchunks) {
+            ring[r].q0 = cmm * CH;
+            ring[r].cnt = (int)min((int64_t)CH, ntiles - cmm * CH);
+          } else {
+            ring[r].cnt = 0;  // end of work: the producer stops at this slot
+          }
+        }
+        if (cmm >= nchunks) done = true;
+        mbar_arrive(&sfull[r]);
+        if (done) break;
+      }
     }
   } else if (warp == 0) {
     // ------------------------------------------------------ TMA producer
@@ -241,7 +267,6 @@ __global__ void __launch_bounds__(NC + 64, MINB)
         mbar_wait(&empty[s], (uint32_t)(((k / S) & 1) ^ 1));
 #ifdef MSORT_K3_TRACE
         t_wait += gtimer() - tw0;
-        if (k == 0 && lane == 0) K3_TRACE(2, gtimer() - t_start);
 #endif
         K* sk = stk + (size_t)s * LY::SKE;
         uint32_t* sv = stv + (size_t)s * LY::SVE;

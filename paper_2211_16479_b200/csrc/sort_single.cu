@@ -194,12 +194,12 @@ struct Kernels {
     return MSORT_SUCCESS;
   }
 
-  // Dynamic chunk scheduling: one 64-bit counter in the workspace, zeroed once
-  // per sort; pass p hands out chunk c = atomicAdd(ctr) - base_p and every CTA
-  // overshoots exactly once, so base_{p+1} = base_p + chunks_p + grid_p.
+  // Dynamic chunk scheduling: one 64-bit counter per merge pass in the
+  // workspace (kMaxPasses of them), all zeroed by one memset per sort.
+  static constexpr int kMaxPasses = 64;
   struct Sched {
     unsigned long long* ctr;
-    unsigned long long base;
+    unsigned long long base;  // always 0: each pass has its own counter
   };
 
   template <class PM>
@@ -209,14 +209,14 @@ struct Kernels {
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
     const int64_t nchunks = (ntiles + kChunk - 1) / kChunk;
-    const int64_t grid = std::min<int64_t>(grid3(dev), nchunks);
+    const int64_t grid = std::min<int64_t>(grid3(dev), (nchunks + kGrab - 1) / kGrab);
     {
       LaunchScope ls(kc, s);
       k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, PM>
-          <<<(unsigned)grid, NC + 64, k3_smem, s>>>(sk, sv, dk, dv, pm, ntiles, sc.ctr, sc.base);
+          <<<(unsigned)grid, NC + 64, k3_smem, s>>>(sk, sv, dk, dv, pm, ntiles, sc.ctr, 0ull);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
-    sc.base += (unsigned long long)(nchunks + grid);
+    ++sc.ctr;  // the next pass uses the next counter
     return MSORT_SUCCESS;
   }
 
@@ -246,7 +246,7 @@ struct Kernels {
     }
     Sched sc{reinterpret_cast<unsigned long long*>(w), 0};
     (void)ws_bytes;
-    MSORT_CUDA_TRY(cudaMemsetAsync(sc.ctr, 0, sizeof(unsigned long long), s));
+    MSORT_CUDA_TRY(cudaMemsetAsync(sc.ctr, 0, kMaxPasses * sizeof(unsigned long long), s));
 
     K* bk[2] = {keys, wk};
     uint32_t* bv[2] = {vals, wv};
@@ -292,7 +292,7 @@ struct Kernels {
     }
     int rounds = 0;
     while ((1 << rounds) < runs) ++rounds;
-    MSORT_CUDA_TRY(cudaMemsetAsync(sc.ctr, 0, sizeof(unsigned long long), s));
+    MSORT_CUDA_TRY(cudaMemsetAsync(sc.ctr, 0, kMaxPasses * sizeof(unsigned long long), s));
     // Ping-pong src -> (tmp|dst) ... so that the last round writes dst.
     int64_t off[2 * kMaxPairs + 2];
     for (int r = 0; r <= runs; ++r) off[r] = off_in[r] - off_in[0];

@@ -32,7 +32,7 @@ ms.lib.msort_debug_k3_trace(buf, 4096 * 8)
 t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 8).astype(np.int64)
 t = t[t[:, 5] > 0]
 start = t[:, 0] - t[:, 0].min()
-names = ["start(us)", "search batch0", "first issue", "first full", "end", "tiles",
+names = ["start(us)", "chunk0 coranks", "after grab", "first full", "end", "tiles",
          "consumer wait", "producer wait"]
 print("CTAs", len(t))
 for i, nm in enumerate(names):
