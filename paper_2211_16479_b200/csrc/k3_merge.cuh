@@ -52,8 +52,8 @@ struct K3Layout {
   static constexpr int R = 2 * kGrab;      // chunk ring: two searcher rounds
   static constexpr int SKE = Tm + 4 * EK;  // keys per stage (windows + phase slack)
   static constexpr int SVE = Tm + 16;      // payloads per stage
-  static constexpr size_t bars = 0;        // full[S], empty[S], sfull[R], sempty[R]
-  static constexpr size_t meta = 128;
+  static constexpr size_t bars = 0;  // full[S], empty[S], sfull[R], sempty[R]
+  static constexpr size_t meta = align_up_c(8 * (2 * S + 2 * R), 16);
   static constexpr size_t ring = align_up_c(meta + sizeof(TileMeta) * S, 16);
   static constexpr size_t corank = ring + sizeof(ChunkDesc) * R;  // NC+1 ints
   static constexpr size_t misc = align_up_c(corank + 4 * (NC + 1), 16);
@@ -73,6 +73,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define K3_TRACE(slot, v) g_k3_trace[(blockIdx.x & 4095) * 8 + (slot)] = (v)
 #else
 #define K3_TRACE(slot, v) ((void)0)
+#endif
+
+#ifdef MSORT_K3_CHECK
+// Debug builds only (-DMSORT_K3_CHECK): invariant checks that trap.
+#define K3_CHECK(cond, ...)                                                        \
+  do {                                                                             \
+    if (!(cond)) {                                                                 \
+      printf("K3_CHECK failed: %s block %d thread %d: ", #cond, blockIdx.x, threadIdx.x); \
+      printf(__VA_ARGS__);                                                         \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define K3_CHECK(cond, ...) ((void)0)
 #endif
 
 // Co-rank of tile q's first diagonal by one warp: each round probes 32
@@ -248,6 +262,11 @@ __global__ void __launch_bounds__(NC + 64, MINB)
         const K* bp = src_k + A0 + na_all + j0;
         const int offA = stage_offset(a);
         const int offB = (offA + na + EK - 1) / EK * EK + stage_offset(bp);
+        K3_CHECK(i0 >= 0 && i0 <= i1 && i1 <= na_all && j0 >= 0 && j0 <= j1 && j1 <= nb_all &&
+                     offB + nb <= LY::SKE && na + nb <= Tm,
+                 "q %lld b %lld j %d ccnt %d q0 %lld i0 %lld i1 %lld na_all %lld nb_all %lld d0 %lld\n",
+                 (long long)q, (long long)b, j, ccnt, (long long)cd.q0, (long long)i0,
+                 (long long)i1, (long long)na_all, (long long)nb_all, (long long)d0);
         const uint32_t* av = nullptr;
         const uint32_t* bv = nullptr;
         int offAv = 0, offBv = 0;

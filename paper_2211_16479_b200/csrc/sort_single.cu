@@ -216,6 +216,16 @@ struct Kernels {
           <<<(unsigned)grid, NC + 64, k3_smem, s>>>(sk, sv, dk, dv, pm, ntiles, sc.ctr, 0ull);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
+#ifdef MSORT_K3_CHECK
+    {
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) {
+        fprintf(stderr, "K3 pass failed: ntiles %lld grid %lld: %s\n", (long long)ntiles,
+                (long long)grid, cudaGetErrorString(e));
+        return cuda_fail(e, "k3 (debug sync)");
+      }
+    }
+#endif
     ++sc.ctr;  // the next pass uses the next counter
     return MSORT_SUCCESS;
   }
@@ -257,6 +267,13 @@ struct Kernels {
           <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, in_v, bk[cur], bv[cur], (int64_t)n);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
+#ifdef MSORT_K3_CHECK
+    {
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) fprintf(stderr, "K1 failed: %s\n", cudaGetErrorString(e));
+      if (e != cudaSuccess) return cuda_fail(e, "k1 (debug sync)");
+    }
+#endif
     const int64_t mtiles = (int64_t)((n + Tm - 1) / Tm);
     for (int64_t L = T; L < (int64_t)n; L *= 2) {
       UniformPairs pm{(int64_t)n, L};
