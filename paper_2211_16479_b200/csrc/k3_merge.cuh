@@ -1,49 +1,92 @@
 // k3_merge.cuh -- K3, the global merge pass (SURVEY.md §8(a) S2+S3).
 //
-// One persistent, warp-specialised launch per merge level merges run pairs
-// (A, B) into one run with the stable merge() of P:107 (ties take the left
-// run, R1).  The output of a level is cut into tiles of Tm
-// elements; tile q covers diagonals [q*Tm, (q+1)*Tm) of its pair and needs
-// the merge-path co-rank
+// Merges run pairs (A, B) into one run with the stable merge() of P:107 (ties
+// take the left run, R1).  The output of a merge level is cut into
+// tiles of Tm elements; tile q covers diagonals [q*Tm, (q+1)*Tm) of its pair
+// and needs the merge-path co-rank
 //     i(d) = min{ i : i = min(d, |A|) or A[i] > B[d-1-i] }
-// at its two boundary diagonals (K2).
+// at its two boundary diagonals (K2, fused here).
 //
-// Work is handed out dynamically in chunks of CH consecutive tiles through a
-// global atomic counter, so CTAs that run faster take more chunks (the
-// static split left ~20% of the SMs idle at the end of a level).  Roles:
-//   warp 1      co-rank searcher: grabs the next chunk and binary-searches its
-//               CH+1 boundary co-ranks in global memory (one lane each) into a
-//               ring of R chunk descriptors guarded by mbarriers;
+// One persistent, warp-specialised kernel; work is handed out dynamically in
+// chunks of CH consecutive tiles through a global atomic counter.  Roles:
+//   warp 1      co-rank searcher: grabs kGrab chunks at a time and
+//               binary-searches their boundary co-ranks in global memory (one
+//               lane each) into a ring of chunk descriptors (mbarriers);
 //   warp 0      TMA producer: stages A[i0,i1) and B[j0,j1) of each tile into an
 //               S-stage shared ring with cp.async.bulk (UBLKCP) + mbarrier;
 //   warps 2..   mergers: per thread a merge-path search in shared memory and
 //               a branch-free serial merge of VT outputs; the output overwrites
 //               the consumed stage and leaves by one bulk store.
 // At start every warp helps with the first chunk's co-ranks (32-way
-// cooperative searches: 6 dependent rounds instead of 28), so the first tile
-// starts after ~1/4 of a binary-search latency.
+// cooperative searches).
+//
+// Two work sources (the Src template parameter):
+//   SinglePass  - one merge level (also the distributed k-way merge rounds);
+//   FusedPasses - ALL merge levels of a sort in one launch, as a dataflow:
+//                 a chunk of level p starts as soon as the two level-(p-1)
+//                 pairs it reads are complete (per-pair completion counters,
+//                 release/acquire at GPU scope), so there is no idle gap or
+//                 tail at level boundaries except where a level depends on
+//                 the whole previous one.
 #pragma once
 
 #include "msort_device.cuh"
 
 namespace msort {
 
-struct TileMeta {
-  int64_t out;  // global output index of the tile's first element (-1: stop)
-  int na, nb, offA, offB, offAv, offBv, tot, pad;
+// ---------------------------------------------------------------- pair maps
+// Where output tile q sits: its run pair starts at A0 (global index), run A
+// has na elements, run B (immediately after A) nb, and the tile's first
+// output diagonal is dl inside the pair.  The pair's output occupies
+// [A0, A0+na+nb) of the destination.
+struct UniformPairs {  // runs of length L (the last ones may be short)
+  int64_t n, L;
+  __device__ __forceinline__ void locate(int64_t q, int T, int64_t& A0, int64_t& na,
+                                         int64_t& nb, int64_t& dl) const {
+    int64_t d = q * T;
+    int64_t m = d / (2 * L);
+    A0 = m * 2 * L;
+    na = min(L, n - A0);
+    int64_t B0 = A0 + L;
+    nb = B0 < n ? min(L, n - B0) : 0;
+    dl = d - A0;
+  }
 };
 
-constexpr size_t align_up_c(size_t x, size_t a) { return (x + a - 1) / a * a; }
+constexpr int kMaxPairs = 64;
+struct ExplicitPairs {  // arbitrary consecutive runs, pairs (2m, 2m+1)
+  int npairs;
+  int64_t first_tile[kMaxPairs + 1];
+  int64_t off[2 * kMaxPairs + 1];
+  __device__ __forceinline__ void locate(int64_t q, int T, int64_t& A0, int64_t& na,
+                                         int64_t& nb, int64_t& dl) const {
+    int m = 0;
+    while (m + 1 < npairs && first_tile[m + 1] <= q) ++m;
+    A0 = off[2 * m];
+    na = off[2 * m + 1] - A0;
+    nb = off[2 * m + 2] - off[2 * m + 1];
+    dl = (q - first_tile[m]) * T;
+  }
+};
 
-constexpr int kChunk = 8;  // tiles per dynamically scheduled chunk
-constexpr int kGrab = 3;   // chunks taken per atomic (the searcher fills 3 ring slots per round)
+constexpr int kChunk = 8;        // tiles per dynamically scheduled chunk
+constexpr int kGrab = 3;         // chunks taken per atomic
+constexpr int kMaxFusedPasses = 48;
+
+struct TileMeta {
+  int64_t out;  // output index of the tile's first element (-1: stop)
+  int64_t q;    // tile index within its level
+  int na, nb, offA, offB, offAv, offBv, tot, pass;
+};
 
 struct ChunkDesc {
   int64_t q0;  // first tile
   int cnt;     // tiles in the chunk (0: no more work)
-  int pad;
+  int pass;    // merge level
   int64_t co[kChunk + 1];  // co-ranks of its boundary diagonals
 };
+
+constexpr size_t align_up_c(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 template <class K, bool PAIRS, int NC, int VT, int S>
 struct K3Layout {
@@ -52,7 +95,7 @@ struct K3Layout {
   static constexpr int R = 2 * kGrab;      // chunk ring: two searcher rounds
   static constexpr int SKE = Tm + 4 * EK;  // keys per stage (windows + phase slack)
   static constexpr int SVE = Tm + 16;      // payloads per stage
-  static constexpr size_t bars = 0;  // full[S], empty[S], sfull[R], sempty[R]
+  static constexpr size_t bars = 0;        // full[S], empty[S], sfull[R], sempty[R]
   static constexpr size_t meta = align_up_c(8 * (2 * S + 2 * R), 16);
   static constexpr size_t ring = align_up_c(meta + sizeof(TileMeta) * S, 16);
   static constexpr size_t corank = ring + sizeof(ChunkDesc) * R;  // NC+1 ints
@@ -60,6 +103,107 @@ struct K3Layout {
   static constexpr size_t stage_k = align_up_c(misc + 16, 128);
   static constexpr size_t stage_v = align_up_c(stage_k + (size_t)S * SKE * sizeof(K), 128);
   static constexpr size_t bytes = align_up_c(stage_v + (PAIRS ? (size_t)S * SVE * 4 : 0), 128);
+};
+
+// ------------------------------------------------------------ work sources
+template <class K, class PM>
+struct SinglePass {
+  static constexpr bool kFused = false;
+  PM pm;
+  const K* src_k;
+  const uint32_t* src_v;
+  K* dst_k;
+  uint32_t* dst_v;
+  int64_t ntiles;
+  __device__ __forceinline__ int64_t nchunks() const { return (ntiles + kChunk - 1) / kChunk; }
+  __device__ __forceinline__ void chunk(int64_t g, int& pass, int64_t& q0, int& cnt) const {
+    pass = 0;
+    q0 = g * kChunk;
+    cnt = (int)min((int64_t)kChunk, ntiles - q0);
+  }
+  __device__ __forceinline__ int64_t tiles(int) const { return ntiles; }
+  __device__ __forceinline__ void wait_ready(int, int64_t, int, int, int) const {}
+  __device__ __forceinline__ void locate(int, int64_t q, int Tm, int64_t& A0, int64_t& na,
+                                         int64_t& nb, int64_t& dl) const {
+    pm.locate(q, Tm, A0, na, nb, dl);
+  }
+  __device__ __forceinline__ const K* srck(int) const { return src_k; }
+  __device__ __forceinline__ const uint32_t* srcv(int) const { return src_v; }
+  __device__ __forceinline__ K* dstk(int) const { return dst_k; }
+  __device__ __forceinline__ uint32_t* dstv(int) const { return dst_v; }
+  __device__ __forceinline__ void tile_done(int, int64_t, int) const {}
+};
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// All merge levels of one sort: level p merges runs of L_p = T * 2^p from
+// buffer bk[p & 1] into bk[(p+1) & 1]; every level has the same tile count.
+template <class K>
+struct FusedPasses {
+  static constexpr bool kFused = true;
+  K* bk[2];
+  uint32_t* bv[2];
+  int64_t n, T, ntiles;
+  int P;
+  unsigned* done;  // per level, per pair: tiles completed
+  int64_t pair_base[kMaxFusedPasses + 1];
+  __device__ __forceinline__ int64_t cpp() const { return (ntiles + kChunk - 1) / kChunk; }
+  __device__ __forceinline__ int64_t nchunks() const { return (int64_t)P * cpp(); }
+  __device__ __forceinline__ void chunk(int64_t g, int& pass, int64_t& q0, int& cnt) const {
+    const int64_t c = cpp();
+    pass = (int)(g / c);
+    q0 = (g % c) * kChunk;
+    cnt = (int)min((int64_t)kChunk, ntiles - q0);
+  }
+  __device__ __forceinline__ int64_t tiles(int) const { return ntiles; }
+  __device__ __forceinline__ int64_t L(int pass) const { return T << pass; }
+  __device__ __forceinline__ void locate(int pass, int64_t q, int Tm, int64_t& A0, int64_t& na,
+                                         int64_t& nb, int64_t& dl) const {
+    UniformPairs{n, L(pass)}.locate(q, Tm, A0, na, nb, dl);
+  }
+  __device__ __forceinline__ int64_t pair_of(int pass, int64_t q, int Tm) const {
+    return q * Tm / (2 * L(pass));
+  }
+  __device__ __forceinline__ unsigned pair_tiles(int pass, int64_t m, int Tm) const {
+    const int64_t len = min(2 * L(pass), n - m * 2 * L(pass));
+    return (unsigned)((len + Tm - 1) / Tm);
+  }
+  // Level p >= 1 reads the outputs of level-(p-1) pairs 2m, 2m+1: wait until
+  // those are complete (the whole warp returns together).
+  __device__ __forceinline__ void wait_ready(int pass, int64_t q0, int cnt, int lane,
+                                             int Tm) const {
+    if (pass == 0) return;
+    const int64_t m0 = pair_of(pass, q0, Tm), m1 = pair_of(pass, q0 + cnt - 1, Tm);
+    const int64_t np = pair_base[pass] - pair_base[pass - 1];  // pairs of level p-1
+    const int64_t last = min(2 * m1 + 1, np - 1);
+    for (int64_t dp = 2 * m0 + lane; dp <= last; dp += 32) {
+      const unsigned need = pair_tiles(pass - 1, dp, Tm);
+      const unsigned* c = done + pair_base[pass - 1] + dp;
+      while (ld_acquire_gpu(c) < need) __nanosleep(256);
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ const K* srck(int p) const { return bk[p & 1]; }
+  __device__ __forceinline__ const uint32_t* srcv(int p) const { return bv[p & 1]; }
+  __device__ __forceinline__ K* dstk(int p) const { return bk[(p + 1) & 1]; }
+  __device__ __forceinline__ uint32_t* dstv(int p) const { return bv[(p + 1) & 1]; }
+  // Called by one thread after the tile's output (bulk store waited for,
+  // scalar stores ordered by a CTA barrier) is complete.
+  __device__ __forceinline__ void tile_done(int pass, int64_t q, int Tm) const {
+    fence_proxy_async_global();
+    __threadfence();
+    red_release_gpu_add(done + pair_base[pass] + pair_of(pass, q, Tm), 1u);
+  }
 };
 
 #ifdef MSORT_K3_TRACE
@@ -77,13 +221,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 #ifdef MSORT_K3_CHECK
 // Debug builds only (-DMSORT_K3_CHECK): invariant checks that trap.
-#define K3_CHECK(cond, ...)                                                        \
-  do {                                                                             \
-    if (!(cond)) {                                                                 \
+#define K3_CHECK(cond, ...)                                                                \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
       printf("K3_CHECK failed: %s block %d thread %d: ", #cond, blockIdx.x, threadIdx.x); \
-      printf(__VA_ARGS__);                                                         \
-      __trap();                                                                    \
-    }                                                                              \
+      printf(__VA_ARGS__);                                                                 \
+      __trap();                                                                            \
+    }                                                                                      \
   } while (0)
 #else
 #define K3_CHECK(cond, ...) ((void)0)
@@ -92,12 +236,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Co-rank of tile q's first diagonal by one warp: each round probes 32
 // evenly spaced candidates of [lo, hi) and keeps the bucket holding the
 // first one where the (monotone) predicate A[i] > B[d-1-i] turns true.
-template <class K, class PM>
-__device__ __forceinline__ int64_t corank_warp(const K* __restrict__ src, const PM& pm, int64_t q,
-                                               int T, int lane) {
+template <class K, class Src>
+__device__ __forceinline__ int64_t corank_warp(const Src& src, int pass, int64_t q, int T,
+                                               int lane) {
   int64_t A0, na, nb, dl;
-  pm.locate(q, T, A0, na, nb, dl);
-  const K* a = src + A0;
+  src.locate(pass, q, T, A0, na, nb, dl);
+  const K* a = src.srck(pass) + A0;
   const K* b = a + na;
   int64_t lo = dl - nb > 0 ? dl - nb : 0;
   int64_t hi = dl < na ? dl : na;
@@ -106,7 +250,7 @@ __device__ __forceinline__ int64_t corank_warp(const K* __restrict__ src, const 
     const int64_t step = (span + 31) >> 5;
     const int64_t off = step * (lane + 1);
     const int64_t p = lo + (off < span ? off : span) - 1;
-    const bool pred = __ldg(a + p) > __ldg(b + (dl - 1 - p));
+    const bool pred = a[p] > b[dl - 1 - p];
     const unsigned m = __ballot_sync(0xffffffffu, pred);
     if (m == 0) {
       lo = hi;
@@ -121,11 +265,9 @@ __device__ __forceinline__ int64_t corank_warp(const K* __restrict__ src, const 
   return lo;
 }
 
-template <class K, bool PAIRS, int NC, int VT, int S, int MINB, class PM>
+template <class K, bool PAIRS, int NC, int VT, int S, int MINB, class Src>
 __global__ void __launch_bounds__(NC + 64, MINB)
-    k3_merge_pass(const K* __restrict__ src_k, const uint32_t* __restrict__ src_v,
-                  K* __restrict__ dst_k, uint32_t* __restrict__ dst_v, PM pm, int64_t ntiles,
-                  unsigned long long* __restrict__ ctr, unsigned long long base) {
+    k3_merge_pass(const __grid_constant__ Src src, unsigned long long* __restrict__ ctr) {
   using LY = K3Layout<K, PAIRS, NC, VT, S>;
   constexpr int Tm = LY::Tm, EK = LY::EK, R = LY::R, CH = kChunk;
   constexpr int NW = (NC + 64) / 32;  // warps per CTA
@@ -144,7 +286,7 @@ __global__ void __launch_bounds__(NC + 64, MINB)
   constexpr int H = VT / 2;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nchunks = (ntiles + CH - 1) / CH;
+  const int64_t nchunks = src.nchunks();
 #ifdef MSORT_K3_TRACE
   const unsigned long long t_start = gtimer();
   unsigned long long t_wait = 0;
@@ -155,7 +297,7 @@ __global__ void __launch_bounds__(NC + 64, MINB)
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 32), mbar_init(&empty[s], 1);
     for (int r = 0; r < R; ++r) mbar_init(&sfull[r], 32), mbar_init(&sempty[r], 1);
     fence_mbar_init();
-    *first_chunk = (int64_t)(atomicAdd(ctr, (unsigned long long)kGrab) - base);
+    *first_chunk = (int64_t)atomicAdd(ctr, (unsigned long long)kGrab);
   }
   __syncthreads();
 #ifdef MSORT_K3_TRACE
@@ -166,14 +308,17 @@ __global__ void __launch_bounds__(NC + 64, MINB)
     // kGrab-1 chunks of this grab go to the searcher
     const int64_t c = *first_chunk;
     if (c >= nchunks) return;  // no work for this CTA (uniform)
-    const int64_t q0 = c * CH;
-    const int cnt = (int)min((int64_t)CH, ntiles - q0);
+    int pass, cnt;
+    int64_t q0;
+    src.chunk(c, pass, q0, cnt);
+    if (warp == 0) src.wait_ready(pass, q0, cnt, lane, Tm);
+    __syncthreads();
     for (int w = warp; w <= cnt; w += NW) {
       const int64_t q = q0 + w;
-      const int64_t v = q < ntiles ? corank_warp(src_k, pm, q, Tm, lane) : 0;
+      const int64_t v = q < src.tiles(pass) ? corank_warp<K>(src, pass, q, Tm, lane) : 0;
       if (lane == 0) ring[0].co[w] = v;
     }
-    if (threadIdx.x == 0) ring[0].q0 = q0, ring[0].cnt = cnt;
+    if (threadIdx.x == 0) ring[0].q0 = q0, ring[0].cnt = cnt, ring[0].pass = pass;
   }
   __syncthreads();
 #ifdef MSORT_K3_TRACE
@@ -191,7 +336,7 @@ __global__ void __launch_bounds__(NC + 64, MINB)
     for (int64_t g = 0; !done; ++g) {
       if (g > 0) {
         int64_t c = 0;
-        if (lane == 0) c = (int64_t)(atomicAdd(ctr, (unsigned long long)kGrab) - base);
+        if (lane == 0) c = (int64_t)atomicAdd(ctr, (unsigned long long)kGrab);
         c0 = __shfl_sync(0xffffffffu, c, 0);
       }
       const int m = lane / (CH + 1), j = lane % (CH + 1);
@@ -200,18 +345,28 @@ __global__ void __launch_bounds__(NC + 64, MINB)
         const int r = (int)(b % R);
         mbar_wait(&sempty[r], (uint32_t)(((b / R) & 1) ^ 1));
       }
-      // every lane searches its co-rank (if any) of this grab
-      int64_t v = 0;
+      // the chunks of this grab in order; the whole warp waits for each one's
+      // inputs, then every lane searches its co-rank (if any)
+      int passm = 0, cntm = 0;
+      int64_t q0m = 0;
       const int64_t cm = c0 + m;
       const bool mine = m < kGrab && !(g == 0 && m == 0) && cm < nchunks;
-      int cntm = 0;
-      if (m < kGrab && cm < nchunks) cntm = (int)min((int64_t)CH, ntiles - cm * CH);
+      for (int mm = (g == 0 ? 1 : 0); mm < kGrab; ++mm) {
+        if (c0 + mm >= nchunks) break;
+        int p_, c_;
+        int64_t q_;
+        src.chunk(c0 + mm, p_, q_, c_);
+        src.wait_ready(p_, q_, c_, lane, Tm);
+        if (m == mm) passm = p_, q0m = q_, cntm = c_;
+      }
+      int64_t v = 0;
       if (mine && j <= cntm) {
-        const int64_t q = cm * CH + j;
-        if (q < ntiles) {
+        const int64_t q = q0m + j;
+        if (q < src.tiles(passm)) {
           int64_t A0, na, nb, dl;
-          pm.locate(q, Tm, A0, na, nb, dl);
-          v = merge_path_global(src_k + A0, na, src_k + A0 + na, nb, dl);
+          src.locate(passm, q, Tm, A0, na, nb, dl);
+          const K* sk = src.srck(passm);
+          v = merge_path_global(sk + A0, na, sk + A0 + na, nb, dl);
         }
       }
       for (int mm = (g == 0 ? 1 : 0); mm < kGrab; ++mm) {
@@ -220,8 +375,10 @@ __global__ void __launch_bounds__(NC + 64, MINB)
         if (m == mm && mine && j <= cntm) ring[r].co[j] = v;
         if (lane == 0) {
           if (cmm < nchunks) {
-            ring[r].q0 = cmm * CH;
-            ring[r].cnt = (int)min((int64_t)CH, ntiles - cmm * CH);
+            int p_, c_;
+            int64_t q_;
+            src.chunk(cmm, p_, q_, c_);
+            ring[r].q0 = q_, ring[r].cnt = c_, ring[r].pass = p_;
           } else {
             ring[r].cnt = 0;  // end of work: the producer stops at this slot
           }
@@ -239,6 +396,7 @@ __global__ void __launch_bounds__(NC + 64, MINB)
       mbar_wait(&sfull[r], (uint32_t)((b / R) & 1));
       const ChunkDesc& cd = ring[r];
       const int ccnt = cd.cnt;
+      const int pass = cd.pass;
       if (ccnt == 0) {
         // no more chunks: tell the mergers to stop
         const int s = (int)(k % S);
@@ -247,11 +405,16 @@ __global__ void __launch_bounds__(NC + 64, MINB)
         mbar_arrive(&full[s]);
         break;
       }
+      // inputs written by other SMs (generic or bulk stores) were acquired by
+      // the searcher; order them before this thread's bulk (async-proxy) loads
+      if constexpr (Src::kFused) fence_proxy_async_global();
+      const K* src_k = src.srck(pass);
+      const uint32_t* src_v = src.srcv(pass);
       for (int j = 0; j < ccnt; ++j, ++k) {
         const int64_t q = cd.q0 + j;
         const int s = (int)(k % S);
         int64_t A0, na_all, nb_all, d0;
-        pm.locate(q, Tm, A0, na_all, nb_all, d0);
+        src.locate(pass, q, Tm, A0, na_all, nb_all, d0);
         const int64_t tot_all = na_all + nb_all;
         const int64_t d1 = min(d0 + Tm, tot_all);
         const int64_t i0 = cd.co[j];
@@ -264,9 +427,9 @@ __global__ void __launch_bounds__(NC + 64, MINB)
         const int offB = (offA + na + EK - 1) / EK * EK + stage_offset(bp);
         K3_CHECK(i0 >= 0 && i0 <= i1 && i1 <= na_all && j0 >= 0 && j0 <= j1 && j1 <= nb_all &&
                      offB + nb <= LY::SKE && na + nb <= Tm,
-                 "q %lld b %lld j %d ccnt %d q0 %lld i0 %lld i1 %lld na_all %lld nb_all %lld d0 %lld\n",
-                 (long long)q, (long long)b, j, ccnt, (long long)cd.q0, (long long)i0,
-                 (long long)i1, (long long)na_all, (long long)nb_all, (long long)d0);
+                 "pass %d q %lld j %d ccnt %d i0 %lld i1 %lld na_all %lld nb_all %lld d0 %lld\n",
+                 pass, (long long)q, j, ccnt, (long long)i0, (long long)i1, (long long)na_all,
+                 (long long)nb_all, (long long)d0);
         const uint32_t* av = nullptr;
         const uint32_t* bv = nullptr;
         int offAv = 0, offBv = 0;
@@ -290,7 +453,7 @@ __global__ void __launch_bounds__(NC + 64, MINB)
         K* sk = stk + (size_t)s * LY::SKE;
         uint32_t* sv = stv + (size_t)s * LY::SVE;
         if (lane == 0) {
-          meta[s] = TileMeta{A0 + d0, na, nb, offA, offB, offAv, offBv, na + nb, 0};
+          meta[s] = TileMeta{A0 + d0, q, na, nb, offA, offB, offAv, offBv, na + nb, pass};
           uint32_t tx = window_bulk_bytes(a, na) + window_bulk_bytes(bp, nb);
           if constexpr (PAIRS) tx += window_bulk_bytes(av, na) + window_bulk_bytes(bv, nb);
           mbar_expect_tx(&full[s], tx);  // before the copies that complete it
@@ -310,7 +473,8 @@ __global__ void __launch_bounds__(NC + 64, MINB)
   } else {
     // ------------------------------------------------------------ mergers
     const int ct = threadIdx.x - 64;  // 0..NC-1
-    int prev_s = -1;
+    int prev_s = -1, prev_pass = 0;
+    int64_t prev_q = 0;
     for (int64_t k = 0;; ++k) {
       const int s = (int)(k % S);
 #ifdef MSORT_K3_TRACE
@@ -365,17 +529,22 @@ __global__ void __launch_bounds__(NC + 64, MINB)
       // the previous tile's head/tail stores (so that stage can be recycled)
       named_bar_sync(1, NC);
       if (ct == 0 && prev_s >= 0) {
-        bulk_wait_read<0>();         // the previous tile's bulk store has read it
-        mbar_arrive(&empty[prev_s]);  // ... so it goes back to the producer
+        if constexpr (Src::kFused) {
+          bulk_wait_all();  // the previous tile's bulk store has completed
+          src.tile_done(prev_pass, prev_q, Tm);
+        } else {
+          bulk_wait_read<0>();  // the previous tile's bulk store has read it
+        }
+        mbar_arrive(&empty[prev_s]);  // ... so its stage goes back to the producer
       }
       // The output keeps its global 16-byte phase so the aligned middle leaves
       // by one bulk store (TMA, cp.async.bulk.global.shared).
-      K* gk = dst_k + m.out;
+      K* gk = src.dstk(m.pass) + m.out;
       const int phk = stage_offset(gk);
       uint32_t* gv = nullptr;
       int phv = 0;
       if constexpr (PAIRS) {
-        gv = dst_v + m.out;
+        gv = src.dstv(m.pass) + m.out;
         phv = stage_offset(gv);
       }
 #pragma unroll
@@ -407,11 +576,18 @@ __global__ void __launch_bounds__(NC + 64, MINB)
           gv[j] = sv[phv + j];
         }
       prev_s = s;
+      prev_pass = m.pass;
+      prev_q = m.q;
 #ifdef MSORT_K3_TRACE
       ++ntile_done;
 #endif
     }
-    if (ct == 0) bulk_wait_all();
+    named_bar_sync(1, NC);  // the last tile's head/tail stores are done
+    if (ct == 0) {
+      bulk_wait_all();
+      if constexpr (Src::kFused)
+        if (prev_s >= 0) src.tile_done(prev_pass, prev_q, Tm);
+    }
 #ifdef MSORT_K3_TRACE
     if (ct == 0) K3_TRACE(4, gtimer() - t_start), K3_TRACE(6, t_wait), K3_TRACE(5, ntile_done);
 #endif

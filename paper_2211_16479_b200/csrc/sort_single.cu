@@ -25,41 +25,6 @@
 
 namespace msort {
 
-// ---------------------------------------------------------------- pair maps
-// Where output tile q sits: its run pair starts at A0 (global index), run A
-// has na elements, run B (immediately after A) nb, and the tile's first
-// output diagonal is dl inside the pair.  The pair's output occupies
-// [A0, A0+na+nb) of the destination.
-struct UniformPairs {  // runs of length L (the last ones may be short)
-  int64_t n, L;
-  __device__ __forceinline__ void locate(int64_t q, int T, int64_t& A0, int64_t& na,
-                                         int64_t& nb, int64_t& dl) const {
-    int64_t d = q * T;
-    int64_t m = d / (2 * L);
-    A0 = m * 2 * L;
-    na = min(L, n - A0);
-    int64_t B0 = A0 + L;
-    nb = B0 < n ? min(L, n - B0) : 0;
-    dl = d - A0;
-  }
-};
-
-constexpr int kMaxPairs = 64;
-struct ExplicitPairs {  // arbitrary consecutive runs, pairs (2m, 2m+1)
-  int npairs;
-  int64_t first_tile[kMaxPairs + 1];
-  int64_t off[2 * kMaxPairs + 1];
-  __device__ __forceinline__ void locate(int64_t q, int T, int64_t& A0, int64_t& na,
-                                         int64_t& nb, int64_t& dl) const {
-    int m = 0;
-    while (m + 1 < npairs && first_tile[m + 1] <= q) ++m;
-    A0 = off[2 * m];
-    na = off[2 * m + 1] - A0;
-    nb = off[2 * m + 2] - off[2 * m + 1];
-    dl = (q - first_tile[m]) * T;
-  }
-};
-
 // ----------------------------------------------------------------- K1
 // NT threads x VT items (VT odd: "blocked" shared accesses at stride VT are
 // bank-conflict free without padding).
@@ -148,6 +113,10 @@ extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
 #define MSORT_K3_VT 17  // outputs per merging thread (even: two chains per thread)
 #endif
 
+// Scheduler state in the workspace: 64 chunk counters (one per launch of a
+// sort) then the per-level, per-pair completion counters of the fused merge.
+constexpr int kMaxLaunches = 64;
+
 template <class K, bool PAIRS>
 struct Kernels {
   static constexpr int VT = 17;  // odd: conflict-free blocked shared accesses
@@ -164,10 +133,20 @@ struct Kernels {
   static constexpr size_t k1_smem = (size_t)T * sizeof(K) + (PAIRS ? (size_t)T * 8 : 0);
   static constexpr size_t k3_smem = LY::bytes;
   static_assert((2 * T) % Tm == 0, "pair boundaries must be tile boundaries");
+  using Fused = FusedPasses<K>;
+  using Explicit = SinglePass<K, ExplicitPairs>;
 
   static int& grid3(int dev) {
     static int g[64] = {};
     return g[dev & 63];
+  }
+
+  template <class Src>
+  static msort_status set_smem() {
+    auto k = k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, Src>;
+    MSORT_CUDA_TRY(
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3_smem));
+    return MSORT_SUCCESS;
   }
 
   static msort_status init() {
@@ -177,56 +156,42 @@ struct Kernels {
     MSORT_CUDA_TRY(cudaFuncSetAttribute(k1_tile_sort<K, PAIRS, NT1, VT>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)k1_smem));
-    auto ku = k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, UniformPairs>;
-    auto ke = k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, ExplicitPairs>;
-    MSORT_CUDA_TRY(cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)k3_smem));
-    MSORT_CUDA_TRY(cudaFuncSetAttribute(ke, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)k3_smem));
+    MSORT_TRY(set_smem<Fused>());
+    MSORT_TRY(set_smem<Explicit>());
     int sms = 0, occ = 0;
     MSORT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    MSORT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ku, NC + 64, k3_smem));
+    MSORT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, Fused>, NC + 64, k3_smem));
     if (occ < 1) {
       set_error("merge pass kernel does not fit on an SM");
       return MSORT_ERROR_NOT_SUPPORTED;
     }
+    // every CTA of the persistent merge kernel must be resident (the fused
+    // levels wait on each other's progress): grid = SMs x occupancy
     grid3(dev) = sms * occ;
     return MSORT_SUCCESS;
   }
 
-  // Dynamic chunk scheduling: one 64-bit counter per merge pass in the
-  // workspace (kMaxPasses of them), all zeroed by one memset per sort.
-  static constexpr int kMaxPasses = 64;
-  struct Sched {
-    unsigned long long* ctr;
-    unsigned long long base;  // always 0: each pass has its own counter
-  };
-
-  template <class PM>
-  static msort_status merge_pass(const K* sk, const uint32_t* sv, K* dk, uint32_t* dv,
-                                 const PM& pm, int64_t ntiles, cudaStream_t s, KernelClass kc,
-                                 Sched& sc) {
+  template <class Src>
+  static msort_status launch_k3(const Src& src, int64_t nchunks, unsigned long long* ctr,
+                                cudaStream_t s, KernelClass kc) {
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
-    const int64_t nchunks = (ntiles + kChunk - 1) / kChunk;
     const int64_t grid = std::min<int64_t>(grid3(dev), (nchunks + kGrab - 1) / kGrab);
     {
       LaunchScope ls(kc, s);
-      k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, PM>
-          <<<(unsigned)grid, NC + 64, k3_smem, s>>>(sk, sv, dk, dv, pm, ntiles, sc.ctr, 0ull);
+      k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, Src>
+          <<<(unsigned)grid, NC + 64, k3_smem, s>>>(src, ctr);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
 #ifdef MSORT_K3_CHECK
-    {
-      cudaError_t e = cudaStreamSynchronize(s);
-      if (e != cudaSuccess) {
-        fprintf(stderr, "K3 pass failed: ntiles %lld grid %lld: %s\n", (long long)ntiles,
-                (long long)grid, cudaGetErrorString(e));
-        return cuda_fail(e, "k3 (debug sync)");
-      }
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "K3 failed: chunks %lld grid %lld: %s\n", (long long)nchunks,
+              (long long)grid, cudaGetErrorString(e));
+      return cuda_fail(e, "k3 (debug sync)");
     }
 #endif
-    ++sc.ctr;  // the next pass uses the next counter
     return MSORT_SUCCESS;
   }
 
@@ -246,6 +211,10 @@ struct Kernels {
     const int64_t ntiles = (int64_t)((n + T - 1) / T);
     int passes = 0;
     while ((int64_t(1) << passes) < ntiles) ++passes;
+    if (passes > kMaxFusedPasses) {
+      set_error("too many merge levels");
+      return MSORT_ERROR_NOT_SUPPORTED;
+    }
     char* w = static_cast<char*>(ws);
     K* wk = reinterpret_cast<K*>(w);
     w += align_up(n * sizeof(K), 256);
@@ -254,9 +223,9 @@ struct Kernels {
       wv = reinterpret_cast<uint32_t*>(w);
       w += align_up(n * sizeof(uint32_t), 256);
     }
-    Sched sc{reinterpret_cast<unsigned long long*>(w), 0};
+    auto* ctr = reinterpret_cast<unsigned long long*>(w);
+    auto* done = reinterpret_cast<unsigned*>(ctr + kMaxLaunches);
     (void)ws_bytes;
-    MSORT_CUDA_TRY(cudaMemsetAsync(sc.ctr, 0, kMaxPasses * sizeof(unsigned long long), s));
 
     K* bk[2] = {keys, wk};
     uint32_t* bv[2] = {vals, wv};
@@ -274,14 +243,22 @@ struct Kernels {
       if (e != cudaSuccess) return cuda_fail(e, "k1 (debug sync)");
     }
 #endif
-    const int64_t mtiles = (int64_t)((n + Tm - 1) / Tm);
-    for (int64_t L = T; L < (int64_t)n; L *= 2) {
-      UniformPairs pm{(int64_t)n, L};
-      MSORT_TRY(merge_pass(bk[cur], bv[cur], bk[cur ^ 1], bv[cur ^ 1], pm, mtiles, s, KC_MERGE,
-                           sc));
-      cur ^= 1;
+    if (passes == 0) return MSORT_SUCCESS;
+    // All merge levels in one dataflow launch (k3_merge.cuh, FusedPasses).
+    Fused f{};
+    f.bk[0] = bk[cur], f.bk[1] = bk[cur ^ 1];
+    f.bv[0] = bv[cur], f.bv[1] = bv[cur ^ 1];
+    f.n = (int64_t)n, f.T = T, f.ntiles = (int64_t)((n + Tm - 1) / Tm), f.P = passes;
+    f.done = done;
+    int64_t pb = 0;
+    for (int p = 0; p < passes; ++p) {
+      f.pair_base[p] = pb;
+      const int64_t twoL = (int64_t)2 * T << p;
+      pb += ((int64_t)n + twoL - 1) / twoL;
     }
-    return MSORT_SUCCESS;
+    f.pair_base[passes] = pb;
+    MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * 8 + pb * 4, s));
+    return launch_k3(f, (int64_t)passes * ((f.ntiles + kChunk - 1) / kChunk), ctr, s, KC_MERGE);
   }
 
   // Merge `runs` consecutive runs src[off[r], off[r+1]) into dst with rounds of
@@ -291,7 +268,6 @@ struct Kernels {
                            uint32_t* dst_v, const int64_t* off_in, int runs,
                            unsigned long long* ctr, cudaStream_t s) {
     MSORT_TRY(init());
-    Sched sc{ctr, 0};
     const int64_t n = off_in[runs] - off_in[0];
     if (runs <= 1 || n == 0) {
       if (n > 0 && src_k != dst_k) {
@@ -309,7 +285,7 @@ struct Kernels {
     }
     int rounds = 0;
     while ((1 << rounds) < runs) ++rounds;
-    MSORT_CUDA_TRY(cudaMemsetAsync(sc.ctr, 0, kMaxPasses * sizeof(unsigned long long), s));
+    MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * sizeof(unsigned long long), s));
     // Ping-pong src -> (tmp|dst) ... so that the last round writes dst.
     int64_t off[2 * kMaxPairs + 2];
     for (int r = 0; r <= runs; ++r) off[r] = off_in[r] - off_in[0];
@@ -320,7 +296,8 @@ struct Kernels {
       const bool to_dst = ((rounds - 1 - round) % 2) == 0;
       K* nk = to_dst ? dst_k : tmp_k;
       uint32_t* nv = to_dst ? dst_v : tmp_v;
-      ExplicitPairs pm{};
+      Explicit src{};
+      ExplicitPairs& pm = src.pm;
       pm.npairs = (runs + 1) / 2;
       int64_t tiles = 0;
       for (int m = 0; m < pm.npairs; ++m) {
@@ -333,9 +310,11 @@ struct Kernels {
         tiles += (e - a + Tm - 1) / Tm;
       }
       pm.first_tile[pm.npairs] = tiles;
+      src.src_k = ck, src.src_v = cv, src.dst_k = nk, src.dst_v = nv, src.ntiles = tiles;
       // empty pairs own no tiles; locate() picks the last pair whose first
       // tile <= q, which is never an empty one
-      if (tiles > 0) MSORT_TRY(merge_pass(ck, cv, nk, nv, pm, tiles, s, KC_KWAY, sc));
+      if (tiles > 0)
+        MSORT_TRY(launch_k3(src, (tiles + kChunk - 1) / kChunk, ctr + round, s, KC_KWAY));
       int nr = pm.npairs;
       for (int m = 0; m <= nr; ++m) off[m] = off[std::min(2 * m, runs)];
       runs = nr;
