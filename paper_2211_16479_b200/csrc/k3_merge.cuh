@@ -345,47 +345,60 @@ __global__ void __launch_bounds__(NC + 64, MINB)
         const int r = (int)(b % R);
         mbar_wait(&sempty[r], (uint32_t)(((b / R) & 1) ^ 1));
       }
-      // the chunks of this grab in order; the whole warp waits for each one's
-      // inputs, then every lane searches its co-rank (if any)
-      int passm = 0, cntm = 0;
-      int64_t q0m = 0;
-      const int64_t cm = c0 + m;
-      const bool mine = m < kGrab && !(g == 0 && m == 0) && cm < nchunks;
-      for (int mm = (g == 0 ? 1 : 0); mm < kGrab; ++mm) {
-        if (c0 + mm >= nchunks) break;
-        int p_, c_;
-        int64_t q_;
-        src.chunk(c0 + mm, p_, q_, c_);
-        src.wait_ready(p_, q_, c_, lane, Tm);
-        if (m == mm) passm = p_, q0m = q_, cntm = c_;
-      }
-      int64_t v = 0;
-      if (mine && j <= cntm) {
-        const int64_t q = q0m + j;
-        if (q < src.tiles(passm)) {
-          int64_t A0, na, nb, dl;
-          src.locate(passm, q, Tm, A0, na, nb, dl);
-          const K* sk = src.srck(passm);
-          v = merge_path_global(sk + A0, na, sk + A0 + na, nb, dl);
+      // The grab's chunks in order, in groups of the same merge level: a later
+      // level may read an earlier chunk of this very grab, so each group is
+      // published before the next one waits for its inputs.
+      int mm0 = g == 0 ? 1 : 0;
+      while (mm0 < kGrab && !done) {
+        if (c0 + mm0 >= nchunks) {
+          const int r = (int)((g * kGrab + mm0) % R);
+          if (lane == 0) ring[r].cnt = 0;  // end of work: the producer stops here
+          mbar_arrive(&sfull[r]);
+          done = true;
+          break;
         }
-      }
-      for (int mm = (g == 0 ? 1 : 0); mm < kGrab; ++mm) {
-        const int r = (int)((g * kGrab + mm) % R);
-        const int64_t cmm = c0 + mm;
-        if (m == mm && mine && j <= cntm) ring[r].co[j] = v;
-        if (lane == 0) {
-          if (cmm < nchunks) {
-            int p_, c_;
-            int64_t q_;
-            src.chunk(cmm, p_, q_, c_);
-            ring[r].q0 = q_, ring[r].cnt = c_, ring[r].pass = p_;
-          } else {
-            ring[r].cnt = 0;  // end of work: the producer stops at this slot
+        int pass0, cnt_;
+        int64_t q_;
+        src.chunk(c0 + mm0, pass0, q_, cnt_);
+        int mm1 = mm0 + 1;
+        while (mm1 < kGrab && c0 + mm1 < nchunks) {
+          int p_, c_;
+          int64_t q2;
+          src.chunk(c0 + mm1, p_, q2, c_);
+          if (p_ != pass0) break;
+          ++mm1;
+        }
+        for (int mm = mm0; mm < mm1; ++mm) {
+          int p_, c_;
+          int64_t q2;
+          src.chunk(c0 + mm, p_, q2, c_);
+          src.wait_ready(p_, q2, c_, lane, Tm);
+        }
+        int64_t v = 0;
+        int cntm = 0;
+        int64_t q0m = 0;
+        if (m >= mm0 && m < mm1) {
+          int p_;
+          src.chunk(c0 + m, p_, q0m, cntm);
+          if (j <= cntm && q0m + j < src.tiles(pass0)) {
+            int64_t A0, na, nb, dl;
+            src.locate(pass0, q0m + j, Tm, A0, na, nb, dl);
+            const K* sk = src.srck(pass0);
+            v = merge_path_global(sk + A0, na, sk + A0 + na, nb, dl);
           }
         }
-        if (cmm >= nchunks) done = true;
-        mbar_arrive(&sfull[r]);
-        if (done) break;
+        for (int mm = mm0; mm < mm1; ++mm) {
+          const int r = (int)((g * kGrab + mm) % R);
+          if (m == mm && j <= cntm) ring[r].co[j] = v;
+          if (lane == 0) {
+            int p_, c_;
+            int64_t q2;
+            src.chunk(c0 + mm, p_, q2, c_);
+            ring[r].q0 = q2, ring[r].cnt = c_, ring[r].pass = p_;
+          }
+          mbar_arrive(&sfull[r]);
+        }
+        mm0 = mm1;
       }
     }
   } else if (warp == 0) {
