@@ -488,8 +488,18 @@ __global__ void __launch_bounds__(NC + 64, MINB)
     const int ct = threadIdx.x - 64;  // 0..NC-1
     int prev_s = -1, prev_pass = 0;
     int64_t prev_q = 0;
+    bool pending = false;  // ct 0: a stored tile whose completion is not yet published
     for (int64_t k = 0;; ++k) {
       const int s = (int)(k % S);
+      if constexpr (Src::kFused) {
+        // Never sit on an unpublished tile while waiting: another chunk (maybe
+        // this CTA's own next one) may be waiting for it.
+        if (ct == 0 && pending && !mbar_test(&full[s], (uint32_t)((k / S) & 1))) {
+          bulk_wait_all();
+          src.tile_done(prev_pass, prev_q, Tm);
+          pending = false;
+        }
+      }
 #ifdef MSORT_K3_TRACE
       const unsigned long long tw0 = gtimer();
 #endif
@@ -544,7 +554,8 @@ __global__ void __launch_bounds__(NC + 64, MINB)
       if (ct == 0 && prev_s >= 0) {
         if constexpr (Src::kFused) {
           bulk_wait_all();  // the previous tile's bulk store has completed
-          src.tile_done(prev_pass, prev_q, Tm);
+          if (pending) src.tile_done(prev_pass, prev_q, Tm);
+          pending = false;
         } else {
           bulk_wait_read<0>();  // the previous tile's bulk store has read it
         }
@@ -574,20 +585,23 @@ __global__ void __launch_bounds__(NC + 64, MINB)
       int hv = 0, mv = 0;
       if constexpr (PAIRS) window_split(gv, m.tot, hv, mv);
       if (ct == 0) {
+        // one thread writes the whole tile (bulk middle + <16-byte head and
+        // tail), so its completion can be published by that thread alone
         if (mk) bulk_s2g(gk + hk, sk + phk + hk, (uint32_t)(mk * sizeof(K)));
         if constexpr (PAIRS)
           if (mv) bulk_s2g(gv + hv, sv + phv + hv, (uint32_t)(mv * 4));
         bulk_commit();
-      }
-      for (int i = ct; i < m.tot - mk; i += NC) {
-        const int j = i < hk ? i : i + mk;
-        gk[j] = sk[phk + j];
-      }
-      if constexpr (PAIRS)
-        for (int i = ct; i < m.tot - mv; i += NC) {
-          const int j = i < hv ? i : i + mv;
-          gv[j] = sv[phv + j];
+        for (int i = 0; i < m.tot - mk; ++i) {
+          const int j = i < hk ? i : i + mk;
+          gk[j] = sk[phk + j];
         }
+        if constexpr (PAIRS)
+          for (int i = 0; i < m.tot - mv; ++i) {
+            const int j = i < hv ? i : i + mv;
+            gv[j] = sv[phv + j];
+          }
+        pending = true;
+      }
       prev_s = s;
       prev_pass = m.pass;
       prev_q = m.q;
@@ -595,11 +609,10 @@ __global__ void __launch_bounds__(NC + 64, MINB)
       ++ntile_done;
 #endif
     }
-    named_bar_sync(1, NC);  // the last tile's head/tail stores are done
     if (ct == 0) {
       bulk_wait_all();
       if constexpr (Src::kFused)
-        if (prev_s >= 0) src.tile_done(prev_pass, prev_q, Tm);
+        if (pending) src.tile_done(prev_pass, prev_q, Tm);
     }
 #ifdef MSORT_K3_TRACE
     if (ct == 0) K3_TRACE(4, gtimer() - t_start), K3_TRACE(6, t_wait), K3_TRACE(5, ntile_done);
