@@ -264,25 +264,28 @@ def main():
         dist.all_reduce(okt, op=dist.ReduceOp.MIN)
         ok = bool(okt.item())
 
-    # roofline of the dominant kernel (the merge pass) from live CUDA events
+    # roofline of the dominant kernel (the merge kernel) from live CUDA events
     peak, peak_src = load_peaks()
     mp_launches, mp_ms = prof["merge_pass"]
     wk = 4
-    alg_bytes = 2 * n * wk  # each merge pass reads and writes every key once
+    alg_bytes = 2 * n * wk  # each merge level reads and writes every key once
+    tile = ms.tile_size(ms.MSORT_INT32, ms.MSORT_NONE)
+    ntiles = (n + tile - 1) // tile
+    passes = (ntiles - 1).bit_length()  # merge levels per sort
     roof = None
     if mp_launches:
+        # the merge kernel runs all `passes` levels of a sort in one launch
+        per_launch = alg_bytes * passes * args.steps / mp_launches
         avg_s = mp_ms / mp_launches / 1e3
-        ach = alg_bytes / avg_s / 1e9
+        ach = per_launch / avg_s / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": ncu_traffic(f"C5_n{n}"),
-                "kernel": "k3_merge_pass", "algorithmic_bytes_per_launch": alg_bytes,
+                "kernel": "k3_merge_pass", "algorithmic_bytes_per_launch": int(per_launch),
+                "merge_levels_per_launch": passes * args.steps / mp_launches,
                 "launches": mp_launches, "avg_launch_ms": round(mp_ms / mp_launches, 4),
                 "peak_source": peak_src}
     phases = {k: {"launches_per_step": v[0] / args.steps, "ms_per_step": round(v[1] / args.steps, 4)}
               for k, v in prof.items() if v[0]}
-    tile = ms.tile_size(ms.MSORT_INT32, ms.MSORT_NONE)
-    ntiles = (n + tile - 1) // tile
-    passes = (ntiles - 1).bit_length()
     # whole-step roofline: bytes of every executed pass at HBM rate (+ NVLink)
     step_bytes = (passes + 1) * alg_bytes
     t_roof = step_bytes / (peak * 1e9)

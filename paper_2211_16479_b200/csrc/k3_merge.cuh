@@ -488,16 +488,21 @@ __global__ void __launch_bounds__(NC + 64, MINB)
     const int ct = threadIdx.x - 64;  // 0..NC-1
     int prev_s = -1, prev_pass = 0;
     int64_t prev_q = 0;
-    bool pending = false;  // ct 0: a stored tile whose completion is not yet published
+    // ct 0: stored tiles whose completion is not yet published, newest first
+    // (their bulk stores are waited for lazily, one tile behind)
+    bool pend1 = false, pend2 = false;
+    int pass1 = 0, pass2 = 0;
+    int64_t q1 = 0, q2 = 0;
     for (int64_t k = 0;; ++k) {
       const int s = (int)(k % S);
       if constexpr (Src::kFused) {
         // Never sit on an unpublished tile while waiting: another chunk (maybe
         // this CTA's own next one) may be waiting for it.
-        if (ct == 0 && pending && !mbar_test(&full[s], (uint32_t)((k / S) & 1))) {
+        if (ct == 0 && (pend1 || pend2) && !mbar_test(&full[s], (uint32_t)((k / S) & 1))) {
           bulk_wait_all();
-          src.tile_done(prev_pass, prev_q, Tm);
-          pending = false;
+          if (pend2) src.tile_done(pass2, q2, Tm);
+          if (pend1) src.tile_done(pass1, q1, Tm);
+          pend1 = pend2 = false;
         }
       }
 #ifdef MSORT_K3_TRACE
@@ -552,14 +557,15 @@ __global__ void __launch_bounds__(NC + 64, MINB)
       // the previous tile's head/tail stores (so that stage can be recycled)
       named_bar_sync(1, NC);
       if (ct == 0 && prev_s >= 0) {
-        if constexpr (Src::kFused) {
-          bulk_wait_all();  // the previous tile's bulk store has completed
-          if (pending) src.tile_done(prev_pass, prev_q, Tm);
-          pending = false;
-        } else {
-          bulk_wait_read<0>();  // the previous tile's bulk store has read it
-        }
+        bulk_wait_read<0>();          // the previous tile's bulk store has read it
         mbar_arrive(&empty[prev_s]);  // ... so its stage goes back to the producer
+        if constexpr (Src::kFused) {
+          if (pend2) {
+            bulk_wait<1>();  // all but the newest store complete: publish the older
+            src.tile_done(pass2, q2, Tm);
+            pend2 = false;
+          }
+        }
       }
       // The output keeps its global 16-byte phase so the aligned middle leaves
       // by one bulk store (TMA, cp.async.bulk.global.shared).
@@ -600,7 +606,8 @@ __global__ void __launch_bounds__(NC + 64, MINB)
             const int j = i < hv ? i : i + mv;
             gv[j] = sv[phv + j];
           }
-        pending = true;
+        if (pend1) pend2 = true, pass2 = pass1, q2 = q1;
+        pend1 = true, pass1 = m.pass, q1 = m.q;
       }
       prev_s = s;
       prev_pass = m.pass;
@@ -611,8 +618,10 @@ __global__ void __launch_bounds__(NC + 64, MINB)
     }
     if (ct == 0) {
       bulk_wait_all();
-      if constexpr (Src::kFused)
-        if (pending) src.tile_done(prev_pass, prev_q, Tm);
+      if constexpr (Src::kFused) {
+        if (pend2) src.tile_done(pass2, q2, Tm);
+        if (pend1) src.tile_done(pass1, q1, Tm);
+      }
     }
 #ifdef MSORT_K3_TRACE
     if (ct == 0) K3_TRACE(4, gtimer() - t_start), K3_TRACE(6, t_wait), K3_TRACE(5, ntile_done);

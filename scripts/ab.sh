@@ -8,7 +8,7 @@ lib,out=sys.argv[1],sys.argv[2]
 try:
     d=json.loads(out)
     ph=d["phases"]
-    print(f"{lib.split('/')[-1]:28s} ms/step={d['ms_per_step']:.3f} Gk/s={d['value']/1e9:.2f} merge={ph['merge_pass']['ms_per_step']/ph['merge_pass']['launches_per_step']:.4f} tile={ph['tile_sort']['ms_per_step']:.3f} frac={d['roofline']['frac']} ok={d['verified']}")
+    print(f"{lib.split('/')[-1]:28s} ms/step={d['ms_per_step']:.3f} Gk/s={d['value']/1e9:.2f} merge_total={ph['merge_pass']['ms_per_step']:.4f} per_level={ph['merge_pass']['ms_per_step']/d['config']['merge_passes']:.4f} tile={ph['tile_sort']['ms_per_step']:.3f} frac={d['roofline']['frac']} ok={d['verified']}")
 except Exception as e:
     print(lib, "FAILED", out[:300])
 PY
