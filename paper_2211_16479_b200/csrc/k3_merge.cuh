@@ -95,8 +95,8 @@ struct K3Layout {
   static constexpr int R = 2 * kGrab;      // chunk ring: two searcher rounds
   static constexpr int SKE = Tm + 4 * EK;  // keys per stage (windows + phase slack)
   static constexpr int SVE = Tm + 16;      // payloads per stage
-  static constexpr size_t bars = 0;        // full[S], empty[S], sfull[R], sempty[R]
-  static constexpr size_t meta = align_up_c(8 * (2 * S + 2 * R), 16);
+  static constexpr size_t bars = 0;  // full[S], empty[S], sfull[R], sempty[R], outr[S]
+  static constexpr size_t meta = align_up_c(8 * (3 * S + 2 * R), 16);
   static constexpr size_t ring = align_up_c(meta + sizeof(TileMeta) * S, 16);
   static constexpr size_t corank = ring + sizeof(ChunkDesc) * R;  // NC+1 ints
   static constexpr size_t misc = align_up_c(corank + 4 * (NC + 1), 16);
@@ -200,8 +200,9 @@ struct FusedPasses {
   // Called by one thread after the tile's output (bulk store waited for,
   // scalar stores ordered by a CTA barrier) is complete.
   __device__ __forceinline__ void tile_done(int pass, int64_t q, int Tm) const {
+#ifndef MSORT_K3_NOPROXYFENCE
     fence_proxy_async_global();
-    __threadfence();
+#endif
     red_release_gpu_add(done + pair_base[pass] + pair_of(pass, q, Tm), 1u);
   }
 };
@@ -265,17 +266,20 @@ __device__ __forceinline__ int64_t corank_warp(const Src& src, int pass, int64_t
   return lo;
 }
 
+constexpr int kK3Extra = 96;  // producer, searcher and store warps
+
 template <class K, bool PAIRS, int NC, int VT, int S, int MINB, class Src>
-__global__ void __launch_bounds__(NC + 64, MINB)
+__global__ void __launch_bounds__(NC + kK3Extra, MINB)
     k3_merge_pass(const __grid_constant__ Src src, unsigned long long* __restrict__ ctr) {
   using LY = K3Layout<K, PAIRS, NC, VT, S>;
   constexpr int Tm = LY::Tm, EK = LY::EK, R = LY::R, CH = kChunk;
-  constexpr int NW = (NC + 64) / 32;  // warps per CTA
+  constexpr int NW = (NC + kK3Extra) / 32;  // warps per CTA
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + LY::bars);
   uint64_t* empty = full + S;
   uint64_t* sfull = empty + S;
   uint64_t* sempty = sfull + R;
+  uint64_t* outr = sempty + R;  // output tile of stage s written, ready to store
   TileMeta* meta = reinterpret_cast<TileMeta*>(smem + LY::meta);
   ChunkDesc* ring = reinterpret_cast<ChunkDesc*>(smem + LY::ring);
   int* corank = reinterpret_cast<int*>(smem + LY::corank);
@@ -294,7 +298,8 @@ __global__ void __launch_bounds__(NC + 64, MINB)
   if (threadIdx.x == 0) K3_TRACE(0, t_start);
 #endif
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&full[s], 32), mbar_init(&empty[s], 1);
+    for (int s = 0; s < S; ++s)
+      mbar_init(&full[s], 32), mbar_init(&empty[s], 1), mbar_init(&outr[s], NC / 32);
     for (int r = 0; r < R; ++r) mbar_init(&sfull[r], 32), mbar_init(&sempty[r], 1);
     fence_mbar_init();
     *first_chunk = (int64_t)atomicAdd(ctr, (unsigned long long)kGrab);
@@ -483,28 +488,75 @@ __global__ void __launch_bounds__(NC + 64, MINB)
 #ifdef MSORT_K3_TRACE
     if (lane == 0) K3_TRACE(7, t_wait);
 #endif
-  } else {
-    // ------------------------------------------------------------ mergers
-    const int ct = threadIdx.x - 64;  // 0..NC-1
-    int prev_s = -1, prev_pass = 0;
-    int64_t prev_q = 0;
-    // ct 0: stored tiles whose completion is not yet published, newest first
-    // (their bulk stores are waited for lazily, one tile behind)
-    bool pend1 = false, pend2 = false;
-    int pass1 = 0, pass2 = 0;
-    int64_t q1 = 0, q2 = 0;
-    for (int64_t k = 0;; ++k) {
-      const int s = (int)(k % S);
-      if constexpr (Src::kFused) {
-        // Never sit on an unpublished tile while waiting: another chunk (maybe
-        // this CTA's own next one) may be waiting for it.
-        if (ct == 0 && (pend1 || pend2) && !mbar_test(&full[s], (uint32_t)((k / S) & 1))) {
-          bulk_wait_all();
-          if (pend2) src.tile_done(pass2, q2, Tm);
-          if (pend1) src.tile_done(pass1, q1, Tm);
-          pend1 = pend2 = false;
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ store warp
+    // Lane 0 writes each merged tile out of its stage (bulk store of the
+    // 16-byte aligned middle, plain stores of the <16-byte head and tail),
+    // hands the stage back once the store has read it, and publishes the
+    // tile's completion (fused levels) one tile later, when its store is done.
+    if (lane == 0) {
+      bool pend = false;
+      int ppass = 0;
+      int64_t pq = 0;
+      for (int64_t k = 0;; ++k) {
+        const int s = (int)(k % S);
+        const uint32_t par = (uint32_t)((k / S) & 1);
+        if constexpr (Src::kFused) {
+          // never sit on an unpublished tile: another chunk (maybe this CTA's
+          // own next one) may be waiting for it
+          if (pend && !mbar_test(&outr[s], par)) {
+            bulk_wait_all();
+            src.tile_done(ppass, pq, Tm);
+            pend = false;
+          }
+        }
+        mbar_wait(&outr[s], par);
+        const TileMeta m = meta[s];
+        if (m.out < 0) break;
+        K* sk = stk + (size_t)s * LY::SKE;
+        uint32_t* sv = stv + (size_t)s * LY::SVE;
+        K* gk = src.dstk(m.pass) + m.out;
+        const int phk = stage_offset(gk);
+        int hk, mk;
+        window_split(gk, m.tot, hk, mk);
+        if (mk) bulk_s2g(gk + hk, sk + phk + hk, (uint32_t)(mk * sizeof(K)));
+        uint32_t* gv = nullptr;
+        int phv = 0, hv = 0, mv = 0;
+        if constexpr (PAIRS) {
+          gv = src.dstv(m.pass) + m.out;
+          phv = stage_offset(gv);
+          window_split(gv, m.tot, hv, mv);
+          if (mv) bulk_s2g(gv + hv, sv + phv + hv, (uint32_t)(mv * 4));
+        }
+        bulk_commit();
+        for (int i = 0; i < m.tot - mk; ++i) {
+          const int j = i < hk ? i : i + mk;
+          gk[j] = sk[phk + j];
+        }
+        if constexpr (PAIRS)
+          for (int i = 0; i < m.tot - mv; ++i) {
+            const int j = i < hv ? i : i + mv;
+            gv[j] = sv[phv + j];
+          }
+        bulk_wait_read<0>();     // this tile's store has read the stage
+        mbar_arrive(&empty[s]);  // ... so it goes back to the producer
+        if constexpr (Src::kFused) {
+          if (pend) {
+            bulk_wait<1>();  // the previous tile's store is complete
+            src.tile_done(ppass, pq, Tm);
+          }
+          pend = true, ppass = m.pass, pq = m.q;
         }
       }
+      bulk_wait_all();
+      if constexpr (Src::kFused)
+        if (pend) src.tile_done(ppass, pq, Tm);
+    }
+  } else {
+    // ------------------------------------------------------------ mergers
+    const int ct = threadIdx.x - kK3Extra;  // 0..NC-1
+    for (int64_t k = 0;; ++k) {
+      const int s = (int)(k % S);
 #ifdef MSORT_K3_TRACE
       const unsigned long long tw0 = gtimer();
 #endif
@@ -514,7 +566,11 @@ __global__ void __launch_bounds__(NC + 64, MINB)
       if (k == 0 && ct == 0) K3_TRACE(3, gtimer() - t_start);
 #endif
       const TileMeta m = meta[s];
-      if (m.out < 0) break;
+      if (m.out < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&outr[s]);  // pass the stop on to the store warp
+        break;
+      }
       K* sk = stk + (size_t)s * LY::SKE;
       uint32_t* sv = stv + (size_t)s * LY::SVE;
       K key[VT];
@@ -553,30 +609,12 @@ __global__ void __launch_bounds__(NC + 64, MINB)
           }
         }
       }
-      // everyone is done reading stage s (so it can be overwritten) and with
-      // the previous tile's head/tail stores (so that stage can be recycled)
-      named_bar_sync(1, NC);
-      if (ct == 0 && prev_s >= 0) {
-        bulk_wait_read<0>();          // the previous tile's bulk store has read it
-        mbar_arrive(&empty[prev_s]);  // ... so its stage goes back to the producer
-        if constexpr (Src::kFused) {
-          if (pend2) {
-            bulk_wait<1>();  // all but the newest store complete: publish the older
-            src.tile_done(pass2, q2, Tm);
-            pend2 = false;
-          }
-        }
-      }
+      named_bar_sync(1, NC);  // everyone is done reading stage s: overwrite it
       // The output keeps its global 16-byte phase so the aligned middle leaves
       // by one bulk store (TMA, cp.async.bulk.global.shared).
-      K* gk = src.dstk(m.pass) + m.out;
-      const int phk = stage_offset(gk);
-      uint32_t* gv = nullptr;
+      const int phk = stage_offset(src.dstk(m.pass) + m.out);
       int phv = 0;
-      if constexpr (PAIRS) {
-        gv = src.dstv(m.pass) + m.out;
-        phv = stage_offset(gv);
-      }
+      if constexpr (PAIRS) phv = stage_offset(src.dstv(m.pass) + m.out);
 #pragma unroll
       for (int t = 0; t < VT; ++t) {
         if (d + t < m.tot) {
@@ -584,44 +622,12 @@ __global__ void __launch_bounds__(NC + 64, MINB)
           if constexpr (PAIRS) sv[phv + d + t] = val[t];
         }
       }
-      fence_proxy_async_smem();
-      named_bar_sync(1, NC);  // output tile complete in shared memory
-      int hk, mk;
-      window_split(gk, m.tot, hk, mk);
-      int hv = 0, mv = 0;
-      if constexpr (PAIRS) window_split(gv, m.tot, hv, mv);
-      if (ct == 0) {
-        // one thread writes the whole tile (bulk middle + <16-byte head and
-        // tail), so its completion can be published by that thread alone
-        if (mk) bulk_s2g(gk + hk, sk + phk + hk, (uint32_t)(mk * sizeof(K)));
-        if constexpr (PAIRS)
-          if (mv) bulk_s2g(gv + hv, sv + phv + hv, (uint32_t)(mv * 4));
-        bulk_commit();
-        for (int i = 0; i < m.tot - mk; ++i) {
-          const int j = i < hk ? i : i + mk;
-          gk[j] = sk[phk + j];
-        }
-        if constexpr (PAIRS)
-          for (int i = 0; i < m.tot - mv; ++i) {
-            const int j = i < hv ? i : i + mv;
-            gv[j] = sv[phv + j];
-          }
-        if (pend1) pend2 = true, pass2 = pass1, q2 = q1;
-        pend1 = true, pass1 = m.pass, q1 = m.q;
-      }
-      prev_s = s;
-      prev_pass = m.pass;
-      prev_q = m.q;
+      fence_proxy_async_smem();  // visible to the bulk-store engine
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&outr[s]);
 #ifdef MSORT_K3_TRACE
       ++ntile_done;
 #endif
-    }
-    if (ct == 0) {
-      bulk_wait_all();
-      if constexpr (Src::kFused) {
-        if (pend2) src.tile_done(pass2, q2, Tm);
-        if (pend1) src.tile_done(pass1, q1, Tm);
-      }
     }
 #ifdef MSORT_K3_TRACE
     if (ct == 0) K3_TRACE(4, gtimer() - t_start), K3_TRACE(6, t_wait), K3_TRACE(5, ntile_done);

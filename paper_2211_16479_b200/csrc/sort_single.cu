@@ -158,10 +158,13 @@ struct Kernels {
                                         (int)k1_smem));
     MSORT_TRY(set_smem<Fused>());
     MSORT_TRY(set_smem<Explicit>());
+#ifdef MSORT_K3_PERPASS
+    MSORT_TRY((set_smem<SinglePass<K, UniformPairs>>()));
+#endif
     int sms = 0, occ = 0;
     MSORT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     MSORT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ, k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, Fused>, NC + 64, k3_smem));
+        &occ, k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, Fused>, NC + kK3Extra, k3_smem));
     if (occ < 1) {
       set_error("merge pass kernel does not fit on an SM");
       return MSORT_ERROR_NOT_SUPPORTED;
@@ -181,7 +184,7 @@ struct Kernels {
     {
       LaunchScope ls(kc, s);
       k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, Src>
-          <<<(unsigned)grid, NC + 64, k3_smem, s>>>(src, ctr);
+          <<<(unsigned)grid, NC + kK3Extra, k3_smem, s>>>(src, ctr);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
 #ifdef MSORT_K3_CHECK
@@ -244,6 +247,19 @@ struct Kernels {
     }
 #endif
     if (passes == 0) return MSORT_SUCCESS;
+#ifdef MSORT_K3_PERPASS
+    // tuning variant: one launch per merge level
+    MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * 8, s));
+    for (int p = 0; p < passes; ++p) {
+      SinglePass<K, UniformPairs> sp{};
+      sp.pm = UniformPairs{(int64_t)n, (int64_t)T << p};
+      sp.src_k = bk[cur], sp.src_v = bv[cur], sp.dst_k = bk[cur ^ 1], sp.dst_v = bv[cur ^ 1];
+      sp.ntiles = (int64_t)((n + Tm - 1) / Tm);
+      MSORT_TRY(launch_k3(sp, (sp.ntiles + kChunk - 1) / kChunk, ctr + p, s, KC_MERGE));
+      cur ^= 1;
+    }
+    return MSORT_SUCCESS;
+#endif
     // All merge levels in one dataflow launch (k3_merge.cuh, FusedPasses).
     Fused f{};
     f.bk[0] = bk[cur], f.bk[1] = bk[cur ^ 1];
