@@ -339,13 +339,33 @@ __device__ __forceinline__ void batcher_sort(K (&x)[N]) {
   }
 }
 
-// Keys-only network for any N: Batcher on the largest power of two P <= N,
+// Bitonic sorting network over the first P (a power of two) of N registers;
+// three plain counted loops that always unroll completely.
+template <int P, int N, class K>
+__device__ __forceinline__ void bitonic_sort(K (&x)[N]) {
+#pragma unroll
+  for (int k = 2; k <= P; k *= 2) {
+#pragma unroll
+    for (int j = k / 2; j > 0; j /= 2) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          if ((i & k) == 0) cmp_swap(x[i], x[l]);
+          else cmp_swap(x[l], x[i]);
+        }
+      }
+    }
+  }
+}
+
+// Keys-only network for any N: bitonic on the largest power of two P <= N,
 // then each remaining element is inserted by a compare-exchange chain.
 template <int N, class K>
 __device__ __forceinline__ void keys_network(K (&x)[N]) {
   constexpr int P = N >= 16 ? 16 : (N >= 8 ? 8 : (N >= 4 ? 4 : (N >= 2 ? 2 : 1)));
   static_assert(N < 32, "keys_network: N < 32");
-  batcher_sort<P>(x);
+  bitonic_sort<P>(x);
 #pragma unroll
   for (int m = P; m < N; ++m) {
 #pragma unroll

@@ -78,8 +78,13 @@ __global__ void __launch_bounds__(NT)
     const int g0 = (tid / tpg) * 2 * w;
     const int d = (tid % tpg) * VT;
     int i = merge_path<K, false>(sk, g0, w, g0 + w, w, d);
-    serial_merge<K, false, PAIRS, VT>(sk, PAIRS ? si : nullptr, g0 + i, g0 + w, g0 + w + d - i,
-                                      g0 + 2 * w, T - 1, key, idx);
+    if constexpr (PAIRS) {
+      serial_merge<K, false, true, VT>(sk, si, g0 + i, g0 + w, g0 + w + d - i, g0 + 2 * w, T - 1,
+                                       key, idx);
+    } else {
+      serial_merge_fast<K, false, VT>(sk, g0 + i, g0 + w, g0 + w + d - i, g0 + 2 * w, T - 1,
+                                      key, idx);
+    }
   }
 
   __syncthreads();
