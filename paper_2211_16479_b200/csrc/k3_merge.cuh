@@ -379,18 +379,43 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
           src.chunk(c0 + mm, p_, q2, c_);
           src.wait_ready(p_, q2, c_, lane, Tm);
         }
+        // Two rounds: the chunk's first and last co-ranks by full searches,
+        // then the inner ones inside the bracket those give (co-ranks are
+        // monotone: i(d) <= i(d + x) <= i(d) + x within one pair), so the
+        // inner probes fall in the windows the chunk is about to stage
+        // instead of all over the runs (ncu: fewer stray DRAM sectors).
         int64_t v = 0;
         int cntm = 0;
         int64_t q0m = 0;
+        int64_t A0 = -1, na = 0, nb = 0, dl = 0;
+        bool valid = false;
         if (m >= mm0 && m < mm1) {
           int p_;
           src.chunk(c0 + m, p_, q0m, cntm);
-          if (j <= cntm && q0m + j < src.tiles(pass0)) {
-            int64_t A0, na, nb, dl;
-            src.locate(pass0, q0m + j, Tm, A0, na, nb, dl);
-            const K* sk = src.srck(pass0);
-            v = merge_path_global(sk + A0, na, sk + A0 + na, nb, dl);
+          valid = j <= cntm && q0m + j < src.tiles(pass0);
+          if (valid) src.locate(pass0, q0m + j, Tm, A0, na, nb, dl);
+        }
+        const K* sk = src.srck(pass0);
+        const bool edge = j == 0 || j == cntm;
+        if (valid && edge) v = merge_path_global(sk + A0, na, sk + A0 + na, nb, dl);
+        const int l0 = m * (CH + 1) < 32 ? m * (CH + 1) : 0;
+        const int le = l0 + cntm < 32 ? l0 + cntm : 0;
+        const int64_t v0 = __shfl_sync(0xffffffffu, v, l0);
+        const int64_t a00 = __shfl_sync(0xffffffffu, A0, l0);
+        const int64_t ve = __shfl_sync(0xffffffffu, v, le);
+        const int64_t a0e = __shfl_sync(0xffffffffu, A0, le);
+        if (valid && !edge) {
+          int64_t lo = dl - nb > 0 ? dl - nb : 0;
+          int64_t hi = dl < na ? dl : na;
+          if (a00 == A0) {  // same pair as the chunk's first tile
+            lo = max(lo, v0);
+            hi = min(hi, v0 + (int64_t)j * Tm);
           }
+          if (a0e == A0) {  // same pair as the chunk's last boundary
+            lo = max(lo, ve - (int64_t)(cntm - j) * Tm);
+            hi = min(hi, ve);
+          }
+          v = merge_path_global_range(sk + A0, sk + A0 + na, dl, lo, hi);
         }
         for (int mm = mm0; mm < mm1; ++mm) {
           const int r = (int)((g * kGrab + mm) % R);

@@ -84,6 +84,19 @@ __device__ __forceinline__ int64_t merge_path_global(const K* __restrict__ a, in
   return lo;
 }
 
+// The same search restricted to [lo, hi], a bracket known to hold i(d).
+template <class K>
+__device__ __forceinline__ int64_t merge_path_global_range(const K* __restrict__ a,
+                                                           const K* __restrict__ b, int64_t d,
+                                                           int64_t lo, int64_t hi) {
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) > __ldg(b + (d - 1 - mid))) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
 // Serial stable merge of VT outputs starting at (ai, bi): take B only when
 // B < A (strict), so ties go to A.  Positions are indices into the shared
 // buffer s; `pos` records the source position of each output (for payload
@@ -121,7 +134,8 @@ __device__ __forceinline__ void serial_merge(const K* s, const int* src_idx, int
 template <class K, bool TRACK, int VT>
 __device__ __forceinline__ void serial_merge_fast(const K* s, int ai, int aend, int bi, int bend,
                                                   int lim, K (&key)[VT], int (&pos)[VT]) {
-  if (ai + VT <= aend && bi + VT <= bend) {
+  // warp-uniform choice: a divergent warp would run both paths
+  if (__all_sync(__activemask(), ai + VT <= aend && bi + VT <= bend)) {
     K ak = s[ai];
     K bk = s[bi];
 #pragma unroll
