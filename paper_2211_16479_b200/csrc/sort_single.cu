@@ -65,15 +65,20 @@ __global__ void __launch_bounds__(NT)
   else keys_network<VT>(key);
 
   // In-block merge rounds: runs of w -> 2w, merge path per thread.
+  // While a merge group (2w outputs, 2w/VT threads) fits in one warp the
+  // round needs only warp-level synchronisation.
 #pragma unroll 1
   for (int w = VT; w < T; w *= 2) {
-    __syncthreads();
+    const bool in_warp = 2 * w <= 32 * VT;
+    if (in_warp) __syncwarp();
+    else __syncthreads();
 #pragma unroll
     for (int k = 0; k < VT; ++k) {
       sk[tid * VT + k] = key[k];
       if constexpr (PAIRS) si[tid * VT + k] = idx[k];
     }
-    __syncthreads();
+    if (in_warp) __syncwarp();
+    else __syncthreads();
     const int tpg = 2 * w / VT;  // threads per merge group
     const int g0 = (tid / tpg) * 2 * w;
     const int d = (tid % tpg) * VT;
