@@ -377,8 +377,8 @@ __device__ __forceinline__ void bitonic_sort(K (&x)[N]) {
 // then each remaining element is inserted by a compare-exchange chain.
 template <int N, class K>
 __device__ __forceinline__ void keys_network(K (&x)[N]) {
-  constexpr int P = N >= 16 ? 16 : (N >= 8 ? 8 : (N >= 4 ? 4 : (N >= 2 ? 2 : 1)));
-  static_assert(N < 32, "keys_network: N < 32");
+  constexpr int P = N >= 64 ? 64 : N >= 32 ? 32 : N >= 16 ? 16 : (N >= 8 ? 8 : (N >= 4 ? 4 : (N >= 2 ? 2 : 1)));
+  static_assert(N < 128, "keys_network: N < 128");
   bitonic_sort<P>(x);
 #pragma unroll
   for (int m = P; m < N; ++m) {

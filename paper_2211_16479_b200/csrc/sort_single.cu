@@ -119,6 +119,12 @@ extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
 #ifndef MSORT_K3_NC
 #define MSORT_K3_NC 256  // merging threads per K3 CTA
 #endif
+#ifndef MSORT_K1_NT
+#define MSORT_K1_NT 256  // keys-only K1 threads
+#endif
+#ifndef MSORT_K1_VT
+#define MSORT_K1_VT 34  // keys-only K1 items per thread (NT x VT = 8704)
+#endif
 #ifndef MSORT_K3_VT
 #define MSORT_K3_VT 17  // outputs per merging thread (even: two chains per thread)
 #endif
@@ -129,8 +135,13 @@ constexpr int kMaxLaunches = 64;
 
 template <class K, bool PAIRS>
 struct Kernels {
-  static constexpr int VT = 17;  // odd: conflict-free blocked shared accesses
-  static constexpr int NT1 = 512;
+  // K1 shape.  Pairs: 512 threads x 17 (odd: conflict-free blocked shared
+  // accesses; the stable odd-even transposition network is quadratic, so
+  // threads keep few items).  Keys only: fewer threads with more items each
+  // -- a register network level is cheaper than a shared-memory merge round
+  // (and each thread's co-rank search is amortised over more outputs).
+  static constexpr int VT = PAIRS ? 17 : MSORT_K1_VT;
+  static constexpr int NT1 = PAIRS ? 512 : MSORT_K1_NT;
   static constexpr int T = NT1 * VT;  // tile sort size
   static constexpr int NC = MSORT_K3_NC;
   static constexpr int VT3 = MSORT_K3_VT;
