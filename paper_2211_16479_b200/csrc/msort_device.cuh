@@ -156,6 +156,72 @@ __device__ __forceinline__ void serial_merge_fast(const K* s, int ai, int aend, 
   }
 }
 
+// Keys-only merge step kernels on byte offsets into a shared buffer (the
+// output value of a keys-only merge is min(a, b) whichever run it came
+// from, and each step touches one byte offset: select, add, load).
+template <class K>
+__device__ __forceinline__ K ld_off(const char* s, uint32_t off) {
+  return *reinterpret_cast<const K*>(s + off);
+}
+// VT outputs of merge(A, B) from byte offsets oa, ob, no end checks: the
+// caller guarantees neither run ends within VT steps.
+template <class K, int VT>
+__device__ __forceinline__ void merge_keys_nocheck(const char* s, uint32_t oa, uint32_t ob,
+                                                   K (&key)[VT]) {
+  K ak = ld_off<K>(s, oa), bk = ld_off<K>(s, ob);
+#pragma unroll
+  for (int k = 0; k < VT; ++k) {
+    const bool p = bk < ak;
+    key[k] = p ? bk : ak;
+    if (k + 1 < VT) {
+      const uint32_t nx = (p ? ob : oa) + (uint32_t)sizeof(K);
+      oa = p ? oa : nx;
+      ob = p ? nx : ob;
+      const K nv = ld_off<K>(s, nx);
+      ak = p ? ak : nv;
+      bk = p ? nv : bk;
+    }
+  }
+}
+// Same with end checks: a run that is used up reads as "greater than
+// anything" (the other run is taken); loads are clamped to `lim`.
+template <class K, int VT>
+__device__ __forceinline__ void merge_keys_checked(const char* s, uint32_t oa, uint32_t ea,
+                                                   uint32_t ob, uint32_t eb, uint32_t lim,
+                                                   K (&key)[VT]) {
+  K ak = ld_off<K>(s, min(oa, lim)), bk = ld_off<K>(s, min(ob, lim));
+#pragma unroll
+  for (int k = 0; k < VT; ++k) {
+    const bool p = (ob < eb) && ((oa >= ea) || (bk < ak));
+    key[k] = p ? bk : ak;
+    if (k + 1 < VT) {
+      const uint32_t nx = (p ? ob : oa) + (uint32_t)sizeof(K);
+      oa = p ? oa : nx;
+      ob = p ? nx : ob;
+      const K nv = ld_off<K>(s, min(nx, lim));
+      ak = p ? ak : nv;
+      bk = p ? nv : bk;
+    }
+  }
+}
+// Merge-path co-rank (see merge_path) on byte offsets: A at oa (na
+// elements), B at ob (nb), diagonal d.
+template <class K>
+__device__ __forceinline__ int merge_path_off(const char* s, uint32_t oa, int na, uint32_t ob,
+                                              int nb, int d) {
+  int lo = d - nb > 0 ? d - nb : 0;
+  int hi = d < na ? d : na;
+  // B[d-1-mid] sits at ob + (d-1)*sz - mid*sz
+  const uint32_t obd = ob + (uint32_t)((d - 1) * (int)sizeof(K));
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const uint32_t m = (uint32_t)mid * (uint32_t)sizeof(K);
+    if (ld_off<K>(s, oa + m) > ld_off<K>(s, obd - m)) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
 // 2H outputs of one thread merged as two independent chains: the front chain
 // produces outputs 0..H-1 from the co-rank at the thread's first diagonal
 // (ai0, bi0) upwards, the back chain outputs 2H-1..H from the co-rank at its

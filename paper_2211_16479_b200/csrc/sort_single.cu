@@ -42,23 +42,31 @@ __global__ void __launch_bounds__(NT)
   const int64_t base = (int64_t)blockIdx.x * T;
   const int cnt = (int)min((int64_t)T, n - base);
 
-  // Load the tile; pad the partial last tile with the maximum key AFTER the
-  // real elements, so the stable order keeps real keys first.
-#pragma unroll 4
-  for (int i = tid; i < T; i += NT) {
-    sk[i] = i < cnt ? in_k[base + i] : KeyTraits<K>::max_key();
-    if constexpr (PAIRS) {
-      if (i < cnt) sv[i] = in_v[base + i];
-    }
-  }
-  __syncthreads();
-
   K key[VT];
   int idx[VT];
+  if constexpr (PAIRS) {
+    // Load the tile; pad the partial last tile with the maximum key AFTER the
+    // real elements, so the stable order keeps real keys first.
+#pragma unroll 4
+    for (int i = tid; i < T; i += NT) {
+      sk[i] = i < cnt ? in_k[base + i] : KeyTraits<K>::max_key();
+      if (i < cnt) sv[i] = in_v[base + i];
+    }
+    __syncthreads();
 #pragma unroll
-  for (int k = 0; k < VT; ++k) {
-    key[k] = sk[tid * VT + k];
-    idx[k] = tid * VT + k;
+    for (int k = 0; k < VT; ++k) {
+      key[k] = sk[tid * VT + k];
+      idx[k] = tid * VT + k;
+    }
+  } else {
+    // Keys only: which thread holds which key before the network does not
+    // matter (equal keys are indistinguishable), so load straight into
+    // registers, striped (coalesced), padding with the maximum key.
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+      const int i = k * NT + tid;
+      key[k] = i < cnt ? in_k[base + i] : KeyTraits<K>::max_key();
+    }
   }
   // Per-thread register network.
   if constexpr (PAIRS) odd_even_transposition_sort<VT>(key, idx);
@@ -82,6 +90,19 @@ __global__ void __launch_bounds__(NT)
     const int tpg = 2 * w / VT;  // threads per merge group
     const int g0 = (tid / tpg) * 2 * w;
     const int d = (tid % tpg) * VT;
+    if constexpr (!PAIRS) {
+      constexpr uint32_t Z = sizeof(K);
+      const char* sb = reinterpret_cast<const char*>(sk);
+      const uint32_t oa0 = (uint32_t)g0 * Z, ob0 = oa0 + (uint32_t)w * Z;
+      const int i = merge_path_off<K>(sb, oa0, w, ob0, w, d);
+      const uint32_t oa = oa0 + (uint32_t)i * Z, ob = ob0 + (uint32_t)(d - i) * Z;
+      const uint32_t ea = ob0, eb = ob0 + (uint32_t)w * Z;
+      if (__all_sync(0xffffffffu, oa + VT * Z <= ea && ob + VT * Z <= eb))
+        merge_keys_nocheck<K, VT>(sb, oa, ob, key);
+      else
+        merge_keys_checked<K, VT>(sb, oa, ea, ob, eb, (uint32_t)(T - 1) * Z, key);
+      continue;
+    }
     int i = merge_path<K, false>(sk, g0, w, g0 + w, w, d);
     if constexpr (PAIRS) {
       serial_merge<K, false, true, VT>(sk, si, g0 + i, g0 + w, g0 + w + d - i, g0 + 2 * w, T - 1,
@@ -104,6 +125,129 @@ __global__ void __launch_bounds__(NT)
     out_k[base + i] = sk[i];
     if constexpr (PAIRS) out_v[base + i] = sv[si[i]];
   }
+}
+
+// Keys-only K1.  Each thread sorts VT keys in registers (keys_network), then
+// log2(NT) merge-path rounds in shared memory double the runs.  In round r
+// (runs of w = VT << r) pair m = (run 2m = A, run 2m+1 = B) is laid out as
+//     [ B (w) | MAX | A (w) | MAX ]
+// (each sentinel slot is two keys wide, so every run starts at an even
+// element offset and the VT keys of a thread leave as 2-key vector stores,
+// conflict-free for even VT) so that a run that is used up reads as its MAX
+// sentinel: the serial merge
+// needs no end checks (merge_keys_sentinel) and no thread diverges.  (With
+// equal keys indistinguishable, taking A's sentinel on a tie with a real MAX
+// in B outputs the right value; the A cursor is clamped at its sentinel.)
+// Rounds whose merge groups fit in a warp use a per-warp region with 64
+// elements of slack (room for its sentinels) and only warp synchronisation.
+template <class K, int VT>
+__device__ __forceinline__ void merge_keys_sentinel(const char* s, uint32_t oa, uint32_t ea,
+                                                    uint32_t ob, K (&key)[VT]) {
+  K ak = ld_off<K>(s, oa), bk = ld_off<K>(s, ob);
+#pragma unroll
+  for (int k = 0; k < VT; ++k) {
+    const bool p = bk < ak;
+    key[k] = p ? bk : ak;
+    if (k + 1 < VT) {
+      const uint32_t nx = min((p ? ob : oa) + (uint32_t)sizeof(K), ea);  // B lies below ea
+      oa = p ? oa : nx;
+      ob = p ? nx : ob;
+      const K nv = ld_off<K>(s, nx);
+      ak = p ? ak : nv;
+      bk = p ? nv : bk;
+    }
+  }
+}
+
+template <class K>
+struct __align__(2 * sizeof(K)) K2 {
+  K x, y;
+};
+// VT (even) keys to dst (2-key aligned) as VT/2 vector stores.
+template <class K, int VT>
+__device__ __forceinline__ void store_pairs(K* dst, const K (&key)[VT]) {
+#pragma unroll
+  for (int k = 0; k < VT; k += 2) {
+    K2<K> v;
+    v.x = key[k], v.y = key[k + 1];
+    *reinterpret_cast<K2<K>*>(dst + k) = v;
+  }
+}
+
+template <class K, int NT, int VT>
+struct K1KeysShape {
+  static constexpr int T = NT * VT;
+  static constexpr int NW = NT / 32;
+  static constexpr int WREG = 32 * VT + 64;  // per-warp region (in-warp rounds)
+  static constexpr int ROUNDS = __builtin_ctz(NT);
+  static constexpr size_t smem =
+      (size_t)(NW * WREG > T + 2 * NT ? NW * WREG : T + 2 * NT) * sizeof(K);
+  static_assert((NT & (NT - 1)) == 0 && NT >= 32, "NT: power of two >= 32");
+};
+
+template <class K, int NT, int VT>
+__global__ void __launch_bounds__(NT)
+    k1_tile_sort_keys(const K* __restrict__ in_k, K* __restrict__ out_k, int64_t n) {
+  using SH = K1KeysShape<K, NT, VT>;
+  static_assert(VT % 2 == 0, "keys-only K1 stores key pairs: VT even");
+  constexpr int T = SH::T;
+  constexpr uint32_t Z = sizeof(K);
+  extern __shared__ __align__(16) unsigned char smem[];
+  K* sk = reinterpret_cast<K*>(smem);
+  const char* sb = reinterpret_cast<const char*>(smem);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * T;
+  const int cnt = (int)min((int64_t)T, n - base);
+
+  // Which thread holds which key before the network does not matter (keys
+  // only), so load straight into registers, striped (coalesced); the partial
+  // last tile is padded with the maximum key.
+  K key[VT];
+#pragma unroll
+  for (int k = 0; k < VT; ++k) {
+    const int i = k * NT + tid;
+    key[k] = i < cnt ? in_k[base + i] : KeyTraits<K>::max_key();
+  }
+  keys_network<VT>(key);
+
+#pragma unroll 1
+  for (int r = 0; r < SH::ROUNDS; ++r) {
+    const int w = VT << r;
+    const bool in_warp = (2 << r) <= 32;
+    // region origin of this round's pairs (elements)
+    const int org = in_warp ? warp * SH::WREG : 0;
+    const int mbase = in_warp ? (warp * 32) >> (r + 1) : 0;  // first pair of the region
+    if (in_warp) __syncwarp();
+    else __syncthreads();
+    {
+      // my VT keys: run rho = tid >> r at offset (tid mod 2^r) * VT
+      const int rho = tid >> r;
+      const int pos = (tid & ((1 << r) - 1)) * VT;
+      const int m = (rho >> 1) - mbase;
+      const int at = org + m * (2 * w + 4) + ((rho & 1) ? 0 : w + 2) + pos;
+      store_pairs<K, VT>(sk + at, key);
+      if (pos + VT == w) {
+        K2<K> mx;
+        mx.x = mx.y = KeyTraits<K>::max_key();
+        *reinterpret_cast<K2<K>*>(sk + at + VT) = mx;
+      }
+    }
+    if (in_warp) __syncwarp();
+    else __syncthreads();
+    const int m = (tid >> (r + 1)) - mbase;
+    const int d = (tid & ((2 << r) - 1)) * VT;
+    const uint32_t ob0 = (uint32_t)(org + m * (2 * w + 4)) * Z;
+    const uint32_t oa0 = ob0 + (uint32_t)(w + 2) * Z;
+    const int i = merge_path_off<K>(sb, oa0, w, ob0, w, d);
+    merge_keys_sentinel<K, VT>(sb, oa0 + (uint32_t)i * Z, oa0 + (uint32_t)w * Z,
+                               ob0 + (uint32_t)(d - i) * Z, key);
+  }
+
+  __syncthreads();
+  store_pairs<K, VT>(sk + tid * VT, key);
+  __syncthreads();
+#pragma unroll 4
+  for (int i = tid; i < cnt; i += NT) out_k[base + i] = sk[i];
 }
 
 // ----------------------------------------------------------------- K3
@@ -151,7 +295,8 @@ struct Kernels {
   // CTAs per SM the register budget is tuned for (shared memory allows 4 for
   // 4-byte keys without payload, 2-3 otherwise)
   static constexpr int MINB = (sizeof(K) == 4 && !PAIRS) ? 4 : 2;
-  static constexpr size_t k1_smem = (size_t)T * sizeof(K) + (PAIRS ? (size_t)T * 8 : 0);
+  static constexpr size_t k1_smem =
+      PAIRS ? (size_t)T * sizeof(K) + (size_t)T * 8 : K1KeysShape<K, NT1, VT>::smem;
   static constexpr size_t k3_smem = LY::bytes;
   static_assert((2 * T) % Tm == 0, "pair boundaries must be tile boundaries");
   using Fused = FusedPasses<K>;
@@ -174,9 +319,14 @@ struct Kernels {
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
     if (grid3(dev)) return MSORT_SUCCESS;
-    MSORT_CUDA_TRY(cudaFuncSetAttribute(k1_tile_sort<K, PAIRS, NT1, VT>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)k1_smem));
+    if constexpr (PAIRS)
+      MSORT_CUDA_TRY(cudaFuncSetAttribute(k1_tile_sort<K, PAIRS, NT1, VT>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)k1_smem));
+    else
+      MSORT_CUDA_TRY(cudaFuncSetAttribute(k1_tile_sort_keys<K, NT1, VT>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)k1_smem));
     MSORT_TRY(set_smem<Fused>());
     MSORT_TRY(set_smem<Explicit>());
 #ifdef MSORT_K3_PERPASS
@@ -256,8 +406,12 @@ struct Kernels {
     int cur = passes % 2;  // S4: pick K1's destination so the last pass lands in keys
     {
       LaunchScope ls(KC_TILE_SORT, s);
-      k1_tile_sort<K, PAIRS, NT1, VT>
-          <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, in_v, bk[cur], bv[cur], (int64_t)n);
+      if constexpr (PAIRS)
+        k1_tile_sort<K, PAIRS, NT1, VT>
+            <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, in_v, bk[cur], bv[cur], (int64_t)n);
+      else
+        k1_tile_sort_keys<K, NT1, VT>
+            <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, bk[cur], (int64_t)n);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
 #ifdef MSORT_K3_CHECK
