@@ -69,8 +69,14 @@ struct ExplicitPairs {  // arbitrary consecutive runs, pairs (2m, 2m+1)
   }
 };
 
-constexpr int kChunk = 8;        // tiles per dynamically scheduled chunk
-constexpr int kGrab = 3;         // chunks taken per atomic
+#ifndef MSORT_K3_CHUNK
+#define MSORT_K3_CHUNK 8
+#endif
+#ifndef MSORT_K3_GRAB
+#define MSORT_K3_GRAB 3
+#endif
+constexpr int kChunk = MSORT_K3_CHUNK;  // tiles per dynamically scheduled chunk
+constexpr int kGrab = MSORT_K3_GRAB;    // chunks taken per atomic
 constexpr int kMaxFusedPasses = 48;
 
 struct TileMeta {

@@ -288,7 +288,7 @@ struct Kernels {
   static constexpr int NT1 = PAIRS ? 512 : MSORT_K1_NT;
   static constexpr int T = NT1 * VT;  // tile sort size
   static constexpr int NC = MSORT_K3_NC;
-  static constexpr int VT3 = MSORT_K3_VT;
+  static constexpr int VT3 = PAIRS ? 17 : MSORT_K3_VT;
   static constexpr int Tm = NC * VT3;  // merge output tile (divides 2T)
   static constexpr int S = 3;
   using LY = K3Layout<K, PAIRS, NC, VT3, S>;
