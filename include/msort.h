@@ -228,6 +228,16 @@ int64_t msort_launch_count(void);
 /* Tile size (elements) used for key dtype with/without payload. */
 int msort_tile_size(msort_dtype key_dtype, msort_dtype val_dtype);
 
+/* Tuning/testing knob for keys-only sorts: how merge levels are grouped into
+ * HBM passes.  mode 0 (default): one 2-way level per pass (the fused K3
+ * dataflow only); 1: two levels per pass (4-way merge tree, K3Q) while every
+ * CTA gets >= 2 segments, the remaining levels 2-way; 2: 4-way passes whenever
+ * >= 2 levels remain (small inputs too -- for tests).  The result is the same
+ * in every mode (the stable sort is unique); process-wide, not thread-safe
+ * against concurrent sorts.  Overrides the MSORT_QUAD environment variable.
+ * Returns 0. */
+int msort_debug_set_quad(int mode);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,7 +40,7 @@ EXPORTED = (
     "msort_plan_candidates_per_round", "msort_plan_init", "msort_plan_candidates",
     "msort_plan_narrow", "msort_plan_fill", "msort_status_string", "msort_last_error",
     "msort_profile_enable", "msort_profile_reset", "msort_profile_read", "msort_launch_count",
-    "msort_tile_size",
+    "msort_tile_size", "msort_debug_set_quad",
 )
 
 
@@ -371,6 +371,12 @@ def profile_read():
 
 def launch_count() -> int:
     return int(lib.msort_launch_count())
+
+
+def set_quad_mode(mode: int) -> None:
+    """Merge-level grouping for keys-only sorts (include/msort.h
+    msort_debug_set_quad): 0 two-way levels only, 1 auto, 2 force 4-way."""
+    lib.msort_debug_set_quad(int(mode))
 
 
 def tile_size(key_dtype: int, val_dtype: int = MSORT_NONE) -> int:

@@ -91,6 +91,8 @@ size_t single_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd) {
   if (vd != MSORT_NONE) b += align_up(n * 4, 256);
   // partitions: one per output tile (+ slack for the k-way merge's extra tiles)
   b += align_up((n / (size_t)T + 2 + 2 * 64) * sizeof(int64_t), 256);
+  // 4-way pass segment boundaries (4 x int64 each)
+  b += align_up((2 * (n / (size_t)T) + 64) * 4 * sizeof(int64_t), 256);
   return b;
 }
 

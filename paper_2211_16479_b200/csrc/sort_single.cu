@@ -18,8 +18,10 @@
 // "P:n" = /root/reference/PAPER.md line n.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "k3_merge.cuh"
+#include "k3q_merge.cuh"
 #include "msort_device.cuh"
 #include "msort_internal.h"
 
@@ -273,6 +275,31 @@ extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
 #define MSORT_K3_VT 17  // outputs per merging thread (even: two chains per thread)
 #endif
 
+#ifndef MSORT_QUAD
+#define MSORT_QUAD 0  // keys only: 1 = two merge levels per HBM pass (k3q_merge.cuh), see DESIGN.md
+#endif
+#ifndef MSORT_QUAD_SEG
+#define MSORT_QUAD_SEG 65536  // target keys per 4-way segment
+#endif
+#ifndef MSORT_QUAD_NT
+#define MSORT_QUAD_NT 128
+#endif
+#ifndef MSORT_QUAD_VT
+#define MSORT_QUAD_VT 15  // odd: conflict-free blocked stores
+#endif
+
+// 4-way pass mode: 0 off, 1 auto (while every CTA gets >= 2 segments),
+// 2 always (tests); env MSORT_QUAD overrides the default, msort_debug_set_quad
+// overrides both.
+static int g_quad_mode = -1;
+static int quad_mode() {
+  if (g_quad_mode < 0) {
+    const char* e = getenv("MSORT_QUAD");
+    g_quad_mode = e ? atoi(e) : MSORT_QUAD;
+  }
+  return g_quad_mode;
+}
+
 // Scheduler state in the workspace: 64 chunk counters (one per launch of a
 // sort) then the per-level, per-pair completion counters of the fused merge.
 constexpr int kMaxLaunches = 64;
@@ -302,9 +329,30 @@ struct Kernels {
   using Fused = FusedPasses<K>;
   using Explicit = SinglePass<K, ExplicitPairs>;
 
+  // 4-way pass (keys only)
+  static constexpr int NTQ = MSORT_QUAD_NT, VTQ = MSORT_QUAD_VT;
+  using LQ = QuadLayout<K, NTQ, VTQ>;
+  static int& gridq(int dev) {
+    static int g[64] = {};
+    return g[dev & 63];
+  }
+
   static int& grid3(int dev) {
     static int g[64] = {};
     return g[dev & 63];
+  }
+
+  // Segments of the 4-way pass over runs of L: groups of 4L, S_full segments
+  // per full group (S_last for the last), nseg in all.
+  static void quad_geometry(int64_t n, int64_t L, int64_t& ng, int& sf, int& sl, int64_t& nseg) {
+    ng = (n + 4 * L - 1) / (4 * L);
+    auto segs = [](int64_t len) {
+      int64_t k = (len + MSORT_QUAD_SEG - 1) / MSORT_QUAD_SEG;
+      return (int)std::max<int64_t>(1, std::min<int64_t>(k, kQuadMaxSeg));
+    };
+    sf = segs(4 * L);
+    sl = segs(n - (ng - 1) * 4 * L);
+    nseg = (ng - 1) * sf + sl;
   }
 
   template <class Src>
@@ -343,6 +391,15 @@ struct Kernels {
     // every CTA of the persistent merge kernel must be resident (the fused
     // levels wait on each other's progress): grid = SMs x occupancy
     grid3(dev) = sms * occ;
+    if constexpr (!PAIRS) {
+      auto kq = k3q_pass<K, NTQ, VTQ>;
+      MSORT_CUDA_TRY(
+          cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LQ::bytes));
+      int oq = 0;
+      MSORT_CUDA_TRY(
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oq, kq, NTQ + 64, LQ::bytes));
+      gridq(dev) = sms * std::max(oq, 1);
+    }
     return MSORT_SUCCESS;
   }
 
@@ -385,6 +442,24 @@ struct Kernels {
     const int64_t ntiles = (int64_t)((n + T - 1) / T);
     int passes = 0;
     while ((int64_t(1) << passes) < ntiles) ++passes;
+    int dev = 0;
+    MSORT_CUDA_TRY(cudaGetDevice(&dev));
+    // 4-way passes (two levels each) while there are enough segments to keep
+    // every CTA busy; the remaining levels run as the fused 2-way dataflow.
+    int nq = 0;
+    int64_t Lq = T;
+    if constexpr (!PAIRS) {
+      const int mode = quad_mode();
+      while (mode && passes - 2 * nq >= 2) {
+        int64_t ng, nseg;
+        int sf, sl;
+        quad_geometry((int64_t)n, Lq, ng, sf, sl, nseg);
+        if (mode == 1 && nseg < 2 * (int64_t)gridq(dev)) break;
+        ++nq;
+        Lq *= 4;
+      }
+    }
+    const int left = passes - 2 * nq;  // 2-way levels
     if (passes > kMaxFusedPasses) {
       set_error("too many merge levels");
       return MSORT_ERROR_NOT_SUPPORTED;
@@ -399,11 +474,14 @@ struct Kernels {
     }
     auto* ctr = reinterpret_cast<unsigned long long*>(w);
     auto* done = reinterpret_cast<unsigned*>(ctr + kMaxLaunches);
+    auto* qstates = reinterpret_cast<QuadState*>(
+        w + align_up(((size_t)n / T + 2 + 2 * 64) * sizeof(int64_t), 256));
     (void)ws_bytes;
 
     K* bk[2] = {keys, wk};
     uint32_t* bv[2] = {vals, wv};
-    int cur = passes % 2;  // S4: pick K1's destination so the last pass lands in keys
+    // S4: pick K1's destination so the last pass lands in keys
+    int cur = (nq + left) % 2;
     {
       LaunchScope ls(KC_TILE_SORT, s);
       if constexpr (PAIRS)
@@ -422,6 +500,37 @@ struct Kernels {
     }
 #endif
     if (passes == 0) return MSORT_SUCCESS;
+    if constexpr (!PAIRS) {
+      if (nq > 0)
+        MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * sizeof(unsigned long long), s));
+      int64_t L = T;
+      for (int q = 0; q < nq; ++q, L *= 4) {
+        int64_t ng, nseg;
+        int sf, sl;
+        quad_geometry((int64_t)n, L, ng, sf, sl, nseg);
+        {
+          LaunchScope ls(KC_PARTITION, s);
+          k2q_partition<K><<<(unsigned)ng, 256, 0, s>>>(bk[cur], (int64_t)n, L, sf, sl, ng,
+                                                         qstates);
+        }
+        MSORT_CUDA_TRY(cudaGetLastError());
+        {
+          LaunchScope ls(KC_MERGE, s);
+          k3q_pass<K, NTQ, VTQ><<<(unsigned)std::min<int64_t>(gridq(dev), nseg), NTQ + 64,
+                                   LQ::bytes, s>>>(bk[cur], bk[cur ^ 1], (int64_t)n, L, sf, nseg,
+                                                   qstates, ctr + 32 + q);
+        }
+        MSORT_CUDA_TRY(cudaGetLastError());
+#ifdef MSORT_K3_CHECK
+        {
+          cudaError_t e = cudaStreamSynchronize(s);
+          if (e != cudaSuccess) return cuda_fail(e, "k3q (debug sync)");
+        }
+#endif
+        cur ^= 1;
+      }
+      if (left == 0) return MSORT_SUCCESS;
+    }
 #ifdef MSORT_K3_PERPASS
     // tuning variant: one launch per merge level
     MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * 8, s));
@@ -439,17 +548,17 @@ struct Kernels {
     Fused f{};
     f.bk[0] = bk[cur], f.bk[1] = bk[cur ^ 1];
     f.bv[0] = bv[cur], f.bv[1] = bv[cur ^ 1];
-    f.n = (int64_t)n, f.T = T, f.ntiles = (int64_t)((n + Tm - 1) / Tm), f.P = passes;
+    f.n = (int64_t)n, f.T = Lq, f.ntiles = (int64_t)((n + Tm - 1) / Tm), f.P = left;
     f.done = done;
     int64_t pb = 0;
-    for (int p = 0; p < passes; ++p) {
+    for (int p = 0; p < left; ++p) {
       f.pair_base[p] = pb;
-      const int64_t twoL = (int64_t)2 * T << p;
+      const int64_t twoL = (int64_t)2 * Lq << p;
       pb += ((int64_t)n + twoL - 1) / twoL;
     }
-    f.pair_base[passes] = pb;
+    f.pair_base[left] = pb;
     MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * 8 + pb * 4, s));
-    return launch_k3(f, (int64_t)passes * ((f.ntiles + kChunk - 1) / kChunk), ctr, s, KC_MERGE);
+    return launch_k3(f, (int64_t)left * ((f.ntiles + kChunk - 1) / kChunk), ctr, s, KC_MERGE);
   }
 
   // Merge `runs` consecutive runs src[off[r], off[r+1]) into dst with rounds of
@@ -579,3 +688,8 @@ int tile_size_for(msort_dtype kd, msort_dtype vd) {
 }
 
 }  // namespace msort
+
+extern "C" int msort_debug_set_quad(int mode) {
+  msort::g_quad_mode = mode;
+  return 0;
+}
