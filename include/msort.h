@@ -111,6 +111,22 @@ msort_status msort_sort_out_ws(const void *in_keys, const void *in_vals, void *k
                                msort_dtype val_dtype, void *ws, size_t ws_bytes,
                                msort_stream_t stream);
 
+/* End-to-end sort of HOST arrays (the e2e path of bench.py).  Enqueued on
+ * `stream`: host_keys[0..n) (and host_vals) are copied into the caller's
+ * device buffers dev_keys (dev_vals), sorted there in place (msort_sort_ws,
+ * same workspace), and copied back to host_keys_out (host_vals_out).  With
+ * page-locked host buffers the call is asynchronous (returns after enqueue;
+ * synchronise the stream before reading host_keys_out); pageable host memory
+ * works, but then the copies block the calling thread.  host_keys may equal
+ * host_keys_out.  PCIe is full duplex: a caller that alternates two streams
+ * and two sets of device buffers overlaps one call's copy-back with the next
+ * call's upload.  Errors: as msort_sort_ws, plus INVALID_VALUE for NULL host
+ * or device pointers with n > 0. */
+msort_status msort_sort_host(const void *host_keys, const void *host_vals, void *host_keys_out,
+                             void *host_vals_out, size_t n, msort_dtype key_dtype,
+                             msort_dtype val_dtype, void *dev_keys, void *dev_vals, void *ws,
+                             size_t ws_bytes, msort_stream_t stream);
+
 /* --------------------------------------------------------------- multi GPU */
 
 /* Fill `id_out` (host, 128 bytes) with a fresh NCCL unique id.  Rank 0 calls

@@ -40,7 +40,7 @@ EXPORTED = (
     "msort_plan_candidates_per_round", "msort_plan_init", "msort_plan_candidates",
     "msort_plan_narrow", "msort_plan_fill", "msort_status_string", "msort_last_error",
     "msort_profile_enable", "msort_profile_reset", "msort_profile_read", "msort_launch_count",
-    "msort_tile_size", "msort_debug_set_quad",
+    "msort_tile_size", "msort_debug_set_quad", "msort_sort_host",
 )
 
 
@@ -62,6 +62,7 @@ def _load():
     L.msort_workspace_bytes.argtypes = [sz, i32, i32, i32, c.POINTER(c.c_size_t)]
     L.msort_sort_ws.argtypes = [vp, vp, sz, i32, i32, vp, sz, vp]
     L.msort_sort_out_ws.argtypes = [vp, vp, vp, vp, sz, i32, i32, vp, sz, vp]
+    L.msort_sort_host.argtypes = [vp, vp, vp, vp, sz, i32, i32, vp, vp, vp, sz, vp]
     L.msort_sort_distributed_out_ws.argtypes = [vp, vp, vp, vp, sz, i32, i32, vp, vp, sz, vp,
                                                 i64p]
     L.msort_comm_unique_id.argtypes = [vp]
@@ -88,7 +89,7 @@ def _load():
     L.msort_tile_size.argtypes = [i32, i32]
     L.msort_tile_size.restype = i32
     for f in ("msort_sort", "msort_sort_pairs", "msort_workspace_bytes", "msort_sort_ws",
-              "msort_sort_out_ws", "msort_sort_distributed_out_ws",
+              "msort_sort_out_ws", "msort_sort_distributed_out_ws", "msort_sort_host",
               "msort_comm_unique_id", "msort_comm_init", "msort_comm_destroy",
               "msort_sort_distributed", "msort_sort_distributed_ws",
               "msort_sort_distributed_emulated", "msort_plan_init", "msort_plan_candidates",
@@ -200,6 +201,30 @@ def msort_sort_out(in_keys: torch.Tensor, keys_out: torch.Tensor, in_vals=None, 
                                      n, kd, vd, _ptr(ws), ws.numel(),
                                      ctypes.c_void_p(_stream(stream))), "msort_sort_out_ws")
     return keys_out, vals_out
+
+
+def msort_sort_host(host_keys: torch.Tensor, host_keys_out: torch.Tensor, dev_keys: torch.Tensor,
+                    host_vals=None, host_vals_out=None, dev_vals=None,
+                    ws: torch.Tensor | None = None, stream=None):
+    """End-to-end sort of host tensors (include/msort.h msort_sort_host):
+    upload into dev_keys (dev_vals), sort there, copy back to host_keys_out
+    (host_vals_out); asynchronous on `stream` for pinned host tensors."""
+    for t, name in ((host_keys, "host_keys"), (host_keys_out, "host_keys_out")):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous host tensor")
+    _check_tensor(dev_keys, "dev_keys")
+    n = host_keys.numel()
+    if host_keys_out.numel() != n or dev_keys.numel() != n:
+        raise ValueError("host/device sizes differ")
+    kd, vd = _dt(dev_keys), _vdt(dev_vals)
+    if ws is None:
+        ws = workspace(n, dev_keys.dtype, dev_vals is not None, device=dev_keys.device)
+    with torch.cuda.device(dev_keys.device):
+        _check(lib.msort_sort_host(_ptr(host_keys), _ptr(host_vals), _ptr(host_keys_out),
+                                   _ptr(host_vals_out), n, kd, vd, _ptr(dev_keys), _ptr(dev_vals),
+                                   _ptr(ws), ws.numel(), ctypes.c_void_p(_stream(stream))),
+               "msort_sort_host")
+    return host_keys_out, host_vals_out
 
 
 def sort(x: torch.Tensor) -> torch.Tensor:

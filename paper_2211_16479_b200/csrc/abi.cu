@@ -278,6 +278,35 @@ msort_status msort_sort_out_ws(const void* in_keys, const void* in_vals, void* k
                               ws_bytes, (cudaStream_t)stream);
 }
 
+msort_status msort_sort_host(const void* host_keys, const void* host_vals, void* host_keys_out,
+                             void* host_vals_out, size_t n, msort_dtype key_dtype,
+                             msort_dtype val_dtype, void* dev_keys, void* dev_vals, void* ws,
+                             size_t ws_bytes, msort_stream_t stream) {
+  if (n == 0) return MSORT_SUCCESS;
+  const bool pairs = val_dtype != MSORT_NONE;
+  if (!host_keys || !host_keys_out || (pairs && (!host_vals || !host_vals_out))) {
+    set_error("msort_sort_host: NULL host pointer");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  MSORT_TRY(validate_out(dev_keys, pairs ? dev_vals : nullptr, dev_keys,
+                         pairs ? dev_vals : nullptr, n, key_dtype, val_dtype));
+  MSORT_TRY(check_device());
+  if (n >= 2)
+    MSORT_TRY(validate_ws(dev_keys, pairs ? dev_vals : nullptr, n, key_dtype, val_dtype, ws,
+                          ws_bytes, single_ws_bytes(n, key_dtype, val_dtype)));
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t kb = n * dtype_size(key_dtype);
+  MSORT_CUDA_TRY(cudaMemcpyAsync(dev_keys, host_keys, kb, cudaMemcpyHostToDevice, s));
+  if (pairs) MSORT_CUDA_TRY(cudaMemcpyAsync(dev_vals, host_vals, n * 4, cudaMemcpyHostToDevice, s));
+  MSORT_TRY(sort_single_dispatch(dev_keys, pairs ? dev_vals : nullptr, dev_keys,
+                                 pairs ? dev_vals : nullptr, n, key_dtype, val_dtype, ws, ws_bytes,
+                                 s));
+  MSORT_CUDA_TRY(cudaMemcpyAsync(host_keys_out, dev_keys, kb, cudaMemcpyDeviceToHost, s));
+  if (pairs)
+    MSORT_CUDA_TRY(cudaMemcpyAsync(host_vals_out, dev_vals, n * 4, cudaMemcpyDeviceToHost, s));
+  return MSORT_SUCCESS;
+}
+
 msort_status msort_comm_unique_id(void* id_out) {
   if (!id_out) {
     set_error("id_out is NULL");

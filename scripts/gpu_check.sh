@@ -9,4 +9,4 @@ timeout 600 python bench.py > gpurun_out/${TAG}_bench.log 2>&1; echo "bench rc=$
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline \
   > gpurun_out/${TAG}_ncu.log 2>&1; echo "ncu rc=$?" >> gpurun_out/${TAG}_ncu.log
-tail -3 gpurun_out/${TAG}_pytest.log gpurun_out/${TAG}_smoke.log gpurun_out/${TAG}_bench.log gpurun_out/${TAG}_ncu.log
+tail -n 3 gpurun_out/${TAG}_pytest.log gpurun_out/${TAG}_smoke.log gpurun_out/${TAG}_bench.log gpurun_out/${TAG}_ncu.log

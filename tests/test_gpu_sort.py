@@ -200,3 +200,33 @@ def test_torch_generator_on_gpu_matches_numpy():
         a = mi.keys(1 << 20, 9, dist)
         b = mi.keys_torch(1 << 20, 9, dist, device="cuda")
         assert np.array_equal(a, to_host(b, a.dtype))
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_sort_host_entry_point(ms, orc, pinned):
+    """msort_sort_host: host -> device -> sort -> host, keys and pairs."""
+    n = 300007
+    k = mi.keys(n, 12, "i64")
+    v = mi.index_payload(n)
+    hk = torch.from_numpy(k.copy())
+    hv = torch.from_numpy(v.view(np.int32).copy())
+    if pinned:
+        hk, hv = hk.pin_memory(), hv.pin_memory()
+    ok = torch.empty_like(hk)
+    ov = torch.empty_like(hv)
+    if pinned:
+        ok, ov = ok.pin_memory(), ov.pin_memory()
+    dk = torch.empty(n, dtype=torch.int64, device="cuda")
+    dv = torch.empty(n, dtype=torch.int32, device="cuda")
+    ms.msort_sort_host(hk, ok, dk, host_vals=hv, host_vals_out=ov, dev_vals=dv)
+    torch.cuda.synchronize()
+    ek, ev = orc.sort(k, v)
+    assert np.array_equal(ok.numpy(), ek)
+    assert np.array_equal(ov.numpy().view(np.uint32), ev)
+    assert np.array_equal(hk.numpy(), k)  # input untouched
+    # keys only, in place on the host buffer
+    hk2 = torch.from_numpy(mi.keys(n, 13, "u32").view(np.int32).copy())
+    dk2 = torch.empty(n, dtype=torch.int32, device="cuda").view(torch.uint32)
+    ms.msort_sort_host(hk2.view(torch.uint32), hk2.view(torch.uint32), dk2)
+    torch.cuda.synchronize()
+    assert np.array_equal(hk2.numpy().view(np.uint32), orc.sort(mi.keys(n, 13, "u32")))
