@@ -296,41 +296,44 @@ def main():
 
     # end to end through the public API with HOST buffers: every step uploads
     # its input from pinned host memory, sorts, and copies the sorted keys back
-    # (N = 1: msort_sort_host; consecutive steps alternate two streams and two
-    # device buffers so one step's copy-back overlaps the next one's upload --
-    # PCIe is full duplex).  Device-timed: from an event before the first step
+    # (N = 1: msort_sort_host; consecutive steps rotate over three streams and
+    # device buffers so one step's copy-back overlaps a later step's upload and
+    # neither copy engine waits behind the other direction -- PCIe is full
+    # duplex).  Device-timed: from an event before the first step
     # to the last step's completion on either stream.
     e2e = None
     if not args.no_e2e:
         h_in = kin.cpu().pin_memory()
-        ke = max(3, min(args.steps, 10))
+        ke = max(6, min(args.steps, 12))
         if world == 1:
-            h_out = [torch.empty_like(h_in).pin_memory() for _ in range(2)]
-            d_buf = [torch.empty_like(kin) for _ in range(2)]
-            wss = [ws, ms.workspace(n, torch.int32, False, device=dev)]
-            strs = [torch.cuda.Stream(device=dev) for _ in range(2)]
+            NS = 3
+            h_out = [torch.empty_like(h_in).pin_memory() for _ in range(NS)]
+            d_buf = [torch.empty_like(kin) for _ in range(NS)]
+            wss = [ws] + [ms.workspace(n, torch.int32, False, device=dev) for _ in range(NS - 1)]
+            strs = [torch.cuda.Stream(device=dev) for _ in range(NS)]
 
             def e2e_step(i):
                 ms.msort_sort_host(h_in, h_out[i], d_buf[i], ws=wss[i], stream=strs[i])
 
-            e2e_step(0)
-            e2e_step(1)
+            for i in range(NS):
+                e2e_step(i)
             torch.cuda.synchronize()
             f0 = torch.cuda.Event(enable_timing=True)
             f0.record(strs[0])
-            strs[1].wait_event(f0)
+            for i in range(1, NS):
+                strs[i].wait_event(f0)
             for k in range(ke):
-                e2e_step(k % 2)
-            fe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-            for i in range(2):
+                e2e_step(k % NS)
+            fe = [torch.cuda.Event(enable_timing=True) for _ in range(NS)]
+            for i in range(NS):
                 fe[i].record(strs[i])
             torch.cuda.synchronize()
-            te = max(f0.elapsed_time(fe[0]), f0.elapsed_time(fe[1]))
-            for i in range(2):
+            te = max(f0.elapsed_time(fe[i]) for i in range(NS))
+            for i in range(NS):
                 o = h_out[i].numpy()
                 ok &= bool(np.all(o[1:] >= o[:-1]))
             path = ("msort_sort_host (pinned host -> device -> sort -> pinned host), "
-                    "steps alternate 2 streams")
+                    f"steps rotate over {NS} streams")
         else:
             h_out = torch.empty_like(h_in).pin_memory()
             d_in = torch.empty_like(kin)
