@@ -9,7 +9,7 @@
 //
 // One persistent, warp-specialised kernel; work is handed out dynamically in
 // chunks of CH consecutive tiles through a global atomic counter.  Roles:
-//   warp 1      co-rank searcher: grabs kGrab chunks at a time and
+//   warp 1      co-rank searcher: grabs `grab` (<= kGrab) chunks at a time and
 //               binary-searches their boundary co-ranks in global memory (one
 //               lane each) into a ring of chunk descriptors (mbarriers);
 //   warp 0      TMA producer: stages A[i0,i1) and B[j0,j1) of each tile into an
@@ -121,11 +121,13 @@ struct SinglePass {
   K* dst_k;
   uint32_t* dst_v;
   int64_t ntiles;
-  __device__ __forceinline__ int64_t nchunks() const { return (ntiles + kChunk - 1) / kChunk; }
+  int ch;    // tiles per chunk (1..kChunk; small sorts use small chunks)
+  int grab;  // chunks per atomic grab (1..kGrab)
+  __device__ __forceinline__ int64_t nchunks() const { return (ntiles + ch - 1) / ch; }
   __device__ __forceinline__ void chunk(int64_t g, int& pass, int64_t& q0, int& cnt) const {
     pass = 0;
-    q0 = g * kChunk;
-    cnt = (int)min((int64_t)kChunk, ntiles - q0);
+    q0 = g * ch;
+    cnt = (int)min((int64_t)ch, ntiles - q0);
   }
   __device__ __forceinline__ int64_t tiles(int) const { return ntiles; }
   __device__ __forceinline__ void wait_ready(int, int64_t, int, int, int) const {}
@@ -161,15 +163,17 @@ struct FusedPasses {
   uint32_t* bv[2];
   int64_t n, T, ntiles;
   int P;
+  int ch;          // tiles per chunk (1..kChunk; small sorts use small chunks)
+  int grab;        // chunks per atomic grab (1..kGrab)
   unsigned* done;  // per level, per pair: tiles completed
   int64_t pair_base[kMaxFusedPasses + 1];
-  __device__ __forceinline__ int64_t cpp() const { return (ntiles + kChunk - 1) / kChunk; }
+  __device__ __forceinline__ int64_t cpp() const { return (ntiles + ch - 1) / ch; }
   __device__ __forceinline__ int64_t nchunks() const { return (int64_t)P * cpp(); }
   __device__ __forceinline__ void chunk(int64_t g, int& pass, int64_t& q0, int& cnt) const {
     const int64_t c = cpp();
     pass = (int)(g / c);
-    q0 = (g % c) * kChunk;
-    cnt = (int)min((int64_t)kChunk, ntiles - q0);
+    q0 = (g % c) * ch;
+    cnt = (int)min((int64_t)ch, ntiles - q0);
   }
   __device__ __forceinline__ int64_t tiles(int) const { return ntiles; }
   __device__ __forceinline__ int64_t L(int pass) const { return T << pass; }
@@ -278,7 +282,9 @@ template <class K, bool PAIRS, int NC, int VT, int S, int MINB, class Src>
 __global__ void __launch_bounds__(NC + kK3Extra, MINB)
     k3_merge_pass(const __grid_constant__ Src src, unsigned long long* __restrict__ ctr) {
   using LY = K3Layout<K, PAIRS, NC, VT, S>;
-  constexpr int Tm = LY::Tm, EK = LY::EK, R = LY::R, CH = kChunk;
+  constexpr int Tm = LY::Tm, EK = LY::EK, CH = kChunk;
+  const int G = src.grab;  // chunks per grab (<= kGrab); chunk ring of R = 2G slots
+  const int R = 2 * G;
   constexpr int NW = (NC + kK3Extra) / 32;  // warps per CTA
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + LY::bars);
@@ -308,7 +314,7 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
       mbar_init(&full[s], 32), mbar_init(&empty[s], 1), mbar_init(&outr[s], NC / 32);
     for (int r = 0; r < R; ++r) mbar_init(&sfull[r], 32), mbar_init(&sempty[r], 1);
     fence_mbar_init();
-    *first_chunk = (int64_t)atomicAdd(ctr, (unsigned long long)kGrab);
+    *first_chunk = (int64_t)atomicAdd(ctr, (unsigned long long)G);
   }
   __syncthreads();
 #ifdef MSORT_K3_TRACE
@@ -316,7 +322,7 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
 #endif
   {
     // the first chunk's co-ranks, one cooperative search per warp; the other
-    // kGrab-1 chunks of this grab go to the searcher
+    // G-1 chunks of this grab go to the searcher
     const int64_t c = *first_chunk;
     if (c >= nchunks) return;  // no work for this CTA (uniform)
     int pass, cnt;
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
 
   if (warp == 1) {
     // ------------------------------------------------ co-rank searcher (K2)
-    // Round g fills ring slots kGrab*g .. kGrab*g+kGrab-1 (mod R) with the
+    // Round g fills ring slots G*g .. G*g+G-1 (mod R) with the
     // chunks of one grab; lanes 9m..9m+8 search chunk m's CH+1 co-ranks.
     static_assert(kGrab * (kChunk + 1) <= 32, "one lane per co-rank");
     mbar_arrive(&sfull[0]);  // slot 0 (first chunk of grab 0) was filled above
@@ -347,12 +353,12 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
     for (int64_t g = 0; !done; ++g) {
       if (g > 0) {
         int64_t c = 0;
-        if (lane == 0) c = (int64_t)atomicAdd(ctr, (unsigned long long)kGrab);
+        if (lane == 0) c = (int64_t)atomicAdd(ctr, (unsigned long long)G);
         c0 = __shfl_sync(0xffffffffu, c, 0);
       }
       const int m = lane / (CH + 1), j = lane % (CH + 1);
-      for (int mm = (g == 0 ? 1 : 0); mm < kGrab; ++mm) {
-        const int64_t b = g * kGrab + mm;  // ring use index
+      for (int mm = (g == 0 ? 1 : 0); mm < G; ++mm) {
+        const int64_t b = g * G + mm;  // ring use index
         const int r = (int)(b % R);
         mbar_wait(&sempty[r], (uint32_t)(((b / R) & 1) ^ 1));
       }
@@ -360,9 +366,9 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
       // level may read an earlier chunk of this very grab, so each group is
       // published before the next one waits for its inputs.
       int mm0 = g == 0 ? 1 : 0;
-      while (mm0 < kGrab && !done) {
+      while (mm0 < G && !done) {
         if (c0 + mm0 >= nchunks) {
-          const int r = (int)((g * kGrab + mm0) % R);
+          const int r = (int)((g * G + mm0) % R);
           if (lane == 0) ring[r].cnt = 0;  // end of work: the producer stops here
           mbar_arrive(&sfull[r]);
           done = true;
@@ -372,7 +378,7 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
         int64_t q_;
         src.chunk(c0 + mm0, pass0, q_, cnt_);
         int mm1 = mm0 + 1;
-        while (mm1 < kGrab && c0 + mm1 < nchunks) {
+        while (mm1 < G && c0 + mm1 < nchunks) {
           int p_, c_;
           int64_t q2;
           src.chunk(c0 + mm1, p_, q2, c_);
@@ -424,7 +430,7 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
           v = merge_path_global_range(sk + A0, sk + A0 + na, dl, lo, hi);
         }
         for (int mm = mm0; mm < mm1; ++mm) {
-          const int r = (int)((g * kGrab + mm) % R);
+          const int r = (int)((g * G + mm) % R);
           if (m == mm && j <= cntm) ring[r].co[j] = v;
           if (lane == 0) {
             int p_, c_;

@@ -275,6 +275,9 @@ extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
 #define MSORT_K3_VT 17  // outputs per merging thread (even: two chains per thread)
 #endif
 
+#ifndef MSORT_K3_CHDIV
+#define MSORT_K3_CHDIV 2  // full chunks per CTA per level below which chunks shrink
+#endif
 #ifndef MSORT_QUAD
 #define MSORT_QUAD 0  // keys only: 1 = two merge levels per HBM pass (k3q_merge.cuh), see DESIGN.md
 #endif
@@ -340,6 +343,15 @@ struct Kernels {
   static int& grid3(int dev) {
     static int g[64] = {};
     return g[dev & 63];
+  }
+
+  // Tiles per scheduled chunk for a level of `tiles` output tiles: kChunk
+  // when every CTA gets >= 2 full chunks per level (few searches, long bulk
+  // streams), else smaller -- a small sort is latency-bound and a level takes
+  // as long as its longest chunk.
+  static int chunk_tiles(int64_t tiles, int dev) {
+    const int64_t per = tiles / (MSORT_K3_CHDIV * (int64_t)std::max(grid3(dev), 1));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(kChunk, per));
   }
 
   // Segments of the 4-way pass over runs of L: groups of 4L, S_full segments
@@ -408,7 +420,7 @@ struct Kernels {
                                 cudaStream_t s, KernelClass kc) {
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
-    const int64_t grid = std::min<int64_t>(grid3(dev), (nchunks + kGrab - 1) / kGrab);
+    const int64_t grid = std::min<int64_t>(grid3(dev), (nchunks + src.grab - 1) / src.grab);
     {
       LaunchScope ls(kc, s);
       k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, Src>
@@ -539,7 +551,9 @@ struct Kernels {
       sp.pm = UniformPairs{(int64_t)n, (int64_t)T << p};
       sp.src_k = bk[cur], sp.src_v = bv[cur], sp.dst_k = bk[cur ^ 1], sp.dst_v = bv[cur ^ 1];
       sp.ntiles = (int64_t)((n + Tm - 1) / Tm);
-      MSORT_TRY(launch_k3(sp, (sp.ntiles + kChunk - 1) / kChunk, ctr + p, s, KC_MERGE));
+      sp.ch = chunk_tiles(sp.ntiles, dev);
+      sp.grab = sp.ch < kChunk ? 1 : kGrab;
+      MSORT_TRY(launch_k3(sp, (sp.ntiles + sp.ch - 1) / sp.ch, ctr + p, s, KC_MERGE));
       cur ^= 1;
     }
     return MSORT_SUCCESS;
@@ -558,7 +572,9 @@ struct Kernels {
     }
     f.pair_base[left] = pb;
     MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * 8 + pb * 4, s));
-    return launch_k3(f, (int64_t)left * ((f.ntiles + kChunk - 1) / kChunk), ctr, s, KC_MERGE);
+    f.ch = chunk_tiles(f.ntiles, dev);
+    f.grab = f.ch < kChunk ? 1 : kGrab;  // small sorts: one chunk per CTA at a time
+    return launch_k3(f, (int64_t)left * ((f.ntiles + f.ch - 1) / f.ch), ctr, s, KC_MERGE);
   }
 
   // Merge `runs` consecutive runs src[off[r], off[r+1]) into dst with rounds of
@@ -568,6 +584,8 @@ struct Kernels {
                            uint32_t* dst_v, const int64_t* off_in, int runs,
                            unsigned long long* ctr, cudaStream_t s) {
     MSORT_TRY(init());
+    int dev = 0;
+    MSORT_CUDA_TRY(cudaGetDevice(&dev));
     const int64_t n = off_in[runs] - off_in[0];
     if (runs <= 1 || n == 0) {
       if (n > 0 && src_k != dst_k) {
@@ -614,7 +632,9 @@ struct Kernels {
       // empty pairs own no tiles; locate() picks the last pair whose first
       // tile <= q, which is never an empty one
       if (tiles > 0)
-        MSORT_TRY(launch_k3(src, (tiles + kChunk - 1) / kChunk, ctr + round, s, KC_KWAY));
+        src.ch = chunk_tiles(tiles, dev);
+        src.grab = src.ch < kChunk ? 1 : kGrab;
+        MSORT_TRY(launch_k3(src, (tiles + src.ch - 1) / src.ch, ctr + round, s, KC_KWAY));
       int nr = pm.npairs;
       for (int m = 0; m <= nr; ++m) off[m] = off[std::min(2 * m, runs)];
       runs = nr;
