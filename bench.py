@@ -140,6 +140,24 @@ def cpu_baseline(n_sample: int, samples: int):
                       f"(oracle/msort_oracle.c), {t:.1f} s of CPU"}
 
 
+def cpu_paper_mp(n_sample: int):
+    """SURVEY.md §8(d) O-c: the paper's multiprocessing merge sort (chunks of
+    ceil(n/c) sorted in parallel, then pairwise merges) re-created
+    on host threads by the oracle library, all host cores, one 2^k sample."""
+    import msort_inputs as mi
+    import oracle
+
+    cores = len(os.sched_getaffinity(0))
+    k = mi.keys(n_sample, SEED0 + 200, "u31")
+    t0 = time.perf_counter()
+    oracle.paper_mp_inplace(k, None, cores)
+    t = time.perf_counter() - t0
+    return {"value": n_sample / t, "unit": "keys/s", "cores": cores, "kind": "oracle_paper_mp",
+            "sample": f"2^{n_sample.bit_length() - 1} int32 keys uniform [0,2^31), the paper's "
+                      f"multiprocessing merge sort on {cores} host threads "
+                      f"(oracle/msort_oracle.c msort_oracle_paper_mp), {t:.1f} s"}
+
+
 def reference_arm(args, rank):
     """--impl reference: the CPU oracle on a bounded sample per step."""
     if rank != 0:
@@ -363,9 +381,10 @@ def main():
                "h2d_bytes_per_step": n * wk, "d2h_bytes_per_step": n * wk,
                "ms_per_step": te / ke, "steps": ke, "path": path}
 
-    cpu = None
+    cpu = cpu_mp = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(1 << 24, 3)
+        cpu_mp = cpu_paper_mp(1 << 26)
 
     if rank == 0:
         value = world * n * args.steps / (ms_total / 1e3)
@@ -388,6 +407,7 @@ def main():
                               "floor_frac": round(2 * n * wk / (peak * 1e9) * 1e3 / ms_step, 4)},
             "phases": phases,
             "cpu_baseline": cpu,
+            "cpu_paper_mp": cpu_mp,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,

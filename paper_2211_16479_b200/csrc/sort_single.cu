@@ -263,7 +263,7 @@ extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
 
 // ------------------------------------------------------------ host driver
 #ifndef MSORT_K3_NC
-#define MSORT_K3_NC 256  // merging threads per K3 CTA
+#define MSORT_K3_NC 512  // merging threads per K3 CTA (4-byte keys only; 256 otherwise)
 #endif
 #ifndef MSORT_K1_NT
 #define MSORT_K1_NT 256  // keys-only K1 threads
@@ -317,14 +317,25 @@ struct Kernels {
   static constexpr int VT = PAIRS ? 17 : MSORT_K1_VT;
   static constexpr int NT1 = PAIRS ? 512 : MSORT_K1_NT;
   static constexpr int T = NT1 * VT;  // tile sort size
-  static constexpr int NC = MSORT_K3_NC;
+  // 4-byte keys: 512 mergers x 17 = one 8704-key output tile (= T) per stage,
+  // 2 CTAs/SM -- half the tiles (and co-rank searches) of 256 x 17, measured
+  // 5.35 vs 5.71 ms for the 15 levels of 2^28; wider records
+  // keep 256 mergers so three stages fit in shared memory.
+  static constexpr bool WIDE3 = sizeof(K) == 4 && !PAIRS;
+  static constexpr int NC = WIDE3 ? MSORT_K3_NC : 256;
   static constexpr int VT3 = PAIRS ? 17 : MSORT_K3_VT;
   static constexpr int Tm = NC * VT3;  // merge output tile (divides 2T)
-  static constexpr int S = 3;
+#ifndef MSORT_K3_S
+#define MSORT_K3_S 3
+#endif
+  static constexpr int S = MSORT_K3_S;  // stage ring depth
   using LY = K3Layout<K, PAIRS, NC, VT3, S>;
   // CTAs per SM the register budget is tuned for (shared memory allows 4 for
   // 4-byte keys without payload, 2-3 otherwise)
-  static constexpr int MINB = (sizeof(K) == 4 && !PAIRS) ? 4 : 2;
+#ifndef MSORT_K3_MINB
+#define MSORT_K3_MINB 2
+#endif
+  static constexpr int MINB = WIDE3 ? MSORT_K3_MINB : 2;  // CTAs/SM the registers are tuned for
   static constexpr size_t k1_smem =
       PAIRS ? (size_t)T * sizeof(K) + (size_t)T * 8 : K1KeysShape<K, NT1, VT>::smem;
   static constexpr size_t k3_smem = LY::bytes;
