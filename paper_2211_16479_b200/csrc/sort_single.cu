@@ -322,20 +322,24 @@ struct Kernels {
   // 5.35 vs 5.71 ms for the 15 levels of 2^28; wider records
   // keep 256 mergers so three stages fit in shared memory.
   static constexpr bool WIDE3 = sizeof(K) == 4 && !PAIRS;
-  static constexpr int NC = WIDE3 ? MSORT_K3_NC : 256;
+  // 8-byte keys (with or without payload): 512 mergers and two stages, one
+  // CTA/SM (C3: 4.25 -> 3.67 ms of merging); 4-byte keys with a payload keep
+  // 256 mergers and three stages (512 x 2 stages: C4 5.40 -> 6.10 ms).
+  static constexpr bool WIDE8 = sizeof(K) == 8;
+  static constexpr int NC = WIDE3 ? MSORT_K3_NC : (WIDE8 ? 512 : 256);
   static constexpr int VT3 = PAIRS ? 17 : MSORT_K3_VT;
   static constexpr int Tm = NC * VT3;  // merge output tile (divides 2T)
 #ifndef MSORT_K3_S
 #define MSORT_K3_S 3
 #endif
-  static constexpr int S = MSORT_K3_S;  // stage ring depth
+  static constexpr int S = WIDE3 ? MSORT_K3_S : (WIDE8 ? 2 : 3);  // stage ring depth
   using LY = K3Layout<K, PAIRS, NC, VT3, S>;
   // CTAs per SM the register budget is tuned for (shared memory allows 4 for
   // 4-byte keys without payload, 2-3 otherwise)
 #ifndef MSORT_K3_MINB
 #define MSORT_K3_MINB 2
 #endif
-  static constexpr int MINB = WIDE3 ? MSORT_K3_MINB : 2;  // CTAs/SM the registers are tuned for
+  static constexpr int MINB = WIDE3 ? MSORT_K3_MINB : (WIDE8 ? 1 : 2);  // CTAs/SM for registers
   static constexpr size_t k1_smem =
       PAIRS ? (size_t)T * sizeof(K) + (size_t)T * 8 : K1KeysShape<K, NT1, VT>::smem;
   static constexpr size_t k3_smem = LY::bytes;
