@@ -254,6 +254,19 @@ int msort_tile_size(msort_dtype key_dtype, msort_dtype val_dtype);
  * Returns 0. */
 int msort_debug_set_quad(int mode);
 
+/* Exchange mode of the distributed sort (D3+D4).  mode 0 (default): one NCCL
+ * all-to-all (grouped ncclSend/ncclRecv) into a receive buffer, then the local
+ * k-way merge.  mode 1 ("pull", the fused exchange): D1 leaves each sorted
+ * shard in the workspace's exchange buffer, every rank publishes that buffer
+ * through CUDA IPC, and the first k-way merge round reads its p segments in
+ * place from their owners (peer memory over NVLink/NVSwitch) -- the segments
+ * cross NVLink once, straight into the merge, with no receive-buffer pass
+ * through HBM; a barrier then frees the exchange buffers.  Requires the
+ * workspace to come from cudaMalloc (IPC-exportable).  Validated on one GPU
+ * through msort_sort_distributed_emulated (the same kernels, peers = local
+ * buffers); environment MSORT_EXCHANGE=pull selects it too.  Returns 0. */
+int msort_debug_set_exchange(int mode);
+
 #ifdef __cplusplus
 }
 #endif

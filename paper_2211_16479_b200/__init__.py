@@ -40,7 +40,7 @@ EXPORTED = (
     "msort_plan_candidates_per_round", "msort_plan_init", "msort_plan_candidates",
     "msort_plan_narrow", "msort_plan_fill", "msort_status_string", "msort_last_error",
     "msort_profile_enable", "msort_profile_reset", "msort_profile_read", "msort_launch_count",
-    "msort_tile_size", "msort_debug_set_quad", "msort_sort_host",
+    "msort_tile_size", "msort_debug_set_quad", "msort_sort_host", "msort_debug_set_exchange",
 )
 
 
@@ -396,6 +396,13 @@ def profile_read():
 
 def launch_count() -> int:
     return int(lib.msort_launch_count())
+
+
+def set_exchange_mode(mode: int) -> None:
+    """Distributed exchange (include/msort.h msort_debug_set_exchange): 0 NCCL
+    all-to-all then k-way merge, 1 pull (first merge round reads the peers'
+    sorted segments in place)."""
+    lib.msort_debug_set_exchange(int(mode))
 
 
 def set_quad_mode(mode: int) -> None:

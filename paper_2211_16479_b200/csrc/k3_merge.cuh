@@ -30,6 +30,8 @@
 //                 the whole previous one.
 #pragma once
 
+#include <type_traits>
+
 #include "msort_device.cuh"
 
 namespace msort {
@@ -51,6 +53,16 @@ struct UniformPairs {  // runs of length L (the last ones may be short)
     nb = B0 < n ? min(L, n - B0) : 0;
     dl = d - A0;
   }
+  // runs A and B of tile q's pair (output at A0): contiguous in src
+  template <class T>
+  __device__ __forceinline__ const T* ra(const T* src, int64_t, int64_t A0, int64_t, bool) const {
+    return src + A0;
+  }
+  template <class T>
+  __device__ __forceinline__ const T* rb(const T* src, int64_t, int64_t A0, int64_t na,
+                                         bool) const {
+    return src + A0 + na;
+  }
 };
 
 constexpr int kMaxPairs = 64;
@@ -66,6 +78,53 @@ struct ExplicitPairs {  // arbitrary consecutive runs, pairs (2m, 2m+1)
     na = off[2 * m + 1] - A0;
     nb = off[2 * m + 2] - off[2 * m + 1];
     dl = (q - first_tile[m]) * T;
+  }
+  template <class T>
+  __device__ __forceinline__ const T* ra(const T* src, int64_t, int64_t A0, int64_t, bool) const {
+    return src + A0;
+  }
+  template <class T>
+  __device__ __forceinline__ const T* rb(const T* src, int64_t, int64_t A0, int64_t na,
+                                         bool) const {
+    return src + A0 + na;
+  }
+};
+
+// Runs that live in different buffers -- on a multi-GPU run, in the peers'
+// memory (NVLink/NVSwitch, mapped into this process): pair m merges run
+// a[m] (na[m] keys) with run b[m] (nb[m]) into the output at out[m].  The
+// first k-way merge round of the distributed sort reads the p sorted segments
+// straight from their owners this way ("pull" exchange).
+struct PeerPairs {
+  int npairs;
+  int64_t first_tile[kMaxPairs + 1];
+  int64_t out[kMaxPairs];
+  int64_t na[kMaxPairs], nb[kMaxPairs];
+  const void* ka[kMaxPairs];
+  const void* kb[kMaxPairs];
+  const uint32_t* va[kMaxPairs];
+  const uint32_t* vb[kMaxPairs];
+  __device__ __forceinline__ int find(int64_t q) const {
+    int m = 0;
+    while (m + 1 < npairs && first_tile[m + 1] <= q) ++m;
+    return m;
+  }
+  __device__ __forceinline__ void locate(int64_t q, int T, int64_t& A0, int64_t& na_,
+                                         int64_t& nb_, int64_t& dl) const {
+    const int m = find(q);
+    A0 = out[m], na_ = na[m], nb_ = nb[m];
+    dl = (q - first_tile[m]) * T;
+  }
+  // keys (vals = false) or payloads (vals = true) of tile q's runs
+  template <class T>
+  __device__ __forceinline__ const T* ra(const T*, int64_t q, int64_t, int64_t, bool vals) const {
+    const int m = find(q);
+    return vals ? reinterpret_cast<const T*>(va[m]) : static_cast<const T*>(ka[m]);
+  }
+  template <class T>
+  __device__ __forceinline__ const T* rb(const T*, int64_t q, int64_t, int64_t, bool vals) const {
+    const int m = find(q);
+    return vals ? reinterpret_cast<const T*>(vb[m]) : static_cast<const T*>(kb[m]);
   }
 };
 
@@ -137,6 +196,19 @@ struct SinglePass {
   }
   __device__ __forceinline__ const K* srck(int) const { return src_k; }
   __device__ __forceinline__ const uint32_t* srcv(int) const { return src_v; }
+  // runs A / B (keys, payloads) of tile q, whose pair's output starts at A0
+  __device__ __forceinline__ const K* pa(int, int64_t q, int64_t A0, int64_t na) const {
+    return pm.ra(src_k, q, A0, na, false);
+  }
+  __device__ __forceinline__ const K* pb(int, int64_t q, int64_t A0, int64_t na) const {
+    return pm.rb(src_k, q, A0, na, false);
+  }
+  __device__ __forceinline__ const uint32_t* pva(int, int64_t q, int64_t A0, int64_t na) const {
+    return pm.ra(src_v, q, A0, na, true);
+  }
+  __device__ __forceinline__ const uint32_t* pvb(int, int64_t q, int64_t A0, int64_t na) const {
+    return pm.rb(src_v, q, A0, na, true);
+  }
   __device__ __forceinline__ K* dstk(int) const { return dst_k; }
   __device__ __forceinline__ uint32_t* dstv(int) const { return dst_v; }
   __device__ __forceinline__ void tile_done(int, int64_t, int) const {}
@@ -205,6 +277,18 @@ struct FusedPasses {
   }
   __device__ __forceinline__ const K* srck(int p) const { return bk[p & 1]; }
   __device__ __forceinline__ const uint32_t* srcv(int p) const { return bv[p & 1]; }
+  __device__ __forceinline__ const K* pa(int p, int64_t, int64_t A0, int64_t) const {
+    return bk[p & 1] + A0;
+  }
+  __device__ __forceinline__ const K* pb(int p, int64_t, int64_t A0, int64_t na) const {
+    return bk[p & 1] + A0 + na;
+  }
+  __device__ __forceinline__ const uint32_t* pva(int p, int64_t, int64_t A0, int64_t) const {
+    return bv[p & 1] + A0;
+  }
+  __device__ __forceinline__ const uint32_t* pvb(int p, int64_t, int64_t A0, int64_t na) const {
+    return bv[p & 1] + A0 + na;
+  }
   __device__ __forceinline__ K* dstk(int p) const { return bk[(p + 1) & 1]; }
   __device__ __forceinline__ uint32_t* dstv(int p) const { return bv[(p + 1) & 1]; }
   // Called by one thread after the tile's output (bulk store waited for,
@@ -252,8 +336,8 @@ __device__ __forceinline__ int64_t corank_warp(const Src& src, int pass, int64_t
                                                int lane) {
   int64_t A0, na, nb, dl;
   src.locate(pass, q, T, A0, na, nb, dl);
-  const K* a = src.srck(pass) + A0;
-  const K* b = a + na;
+  const K* a = src.pa(pass, q, A0, na);
+  const K* b = src.pb(pass, q, A0, na);
   int64_t lo = dl - nb > 0 ? dl - nb : 0;
   int64_t hi = dl < na ? dl : na;
   while (hi > lo) {
@@ -407,9 +491,10 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
           valid = j <= cntm && q0m + j < src.tiles(pass0);
           if (valid) src.locate(pass0, q0m + j, Tm, A0, na, nb, dl);
         }
-        const K* sk = src.srck(pass0);
+        const K* ra = valid ? src.pa(pass0, q0m + j, A0, na) : nullptr;
+        const K* rbp = valid ? src.pb(pass0, q0m + j, A0, na) : nullptr;
         const bool edge = j == 0 || j == cntm;
-        if (valid && edge) v = merge_path_global(sk + A0, na, sk + A0 + na, nb, dl);
+        if (valid && edge) v = merge_path_global(ra, na, rbp, nb, dl);
         const int l0 = m * (CH + 1) < 32 ? m * (CH + 1) : 0;
         const int le = l0 + cntm < 32 ? l0 + cntm : 0;
         const int64_t v0 = __shfl_sync(0xffffffffu, v, l0);
@@ -427,7 +512,7 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
             lo = max(lo, ve - (int64_t)(cntm - j) * Tm);
             hi = min(hi, ve);
           }
-          v = merge_path_global_range(sk + A0, sk + A0 + na, dl, lo, hi);
+          v = merge_path_global_range(ra, rbp, dl, lo, hi);
         }
         for (int mm = mm0; mm < mm1; ++mm) {
           const int r = (int)((g * G + mm) % R);
@@ -463,8 +548,6 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
       // inputs written by other SMs (generic or bulk stores) were acquired by
       // the searcher; order them before this thread's bulk (async-proxy) loads
       if constexpr (Src::kFused) fence_proxy_async_global();
-      const K* src_k = src.srck(pass);
-      const uint32_t* src_v = src.srcv(pass);
       for (int j = 0; j < ccnt; ++j, ++k) {
         const int64_t q = cd.q0 + j;
         const int s = (int)(k % S);
@@ -476,8 +559,8 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
         const int64_t i1 = d1 == tot_all ? na_all : cd.co[j + 1];
         const int64_t j0 = d0 - i0, j1 = d1 - i1;
         const int na = (int)(i1 - i0), nb = (int)(j1 - j0);
-        const K* a = src_k + A0 + i0;
-        const K* bp = src_k + A0 + na_all + j0;
+        const K* a = src.pa(pass, q, A0, na_all) + i0;
+        const K* bp = src.pb(pass, q, A0, na_all) + j0;
         const int offA = stage_offset(a);
         const int offB = (offA + na + EK - 1) / EK * EK + stage_offset(bp);
         K3_CHECK(i0 >= 0 && i0 <= i1 && i1 <= na_all && j0 >= 0 && j0 <= j1 && j1 <= nb_all &&
@@ -489,8 +572,8 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
         const uint32_t* bv = nullptr;
         int offAv = 0, offBv = 0;
         if constexpr (PAIRS) {
-          av = src_v + A0 + i0;
-          bv = src_v + A0 + na_all + j0;
+          av = src.pva(pass, q, A0, na_all) + i0;
+          bv = src.pvb(pass, q, A0, na_all) + j0;
           offAv = stage_offset(av);
           offBv = (offAv + na + 3) / 4 * 4 + stage_offset(bv);
         }

@@ -76,4 +76,23 @@ msort_status kway_merge_dispatch(void* src_k, void* src_v, void* tmp_k, void* tm
                                  void* dst_k, void* dst_v, const int64_t* off_host, int runs,
                                  msort_dtype kd, msort_dtype vd, void* part_ws, cudaStream_t s);
 
+// Runs of the pull exchange's first merge round: run r is n[r] keys at k[r]
+// (payloads at v[r]) -- device pointers, possibly into a peer GPU's memory.
+constexpr int kMaxPullRuns = 128;
+struct PullRuns {
+  int runs;
+  const void* k[kMaxPullRuns];
+  const uint32_t* v[kMaxPullRuns];
+  int64_t n[kMaxPullRuns];
+};
+// Merges runs (2m, 2m+1) into out (pair m at the sum of the earlier pairs'
+// sizes); off_out gets the ceil(runs/2)+1 boundaries of the result.
+msort_status pull_round_dispatch(const PullRuns& pr, void* out_k, void* out_v, int64_t* off_out,
+                                 msort_dtype kd, msort_dtype vd, void* part_ws, cudaStream_t s);
+
+// Exchange mode of the distributed sort: 0 = NCCL all-to-all into a receive
+// buffer then a local k-way merge; 1 = pull (the first merge round reads the
+// peers' sorted segments in place).  (sort_dist.cu, msort_debug_set_exchange)
+int exchange_mode();
+
 }  // namespace msort

@@ -15,8 +15,12 @@
 // R10/R11), so the call is in place and balanced for any key distribution.
 #include <nccl.h>
 
+#include <cuda.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -28,6 +32,9 @@ struct msort_comm_s {
   ncclComm_t comm;
   int rank;
   int world;
+  // pull exchange: peers' exchange buffers opened through CUDA IPC, cached by
+  // (rank, handle) -- the workspace allocation is normally reused call to call
+  std::map<std::pair<int, std::string>, void*> ipc_open;
 };
 
 namespace msort {
@@ -150,7 +157,15 @@ struct DistWs {
   void* rv;  // receive vals
   uint64_t *nsz_send, *nsz, *lohi, *cnt, *lteq, *lteq_all;
   int64_t* split;
+  unsigned char *ipc_send, *ipc_all;  // pull exchange: (handle, offset) of the exchange buffers
 };
+
+// CUDA IPC record of one rank's exchange buffers (keys, vals).
+struct IpcRec {
+  cudaIpcMemHandle_t hk, hv;
+  int64_t ok, ov;  // offsets of the buffers inside their allocations
+};
+constexpr size_t kIpcBytes = (sizeof(IpcRec) + 255) / 256 * 256;
 
 static size_t d2_bytes(int world) {
   size_t nb = world > 1 ? world - 1 : 1;
@@ -162,6 +177,7 @@ static size_t d2_bytes(int world) {
   b += align_up(16 * nb, 256);                         // lteq
   b += align_up(16 * nb * (size_t)world, 256);         // lteq_all
   b += align_up(8 * (size_t)(world + 1) * world, 256); // split
+  b += kIpcBytes * (size_t)(world + 1);                // ipc_send, ipc_all
   return b;
 }
 
@@ -185,7 +201,9 @@ static DistWs carve(void* ws, size_t n, msort_dtype kd, msort_dtype vd, int worl
   d.cnt = (uint64_t*)w; w += align_up(8 * nb * B, 256);
   d.lteq = (uint64_t*)w; w += align_up(16 * nb, 256);
   d.lteq_all = (uint64_t*)w; w += align_up(16 * nb * (size_t)world, 256);
-  d.split = (int64_t*)w;
+  d.split = (int64_t*)w; w += align_up(8 * (size_t)(world + 1) * world, 256);
+  d.ipc_send = (unsigned char*)w; w += kIpcBytes;
+  d.ipc_all = (unsigned char*)w;
   return d;
 }
 
@@ -206,6 +224,8 @@ struct RankIO {
   void* vals;
   size_t n;
   DistWs ws;
+  void* sk;  // where D1 leaves the sorted shard: keys, or (pull) the exchange buffer ws.rk
+  void* sv;
 };
 
 static ncclDataType_t nccl_type(msort_dtype d) {
@@ -281,6 +301,81 @@ struct NcclColl {
     return MSORT_SUCCESS;
   }
   int rank_of(int local) const { return c->rank + local; }
+  // pull exchange: after the peers' reads, nobody may reuse its buffer
+  msort_status barrier(RankIO* io) {
+    LaunchScope ls(KC_NCCL, s);
+    MSORT_NCCL_TRY(ncclAllReduce(io[0].ws.nsz, io[0].ws.nsz, 1, ncclUint64, ncclMax, c->comm, s));
+    return MSORT_SUCCESS;
+  }
+  // pull exchange, step 1 (enqueued before the host sync): publish the CUDA
+  // IPC handles of this rank's exchange buffers and gather everyone's into
+  // `host` (valid after the stream synchronises).
+  msort_status ipc_publish(RankIO* io, unsigned char* host) {
+    IpcRec me{};
+    for (int which = 0; which < 2; ++which) {
+      void* p = which == 0 ? io[0].sk : io[0].sv;
+      if (!p) continue;
+      // the driver's cuMemGetAddressRange through the runtime (no libcuda link)
+      using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+      static GetRange get_range = nullptr;
+      if (!get_range) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        MSORT_CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+        get_range = reinterpret_cast<GetRange>(fn);
+      }
+      CUdeviceptr base = 0;
+      size_t size = 0;
+      if (!get_range || get_range(&base, &size, (CUdeviceptr)p) != CUDA_SUCCESS) {
+        set_error("pull exchange: cuMemGetAddressRange failed on the workspace");
+        return MSORT_ERROR_NOT_SUPPORTED;
+      }
+      cudaIpcMemHandle_t h;
+      MSORT_CUDA_TRY(cudaIpcGetMemHandle(&h, (void*)base));
+      (which == 0 ? me.hk : me.hv) = h;
+      (which == 0 ? me.ok : me.ov) = (int64_t)((CUdeviceptr)p - base);
+    }
+    MSORT_CUDA_TRY(cudaMemcpyAsync(io[0].ws.ipc_send, &me, sizeof(me), cudaMemcpyHostToDevice, s));
+    {
+      LaunchScope ls(KC_NCCL, s);
+      MSORT_NCCL_TRY(ncclAllGather(io[0].ws.ipc_send, io[0].ws.ipc_all, kIpcBytes, ncclUint8,
+                                   c->comm, s));
+    }
+    MSORT_CUDA_TRY(cudaMemcpyAsync(host, io[0].ws.ipc_all, kIpcBytes * c->world,
+                                   cudaMemcpyDeviceToHost, s));
+    // the host copy of `me` must outlive the async copy: wait for it here
+    MSORT_CUDA_TRY(cudaStreamSynchronize(s));
+    return MSORT_SUCCESS;
+  }
+  // step 2 (after the sync): map every peer's exchange buffers (cached).
+  msort_status peer_bases(RankIO* io, const unsigned char* host, bool pairs,
+                          std::vector<const void*>& bk, std::vector<const uint32_t*>& bv) {
+    const int p = c->world;
+    bk.assign(p, nullptr), bv.assign(p, nullptr);
+    for (int j = 0; j < p; ++j) {
+      if (j == c->rank) {
+        bk[j] = io[0].sk, bv[j] = (const uint32_t*)io[0].sv;
+        continue;
+      }
+      IpcRec r;
+      memcpy(&r, host + (size_t)j * kIpcBytes, sizeof(r));
+      for (int which = 0; which < (pairs ? 2 : 1); ++which) {
+        const cudaIpcMemHandle_t& h = which == 0 ? r.hk : r.hv;
+        auto key = std::make_pair(j, std::string(reinterpret_cast<const char*>(&h), sizeof(h)));
+        auto it = c->ipc_open.find(key);
+        void* base = nullptr;
+        if (it != c->ipc_open.end()) {
+          base = it->second;
+        } else {
+          MSORT_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+          c->ipc_open[key] = base;
+        }
+        if (which == 0) bk[j] = (const char*)base + r.ok;
+        else bv[j] = (const uint32_t*)((const char*)base + r.ov);
+      }
+    }
+    return MSORT_SUCCESS;
+  }
 };
 
 // Collectives emulated on one device for `world` virtual ranks.
@@ -329,17 +424,25 @@ struct EmulColl {
     return MSORT_SUCCESS;
   }
   int rank_of(int local) const { return local; }
+  msort_status barrier(RankIO*) { return MSORT_SUCCESS; }  // one stream: program order
+  msort_status ipc_publish(RankIO*, unsigned char*) { return MSORT_SUCCESS; }
+  msort_status peer_bases(RankIO* io, const unsigned char*, bool,
+                          std::vector<const void*>& bk, std::vector<const uint32_t*>& bv) {
+    bk.assign(p, nullptr), bv.assign(p, nullptr);
+    for (int j = 0; j < p; ++j) bk[j] = io[j].sk, bv[j] = (const uint32_t*)io[j].sv;
+    return MSORT_SUCCESS;
+  }
 };
 
 template <class K>
 static void launch_count(const RankIO& io, int nb, cudaStream_t s) {
   int tot = nb * B;
-  k4_count<K><<<(tot + 255) / 256, 256, 0, s>>>((const K*)io.keys, (int64_t)io.n, io.ws.lohi, nb,
+  k4_count<K><<<(tot + 255) / 256, 256, 0, s>>>((const K*)io.sk, (int64_t)io.n, io.ws.lohi, nb,
                                                 io.ws.cnt);
 }
 template <class K>
 static void launch_lteq(const RankIO& io, int nb, cudaStream_t s) {
-  k4_lteq<K><<<(2 * nb + 255) / 256, 256, 0, s>>>((const K*)io.keys, (int64_t)io.n, io.ws.lohi,
+  k4_lteq<K><<<(2 * nb + 255) / 256, 256, 0, s>>>((const K*)io.sk, (int64_t)io.n, io.ws.lohi,
                                                   nb, io.ws.lteq);
 }
 
@@ -347,12 +450,12 @@ static int rounds_for(msort_dtype kd) { return dtype_size(kd) == 4 ? 4 : 8; }
 
 template <class Coll>
 static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msort_dtype vd,
-                             cudaStream_t s, int64_t* split_out) {
+                             cudaStream_t s, int64_t* split_out, bool pull_mode) {
   const int p = C.world();
   const int nb = p - 1;
   // D1: local sorts
   for (int l = 0; l < nloc; ++l)
-    MSORT_TRY(sort_single_dispatch(io[l].in_keys, io[l].in_vals, io[l].keys, io[l].vals, io[l].n,
+    MSORT_TRY(sort_single_dispatch(io[l].in_keys, io[l].in_vals, io[l].sk, io[l].sv, io[l].n,
                                    kd, vd, io[l].ws.sort_ws, io[l].ws.sort_ws_bytes, s));
   std::vector<int64_t> S((size_t)(p + 1) * p);
   if (p == 1) {
@@ -407,6 +510,9 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
   }
   MSORT_CUDA_TRY(cudaGetLastError());
   // The one host synchronisation: the exchange sizes are needed on the host.
+  const bool pull = pull_mode;
+  std::vector<unsigned char> ipc_host(pull ? kIpcBytes * (size_t)p : 0);
+  if (pull) MSORT_TRY(C.ipc_publish(io, ipc_host.data()));
   MSORT_CUDA_TRY(cudaMemcpyAsync(S.data(), io[0].ws.split, S.size() * 8, cudaMemcpyDeviceToHost, s));
   MSORT_CUDA_TRY(cudaStreamSynchronize(s));
   if (split_out) memcpy(split_out, S.data(), S.size() * 8);
@@ -420,6 +526,54 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
       return MSORT_ERROR_INVALID_VALUE;
     }
   }
+  const size_t wk = dtype_size(kd);
+  const bool pairs = vd != MSORT_NONE;
+  if (pull) {
+    // D3+D4 fused ("pull"): round 1 of the k-way merge reads every rank's
+    // sorted segment in place (peer memory over NVLink on a real run), so
+    // the segments cross NVLink once, straight into the merge, with no
+    // receive-buffer pass through HBM.
+    std::vector<const void*> bk;
+    std::vector<const uint32_t*> bv;
+    MSORT_TRY(C.peer_bases(io, ipc_host.data(), pairs, bk, bv));
+    int rounds = 0;
+    while ((1 << rounds) < p) ++rounds;
+    std::vector<std::vector<int64_t>> offs(nloc);
+    for (int l = 0; l < nloc; ++l) {
+      const int me = C.rank_of(l);
+      offs[l].assign((size_t)p + 1, 0);
+      if (io[l].n == 0) continue;
+      PullRuns pr{};
+      pr.runs = p;
+      for (int j = 0; j < p; ++j) {
+        const int64_t a = S[(size_t)me * p + j], b = S[(size_t)(me + 1) * p + j];
+        pr.k[j] = (const char*)bk[j] + a * wk;
+        pr.v[j] = pairs ? bv[j] + a : nullptr;
+        pr.n[j] = b - a;
+      }
+      char* sw = io[l].ws.sort_ws;
+      void* tk = sw;
+      void* tv = pairs ? sw + align_up(io[l].n * wk, 256) : nullptr;
+      void* part = sw + align_up(io[l].n * wk, 256) + (pairs ? align_up(io[l].n * 4, 256) : 0);
+      void* ok = rounds == 1 ? io[l].keys : tk;
+      void* ov = rounds == 1 ? io[l].vals : tv;
+      MSORT_TRY(pull_round_dispatch(pr, ok, ov, offs[l].data(), kd, vd, part, s));
+    }
+    // every rank has read the others' segments: exchange buffers are free
+    MSORT_TRY(C.barrier(io));
+    if (rounds > 1) {
+      for (int l = 0; l < nloc; ++l) {
+        if (io[l].n == 0) continue;
+        char* sw = io[l].ws.sort_ws;
+        void* tk = sw;
+        void* tv = pairs ? sw + align_up(io[l].n * wk, 256) : nullptr;
+        void* part = sw + align_up(io[l].n * wk, 256) + (pairs ? align_up(io[l].n * 4, 256) : 0);
+        MSORT_TRY(kway_merge_dispatch(tk, tv, io[l].ws.rk, io[l].ws.rv, io[l].keys, io[l].vals,
+                                      offs[l].data(), (p + 1) / 2, kd, vd, part, s));
+      }
+    }
+    return MSORT_SUCCESS;
+  }
   // D3: exchange
   MSORT_TRY(C.exchange(io, S, kd, vd));
   // D4: k-way merge of the received runs (source-rank order) into keys
@@ -429,7 +583,6 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
     off[0] = 0;
     for (int j = 0; j < p; ++j) off[j + 1] = off[j] + S[(size_t)(me + 1) * p + j] - S[(size_t)me * p + j];
     if (io[l].n == 0) continue;
-    const size_t wk = dtype_size(kd);
     char* sw = io[l].ws.sort_ws;  // sort workspace doubles as the ping-pong buffer
     void* tk = sw;
     void* tv = vd != MSORT_NONE ? sw + align_up(io[l].n * wk, 256) : nullptr;
@@ -448,10 +601,13 @@ msort_status dist_nccl(const void* in_keys, const void* in_vals, void* keys, voi
     return MSORT_ERROR_NOT_SUPPORTED;
   }
   const bool pv = vd != MSORT_NONE;
+  const bool pull = exchange_mode() == 1 && comm->world > 1;
   RankIO io{in_keys, pv ? in_vals : nullptr, keys, pv ? vals : nullptr, n,
-            carve(ws, n, kd, vd, comm->world)};
+            carve(ws, n, kd, vd, comm->world), nullptr, nullptr};
+  io.sk = pull ? io.ws.rk : io.keys;
+  io.sv = pull ? io.ws.rv : io.vals;
   NcclColl C{comm, s};
-  return dist_run(C, &io, 1, kd, vd, s, split_out);
+  return dist_run(C, &io, 1, kd, vd, s, split_out, pull);
 }
 
 msort_status dist_emulated(void* const* keys, void* const* vals, const size_t* n, int world,
@@ -465,11 +621,25 @@ msort_status dist_emulated(void* const* keys, void* const* vals, const size_t* n
   for (int r = 0; r < world; ++r)
   {
     void* v = vd == MSORT_NONE || !vals ? nullptr : vals[r];
-    io[r] = RankIO{keys[r], v, keys[r], v, n[r], carve(ws[r], n[r], kd, vd, world)};
+    io[r] = RankIO{keys[r], v, keys[r], v, n[r], carve(ws[r], n[r], kd, vd, world), nullptr,
+                   nullptr};
+    const bool pull = exchange_mode() == 1 && world > 1;
+    io[r].sk = pull ? io[r].ws.rk : io[r].keys;
+    io[r].sv = pull ? io[r].ws.rv : io[r].vals;
   }
   EmulColl C{world, s};
-  return dist_run(C, io.data(), world, kd, vd, s, split_out);
+  return dist_run(C, io.data(), world, kd, vd, s, split_out, exchange_mode() == 1 && world > 1);
 }
+
+static int g_exchange_mode = -1;
+int exchange_mode() {
+  if (g_exchange_mode < 0) {
+    const char* e = getenv("MSORT_EXCHANGE");
+    g_exchange_mode = e && std::string(e) == "pull" ? 1 : 0;
+  }
+  return g_exchange_mode;
+}
+void set_exchange_mode(int m) { g_exchange_mode = m; }
 
 msort_status comm_unique_id(void* out) {
   ncclUniqueId id;
@@ -483,12 +653,13 @@ msort_status comm_init(const void* idp, int rank, int world, msort_comm_s** out)
   memcpy(&id, idp, sizeof(id));
   ncclComm_t c;
   MSORT_NCCL_TRY(ncclCommInitRank(&c, world, id, rank));
-  *out = new msort_comm_s{c, rank, world};
+  *out = new msort_comm_s{c, rank, world, {}};
   return MSORT_SUCCESS;
 }
 
 msort_status comm_destroy(msort_comm_s* c) {
   if (!c) return MSORT_SUCCESS;
+  for (auto& kv : c->ipc_open) cudaIpcCloseMemHandle(kv.second);
   ncclResult_t r = ncclCommDestroy(c->comm);
   delete c;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
@@ -498,3 +669,9 @@ msort_status comm_destroy(msort_comm_s* c) {
 int comm_world(msort_comm_s* c) { return c->world; }
 
 }  // namespace msort
+
+extern "C" int msort_debug_set_exchange(int mode) {
+  msort::set_exchange_mode(mode ? 1 : 0);
+  return 0;
+}
+

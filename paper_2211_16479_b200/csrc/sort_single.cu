@@ -346,6 +346,7 @@ struct Kernels {
   static_assert((2 * T) % Tm == 0, "pair boundaries must be tile boundaries");
   using Fused = FusedPasses<K>;
   using Explicit = SinglePass<K, ExplicitPairs>;
+  using Peer = SinglePass<K, PeerPairs>;
 
   // 4-way pass (keys only)
   static constexpr int NTQ = MSORT_QUAD_NT, VTQ = MSORT_QUAD_VT;
@@ -404,6 +405,7 @@ struct Kernels {
                                           (int)k1_smem));
     MSORT_TRY(set_smem<Fused>());
     MSORT_TRY(set_smem<Explicit>());
+    MSORT_TRY(set_smem<Peer>());
 #ifdef MSORT_K3_PERPASS
     MSORT_TRY((set_smem<SinglePass<K, UniformPairs>>()));
 #endif
@@ -592,6 +594,47 @@ struct Kernels {
     return launch_k3(f, (int64_t)left * ((f.ntiles + f.ch - 1) / f.ch), ctr, s, KC_MERGE);
   }
 
+  // First k-way round straight from the runs' owners (pull exchange): pair
+  // m = runs (2m, 2m+1), each possibly in another GPU's memory, merged into
+  // out at the sum of the earlier pairs' sizes (ties to the lower run).
+  // Writes the run boundaries of the result (ceil(runs/2) runs) to off_out.
+  static msort_status pull(const PullRuns& pr, K* out_k, uint32_t* out_v, int64_t* off_out,
+                           unsigned long long* ctr, cudaStream_t s) {
+    MSORT_TRY(init());
+    int dev = 0;
+    MSORT_CUDA_TRY(cudaGetDevice(&dev));
+    if (pr.runs > 2 * kMaxPairs) {
+      set_error("pull merge: too many runs");
+      return MSORT_ERROR_NOT_SUPPORTED;
+    }
+    Peer src{};
+    PeerPairs& pm = src.pm;
+    pm.npairs = (pr.runs + 1) / 2;
+    int64_t tiles = 0, out = 0;
+    for (int m = 0; m < pm.npairs; ++m) {
+      const int a = 2 * m, b = 2 * m + 1 < pr.runs ? 2 * m + 1 : -1;
+      pm.first_tile[m] = tiles;
+      pm.out[m] = out;
+      off_out[m] = out;
+      pm.na[m] = pr.n[a];
+      pm.nb[m] = b >= 0 ? pr.n[b] : 0;
+      pm.ka[m] = pr.k[a];
+      pm.kb[m] = b >= 0 ? pr.k[b] : pr.k[a];
+      pm.va[m] = PAIRS ? pr.v[a] : nullptr;
+      pm.vb[m] = PAIRS ? (b >= 0 ? pr.v[b] : pr.v[a]) : nullptr;
+      tiles += (pm.na[m] + pm.nb[m] + Tm - 1) / Tm;
+      out += pm.na[m] + pm.nb[m];
+    }
+    pm.first_tile[pm.npairs] = tiles;
+    off_out[pm.npairs] = out;
+    if (tiles == 0) return MSORT_SUCCESS;
+    src.dst_k = out_k, src.dst_v = out_v, src.ntiles = tiles;
+    src.ch = chunk_tiles(tiles, dev);
+    src.grab = src.ch < kChunk ? 1 : kGrab;
+    MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * sizeof(unsigned long long), s));
+    return launch_k3(src, (tiles + src.ch - 1) / src.ch, ctr, s, KC_KWAY);
+  }
+
   // Merge `runs` consecutive runs src[off[r], off[r+1]) into dst with rounds of
   // pairwise merges (ties to the lower run: merge() left-first at every
   // round keeps the lower run on the left).
@@ -646,10 +689,11 @@ struct Kernels {
       src.src_k = ck, src.src_v = cv, src.dst_k = nk, src.dst_v = nv, src.ntiles = tiles;
       // empty pairs own no tiles; locate() picks the last pair whose first
       // tile <= q, which is never an empty one
-      if (tiles > 0)
+      if (tiles > 0) {
         src.ch = chunk_tiles(tiles, dev);
         src.grab = src.ch < kChunk ? 1 : kGrab;
         MSORT_TRY(launch_k3(src, (tiles + src.ch - 1) / src.ch, ctr + round, s, KC_KWAY));
+      }
       int nr = pm.npairs;
       for (int m = 0; m <= nr; ++m) off[m] = off[std::min(2 * m, runs)];
       runs = nr;
@@ -707,6 +751,26 @@ msort_status kway_merge_dispatch(void* src_k, void* src_v, void* tmp_k, void* tm
       return kway_k<int64_t>(src_k, src_v, tmp_k, tmp_v, dst_k, dst_v, off_host, runs, ctr, s);
     case MSORT_UINT64:
       return kway_k<uint64_t>(src_k, src_v, tmp_k, tmp_v, dst_k, dst_v, off_host, runs, ctr, s);
+    default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
+  }
+}
+
+template <class K>
+static msort_status pull_k(const PullRuns& pr, void* ok, void* ov, int64_t* off,
+                           unsigned long long* ctr, cudaStream_t s) {
+  if (ov) return Kernels<K, true>::pull(pr, (K*)ok, (uint32_t*)ov, off, ctr, s);
+  return Kernels<K, false>::pull(pr, (K*)ok, nullptr, off, ctr, s);
+}
+
+msort_status pull_round_dispatch(const PullRuns& pr, void* out_k, void* out_v, int64_t* off_out,
+                                 msort_dtype kd, msort_dtype vd, void* part_ws, cudaStream_t s) {
+  auto* ctr = static_cast<unsigned long long*>(part_ws);
+  if (vd == MSORT_NONE) out_v = nullptr;
+  switch (kd) {
+    case MSORT_INT32: return pull_k<int32_t>(pr, out_k, out_v, off_out, ctr, s);
+    case MSORT_UINT32: return pull_k<uint32_t>(pr, out_k, out_v, off_out, ctr, s);
+    case MSORT_INT64: return pull_k<int64_t>(pr, out_k, out_v, off_out, ctr, s);
+    case MSORT_UINT64: return pull_k<uint64_t>(pr, out_k, out_v, off_out, ctr, s);
     default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
   }
 }

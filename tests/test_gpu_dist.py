@@ -18,11 +18,16 @@ import msort_inputs as mi
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def ms():
+@pytest.fixture(scope="module", params=[0, 1], ids=["alltoall", "pull"])
+def ms(request):
+    """Every test runs with both exchange modes (include/msort.h
+    msort_debug_set_exchange): NCCL-style all-to-all + k-way merge, and the
+    fused pull (the first merge round reads the peers' segments in place)."""
     import paper_2211_16479_b200 as m
 
-    return m
+    m.set_exchange_mode(request.param)
+    yield m
+    m.set_exchange_mode(0)
 
 
 def _dev(a):
