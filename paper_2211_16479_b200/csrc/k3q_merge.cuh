@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(NT + 64)
   using LY = QuadLayout<K, NT, VT>;
   constexpr uint32_t Z = sizeof(K), MASK = LY::MASK, RB = LY::RB, XMASK = LY::XMASK;
   constexpr int Tm = LY::Tm;
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(16) unsigned char smem[];
   const char* sb = reinterpret_cast<const char*>(smem);
   K* stk = reinterpret_cast<K*>(smem + LY::stage);
   QuadCtl& C = *reinterpret_cast<QuadCtl*>(smem + LY::misc);

@@ -454,16 +454,38 @@ __device__ __forceinline__ void bitonic_sort(K (&x)[N]) {
 
 // Keys-only network for any N: bitonic on the largest power of two P <= N,
 // then each remaining element is inserted by a compare-exchange chain.
+// Insertion of x[M] into the sorted x[0..M) by a compare-exchange chain,
+// then of x[M+1] ..., x[N-1]; template recursion keeps every index a
+// compile-time constant (registers, never local memory) at any size.
+template <int I, class K, int N>
+struct InsertChain {
+  static __device__ __forceinline__ void run(K (&x)[N]) {
+    cmp_swap(x[I], x[I + 1]);
+    InsertChain<I - 1, K, N>::run(x);
+  }
+};
+template <class K, int N>
+struct InsertChain<-1, K, N> {
+  static __device__ __forceinline__ void run(K (&)[N]) {}
+};
+template <int M, int N, class K>
+struct InsertAll {
+  static __device__ __forceinline__ void run(K (&x)[N]) {
+    InsertChain<M - 1, K, N>::run(x);
+    InsertAll<M + 1, N, K>::run(x);
+  }
+};
+template <int N, class K>
+struct InsertAll<N, N, K> {
+  static __device__ __forceinline__ void run(K (&)[N]) {}
+};
+
 template <int N, class K>
 __device__ __forceinline__ void keys_network(K (&x)[N]) {
-  constexpr int P = N >= 64 ? 64 : N >= 32 ? 32 : N >= 16 ? 16 : (N >= 8 ? 8 : (N >= 4 ? 4 : (N >= 2 ? 2 : 1)));
-  static_assert(N < 128, "keys_network: N < 128");
+  constexpr int P = N >= 128 ? 128 : N >= 64 ? 64 : N >= 32 ? 32 : N >= 16 ? 16 : (N >= 8 ? 8 : (N >= 4 ? 4 : (N >= 2 ? 2 : 1)));
+  static_assert(N < 256, "keys_network: N < 256");
   bitonic_sort<P>(x);
-#pragma unroll
-  for (int m = P; m < N; ++m) {
-#pragma unroll
-    for (int i = m - 1; i >= 0; --i) cmp_swap(x[i], x[i + 1]);
-  }
+  InsertAll<P, N, K>::run(x);
 }
 
 // Odd-even transposition sort: swaps only adjacent elements and only when

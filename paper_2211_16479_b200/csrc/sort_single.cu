@@ -266,10 +266,10 @@ extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
 #define MSORT_K3_NC 512  // merging threads per K3 CTA (4-byte keys only; 256 otherwise)
 #endif
 #ifndef MSORT_K1_NT
-#define MSORT_K1_NT 256  // keys-only K1 threads
+#define MSORT_K1_NT 128  // keys-only K1 threads (4-byte keys)
 #endif
 #ifndef MSORT_K1_VT
-#define MSORT_K1_VT 34  // keys-only K1 items per thread (NT x VT = 8704)
+#define MSORT_K1_VT 68  // keys-only K1 items per thread (NT x VT = 8704)
 #endif
 #ifndef MSORT_K3_VT
 #define MSORT_K3_VT 17  // outputs per merging thread (even: two chains per thread)
@@ -314,8 +314,10 @@ struct Kernels {
   // threads keep few items).  Keys only: fewer threads with more items each
   // -- a register network level is cheaper than a shared-memory merge round
   // (and each thread's co-rank search is amortised over more outputs).
-  static constexpr int VT = PAIRS ? 17 : MSORT_K1_VT;
-  static constexpr int NT1 = PAIRS ? 512 : MSORT_K1_NT;
+  // (4-byte keys: 128 x 68 -- 1.53 ms vs 1.74 for 256 x 34 and 1.99 for 64 x
+  // 136 on 2^28 int32; 8-byte keys keep 256 x 34: twice the registers per key)
+  static constexpr int VT = PAIRS ? 17 : (sizeof(K) == 4 ? MSORT_K1_VT : 34);
+  static constexpr int NT1 = PAIRS ? 512 : (sizeof(K) == 4 ? MSORT_K1_NT : 256);
   static constexpr int T = NT1 * VT;  // tile sort size
   // 4-byte keys: 512 mergers x 17 = one 8704-key output tile (= T) per stage,
   // 2 CTAs/SM -- half the tiles (and co-rank searches) of 256 x 17, measured
