@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU (default 2^28)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-streams", type=int, default=3, help="streams the e2e steps rotate over")
     return ap.parse_args()
 
 
@@ -324,7 +325,7 @@ def main():
         h_in = kin.cpu().pin_memory()
         ke = max(6, min(args.steps, 12))
         if world == 1:
-            NS = 3
+            NS = max(1, args.e2e_streams)
             h_out = [torch.empty_like(h_in).pin_memory() for _ in range(NS)]
             d_buf = [torch.empty_like(kin) for _ in range(NS)]
             wss = [ws] + [ms.workspace(n, torch.int32, False, device=dev) for _ in range(NS - 1)]
