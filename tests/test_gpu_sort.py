@@ -230,3 +230,19 @@ def test_sort_host_entry_point(ms, orc, pinned):
     ms.msort_sort_host(hk2.view(torch.uint32), hk2.view(torch.uint32), dk2)
     torch.cuda.synchronize()
     assert np.array_equal(hk2.numpy().view(np.uint32), orc.sort(mi.keys(n, 13, "u32")))
+
+
+def test_random_sizes_stress(ms, orc):
+    """60 random (size, dtype, distribution, payload) combinations, sizes up to
+    2^21 + ragged tails: every one bit-exact to the oracle."""
+    rng = np.random.default_rng(2211)
+    dts = [np.int32, np.uint32, np.int64, np.uint64]
+    dists = ["rand", "dup", "eq", "asc", "desc", "ext"]
+    for t in range(60):
+        n = int(rng.integers(0, 1 << int(rng.integers(1, 22))))
+        dtype = dts[int(rng.integers(0, 4))]
+        dist = dists[int(rng.integers(0, len(dists)))]
+        pairs = bool(rng.integers(0, 2))
+        k = _keys(n, 5000 + t, dist, dtype)
+        v = mi.index_payload(n) if pairs else None
+        check_parity(ms, orc, k, v)
