@@ -133,9 +133,9 @@ __global__ void __launch_bounds__(NT)
 // log2(NT) merge-path rounds in shared memory double the runs.  In round r
 // (runs of w = VT << r) pair m = (run 2m = A, run 2m+1 = B) is laid out as
 //     [ B (w) | MAX | A (w) | MAX ]
-// (each sentinel slot is two keys wide, so every run starts at an even
-// element offset and the VT keys of a thread leave as 2-key vector stores,
-// conflict-free for even VT) so that a run that is used up reads as its MAX
+// (each sentinel slot is one 16-byte vector wide, so every run starts
+// 16-byte aligned and the VT keys of a thread leave as 16-byte vector stores,
+// see store_vec) so that a run that is used up reads as its MAX
 // sentinel: the serial merge
 // needs no end checks (merge_keys_sentinel) and no thread diverges.  (With
 // equal keys indistinguishable, taking A's sentinel on a tie with a real MAX
@@ -161,18 +161,29 @@ __device__ __forceinline__ void merge_keys_sentinel(const char* s, uint32_t oa, 
   }
 }
 
+// VT keys of a thread stored as 16-byte vectors (4 x 32-bit or 2 x 64-bit
+// keys; VT a multiple of the width, dst 16-byte aligned).  A thread's run
+// starts every VT keys, i.e. 4*VT bytes apart for int32: with VT = 68 that is
+// 17 vector slots, odd, so the 8 lanes of each quarter-warp phase hit 8
+// different slot groups -- conflict-free (2-key vectors would be 2-way).
 template <class K>
-struct __align__(2 * sizeof(K)) K2 {
-  K x, y;
+struct VecOf {
+  static constexpr int W = 16 / sizeof(K);
 };
-// VT (even) keys to dst (2-key aligned) as VT/2 vector stores.
+template <class K, int W>
+struct __align__(16) KVec {
+  K x[W];
+};
 template <class K, int VT>
-__device__ __forceinline__ void store_pairs(K* dst, const K (&key)[VT]) {
+__device__ __forceinline__ void store_vec(K* dst, const K (&key)[VT]) {
+  constexpr int W = VecOf<K>::W;
+  static_assert(VT % W == 0, "VT: multiple of the 16-byte vector width");
 #pragma unroll
-  for (int k = 0; k < VT; k += 2) {
-    K2<K> v;
-    v.x = key[k], v.y = key[k + 1];
-    *reinterpret_cast<K2<K>*>(dst + k) = v;
+  for (int k = 0; k < VT; k += W) {
+    KVec<K, W> v;
+#pragma unroll
+    for (int j = 0; j < W; ++j) v.x[j] = key[k + j];
+    *reinterpret_cast<KVec<K, W>*>(dst + k) = v;
   }
 }
 
@@ -180,10 +191,11 @@ template <class K, int NT, int VT>
 struct K1KeysShape {
   static constexpr int T = NT * VT;
   static constexpr int NW = NT / 32;
-  static constexpr int WREG = 32 * VT + 64;  // per-warp region (in-warp rounds)
+  static constexpr int PADK = VecOf<K>::W;            // sentinel slot (one vector)
+  static constexpr int WREG = 32 * VT + 32 * PADK;   // per-warp region (in-warp rounds)
   static constexpr int ROUNDS = __builtin_ctz(NT);
   static constexpr size_t smem =
-      (size_t)(NW * WREG > T + 2 * NT ? NW * WREG : T + 2 * NT) * sizeof(K);
+      (size_t)(NW * WREG > T + PADK * NT ? NW * WREG : T + PADK * NT) * sizeof(K);
   static_assert((NT & (NT - 1)) == 0 && NT >= 32, "NT: power of two >= 32");
 };
 
@@ -191,7 +203,7 @@ template <class K, int NT, int VT>
 __global__ void __launch_bounds__(NT)
     k1_tile_sort_keys(const K* __restrict__ in_k, K* __restrict__ out_k, int64_t n) {
   using SH = K1KeysShape<K, NT, VT>;
-  static_assert(VT % 2 == 0, "keys-only K1 stores key pairs: VT even");
+  static_assert(VT % VecOf<K>::W == 0, "keys-only K1 stores 16-byte vectors");
   constexpr int T = SH::T;
   constexpr uint32_t Z = sizeof(K);
   extern __shared__ __align__(16) unsigned char smem[];
@@ -226,27 +238,29 @@ __global__ void __launch_bounds__(NT)
       const int rho = tid >> r;
       const int pos = (tid & ((1 << r) - 1)) * VT;
       const int m = (rho >> 1) - mbase;
-      const int at = org + m * (2 * w + 4) + ((rho & 1) ? 0 : w + 2) + pos;
-      store_pairs<K, VT>(sk + at, key);
+      constexpr int PW = SH::PADK;
+      const int at = org + m * (2 * w + 2 * PW) + ((rho & 1) ? 0 : w + PW) + pos;
+      store_vec<K, VT>(sk + at, key);
       if (pos + VT == w) {
-        K2<K> mx;
-        mx.x = mx.y = KeyTraits<K>::max_key();
-        *reinterpret_cast<K2<K>*>(sk + at + VT) = mx;
+        KVec<K, PW> mx;
+#pragma unroll
+        for (int j = 0; j < PW; ++j) mx.x[j] = KeyTraits<K>::max_key();
+        *reinterpret_cast<KVec<K, PW>*>(sk + at + VT) = mx;
       }
     }
     if (in_warp) __syncwarp();
     else __syncthreads();
     const int m = (tid >> (r + 1)) - mbase;
     const int d = (tid & ((2 << r) - 1)) * VT;
-    const uint32_t ob0 = (uint32_t)(org + m * (2 * w + 4)) * Z;
-    const uint32_t oa0 = ob0 + (uint32_t)(w + 2) * Z;
+    const uint32_t ob0 = (uint32_t)(org + m * (2 * w + 2 * SH::PADK)) * Z;
+    const uint32_t oa0 = ob0 + (uint32_t)(w + SH::PADK) * Z;
     const int i = merge_path_off<K>(sb, oa0, w, ob0, w, d);
     merge_keys_sentinel<K, VT>(sb, oa0 + (uint32_t)i * Z, oa0 + (uint32_t)w * Z,
                                ob0 + (uint32_t)(d - i) * Z, key);
   }
 
   __syncthreads();
-  store_pairs<K, VT>(sk + tid * VT, key);
+  store_vec<K, VT>(sk + tid * VT, key);
   __syncthreads();
 #pragma unroll 4
   for (int i = tid; i < cnt; i += NT) out_k[base + i] = sk[i];
