@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-streams", type=int, default=3, help="streams the e2e steps rotate over")
+    ap.add_argument("--exchange", choices=["alltoall", "pull"], default="alltoall",
+                    help="N > 1: NCCL all-to-all + k-way merge, or the fused pull exchange")
     return ap.parse_args()
 
 
@@ -218,6 +220,7 @@ def main():
 
         dist.init_process_group("nccl", device_id=dev)
         comm = ms.Comm()
+        ms.set_exchange_mode(1 if args.exchange == "pull" else 0)
 
     n = args.n
     kin = mi.keys_torch(n, SEED0 + rank, "u31", device=dev)
@@ -401,7 +404,8 @@ def main():
                        "tile": tile, "merge_passes": passes,
                        "l2": "inputs larger than L2 (1 GiB/GPU vs 126 MB); no flush; "
                              "out-of-place sort from the pristine input each step",
-                       "parallelism": f"dp{world}" if world > 1 else "single"},
+                       "parallelism": f"dp{world}" if world > 1 else "single",
+                       "exchange": args.exchange if world > 1 else None},
             "roofline": roof,
             "step_roofline": {"bytes_per_gpu": step_bytes, "t_roof_ms": t_roof * 1e3,
                               "frac": round(t_roof * 1e3 / ms_step, 4),
