@@ -187,8 +187,11 @@ def reference_arm(args, rank):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * t / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": "C5 sample: 2^22 int32 keys uniform [0,2^31), seed 4",
-                   "n_per_step": n_s},
+        "config": {"workload": "C5: 2^28 int32 keys per GPU, uniform [0,2^31), "
+                               "counter-mode SplitMix64 seed 4+rank",
+                   "n_per_gpu": N_PER_GPU, "key_dtype": "int32", "payload": None,
+                   "sample_per_step": f"first 2^22 keys of the rank-0 shard ({n_s} keys)",
+                   "parallelism": "single (host, 1 thread)"},
         "cpu_baseline": {"value": v, "unit": "keys/s", "cores": 1, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
