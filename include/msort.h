@@ -248,7 +248,9 @@ int msort_tile_size(msort_dtype key_dtype, msort_dtype val_dtype);
  * HBM passes.  mode 0 (default): one 2-way level per pass (the fused K3
  * dataflow only); 1: two levels per pass (4-way merge tree, K3Q) while every
  * CTA gets >= 2 segments, the remaining levels 2-way; 2: 4-way passes whenever
- * >= 2 levels remain (small inputs too -- for tests).  The result is the same
+ * >= 2 levels remain (small inputs too -- for tests); 4: every pair of levels
+ * as a K3X pass (4-way super-tiles between X-/Y-side boundary states found
+ * just in time by a searcher warp, no nested searches).  The result is the same
  * in every mode (the stable sort is unique); process-wide, not thread-safe
  * against concurrent sorts.  Overrides the MSORT_QUAD environment variable.
  * Returns 0. */

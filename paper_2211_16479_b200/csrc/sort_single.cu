@@ -22,6 +22,7 @@
 
 #include "k3_merge.cuh"
 #include "k3q_merge.cuh"
+#include "k3x_merge.cuh"
 #include "msort_device.cuh"
 #include "msort_internal.h"
 
@@ -269,6 +270,16 @@ __global__ void __launch_bounds__(NT)
 // ----------------------------------------------------------------- K3
 // k3_merge.cuh: the persistent merge pass with fused co-rank search (K2).
 
+#ifdef MSORT_K3X_TRACE
+extern "C" int msort_debug_k3x_trace(unsigned long long* host, int n, int reset) {
+  int r = (int)cudaMemcpyFromSymbol(host, g_k3x_trace, sizeof(unsigned long long) * n);
+  if (reset) {
+    static unsigned long long z[1024 * 8];
+    cudaMemcpyToSymbol(g_k3x_trace, z, sizeof(z));
+  }
+  return r;
+}
+#endif
 #ifdef MSORT_K3_TRACE
 extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, g_k3_trace, sizeof(unsigned long long) * n);
@@ -297,6 +308,12 @@ extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
 #endif
 #ifndef MSORT_QUAD_SEG
 #define MSORT_QUAD_SEG 65536  // target keys per 4-way segment
+#endif
+#ifndef MSORT_X_NC
+#define MSORT_X_NC 384  // K3X mergers (super-tile capacity NC x 17)
+#endif
+#ifndef MSORT_X_S
+#define MSORT_X_S 2  // K3X stages
 #endif
 #ifndef MSORT_QUAD_NT
 #define MSORT_QUAD_NT 128
@@ -368,6 +385,14 @@ struct Kernels {
   static constexpr int NTQ = MSORT_QUAD_NT, VTQ = MSORT_QUAD_VT;
   using LQ = QuadLayout<K, NTQ, VTQ>;
   static int& gridq(int dev) {
+    static int g[64] = {};
+    return g[dev & 63];
+  }
+
+  // K3X (quad mode 4): two levels per pass, boundaries found just in time
+  static constexpr int NCX = MSORT_X_NC, SX = MSORT_X_S;
+  using LX = K3XLayout<K, NCX, 17, SX>;
+  static int& gridx(int dev) {
     static int g[64] = {};
     return g[dev & 63];
   }
@@ -444,6 +469,12 @@ struct Kernels {
       MSORT_CUDA_TRY(
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oq, kq, NTQ + 64, LQ::bytes));
       gridq(dev) = sms * std::max(oq, 1);
+      auto kx = k3x_pass<K, NCX, 17, SX>;
+      MSORT_CUDA_TRY(
+          cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LX::bytes));
+      int ox = 0;
+      MSORT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, kx, NCX + 96, LX::bytes));
+      gridx(dev) = sms * std::max(ox, 1);
     }
     return MSORT_SUCCESS;
   }
@@ -495,7 +526,8 @@ struct Kernels {
     int64_t Lq = T;
     if constexpr (!PAIRS) {
       const int mode = quad_mode();
-      while (mode && passes - 2 * nq >= 2) {
+      if (mode == 4) nq = passes / 2, Lq = (int64_t)T << (2 * nq);  // K3X: every pair of levels
+      while (mode && mode != 4 && passes - 2 * nq >= 2) {
         int64_t ng, nseg;
         int sf, sl;
         quad_geometry((int64_t)n, Lq, ng, sf, sl, nseg);
@@ -549,7 +581,28 @@ struct Kernels {
       if (nq > 0)
         MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * sizeof(unsigned long long), s));
       int64_t L = T;
-      for (int q = 0; q < nq; ++q, L *= 4) {
+      if (quad_mode() == 4) {
+        for (int q = 0; q < nq; ++q, L *= 4) {
+          const int64_t ng = ((int64_t)n + 4 * L - 1) / (4 * L);
+          const int64_t upg = (2 * L + LX::XS - 1) / LX::XS + 1;
+          {
+            LaunchScope ls(KC_MERGE, s);
+            k3x_pass<K, NCX, 17, SX>
+                <<<(unsigned)std::min<int64_t>(gridx(dev), (ng * upg + 3) / 4), NCX + 96, LX::bytes,
+                   s>>>(bk[cur], bk[cur ^ 1], (int64_t)n, L, ng, upg, ctr + 32 + q);
+          }
+          MSORT_CUDA_TRY(cudaGetLastError());
+#ifdef MSORT_K3_CHECK
+          {
+            cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) return cuda_fail(e, "k3x (debug sync)");
+          }
+#endif
+          cur ^= 1;
+        }
+        if (left == 0) return MSORT_SUCCESS;
+      }
+      for (int q = 0; q < nq && quad_mode() != 4; ++q, L *= 4) {
         int64_t ng, nseg;
         int sf, sl;
         quad_geometry((int64_t)n, L, ng, sf, sl, nseg);

@@ -19,12 +19,16 @@ pytestmark = pytest.mark.gpu
 DTYPES = [np.int32, np.uint32, np.int64, np.uint64]
 
 
-@pytest.fixture(scope="module")
-def ms():
+@pytest.fixture(scope="module", params=[2, 4], ids=["k3q", "k3x"])
+def ms(request):
+    """Mode 2: K3Q (4-way merge tree, sampled segment splitters) whenever two
+    levels remain; mode 4: K3X (4-way super-tiles between X-/Y-side boundary
+    states found just in time) for every pair of levels."""
     import paper_2211_16479_b200 as m
 
     assert torch.cuda.is_available()
-    m.set_quad_mode(2)
+    m.set_quad_mode(request.param)
+    m.QUAD_TEST_MODE = request.param
     yield m
     m.set_quad_mode(0)
 
@@ -74,14 +78,14 @@ def test_quad_modes_agree(ms):
     n = 1 << 22
     src = mi.keys_torch(n, 5, "u31", device="cuda")
     outs = []
-    for mode in (0, 1, 2):
+    for mode in (0, 1, 2, 4):
         ms.set_quad_mode(mode)
         t = src.clone()
         ms.msort_sort(t)
         outs.append(t)
-    ms.set_quad_mode(2)
+    ms.set_quad_mode(ms.QUAD_TEST_MODE)
     torch.cuda.synchronize()
-    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
     assert bool((outs[0][1:] >= outs[0][:-1]).all())
 
 
