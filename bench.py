@@ -198,6 +198,34 @@ def reference_arm(args, rank):
     }), flush=True)
 
 
+def pcie_duplex_ms(h_in, h_out, d_a, d_b, strs, reps=4):
+    """Device-timed ms per step of copying h_in -> d_a and d_b -> h_out
+    concurrently on two streams (pinned host memory): the floor of an e2e step
+    that uploads its input and downloads its result."""
+    import torch
+
+    s1, s2 = strs[0], strs[1 % len(strs)]
+
+    def step():
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_b, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e0.record(s1)
+    s2.wait_event(e0)
+    for _ in range(reps):
+        step()
+    f1, f2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f1.record(s1)
+    f2.record(s2)
+    torch.cuda.synchronize()
+    return max(e0.elapsed_time(f1), e0.elapsed_time(f2)) / reps
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -387,6 +415,12 @@ def main():
         e2e = {"value": world * n * ke / (te / 1e3), "unit": "keys/s",
                "h2d_bytes_per_step": n * wk, "d2h_bytes_per_step": n * wk,
                "ms_per_step": te / ke, "steps": ke, "path": path}
+        if world == 1:
+            # the PCIe ceiling of this e2e step: the same upload and download
+            # alone, both directions at once on two streams (no sort)
+            fl = pcie_duplex_ms(h_in, h_out[0], d_buf[0], kin, strs)
+            e2e["pcie_duplex_ms"] = fl
+            e2e["frac_of_pcie"] = round(fl / (te / ke), 4)
 
     cpu = cpu_mp = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

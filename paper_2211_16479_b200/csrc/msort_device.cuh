@@ -16,18 +16,21 @@ template <>
 struct KeyTraits<int32_t> {
   using U = uint32_t;
   static __host__ __device__ __forceinline__ int32_t max_key() { return 0x7fffffff; }
+  static __host__ __device__ __forceinline__ int32_t min_key() { return (int32_t)0x80000000; }
   static __host__ __device__ __forceinline__ U image(int32_t x) { return (U)x ^ 0x80000000u; }
 };
 template <>
 struct KeyTraits<uint32_t> {
   using U = uint32_t;
   static __host__ __device__ __forceinline__ uint32_t max_key() { return 0xffffffffu; }
+  static __host__ __device__ __forceinline__ uint32_t min_key() { return 0u; }
   static __host__ __device__ __forceinline__ U image(uint32_t x) { return x; }
 };
 template <>
 struct KeyTraits<int64_t> {
   using U = uint64_t;
   static __host__ __device__ __forceinline__ int64_t max_key() { return 0x7fffffffffffffffll; }
+  static __host__ __device__ __forceinline__ int64_t min_key() { return (int64_t)0x8000000000000000ull; }
   static __host__ __device__ __forceinline__ U image(int64_t x) {
     return (U)x ^ 0x8000000000000000ull;
   }
@@ -36,6 +39,7 @@ template <>
 struct KeyTraits<uint64_t> {
   using U = uint64_t;
   static __host__ __device__ __forceinline__ uint64_t max_key() { return ~0ull; }
+  static __host__ __device__ __forceinline__ uint64_t min_key() { return 0ull; }
   static __host__ __device__ __forceinline__ U image(uint64_t x) { return x; }
 };
 

@@ -24,6 +24,7 @@
 #include "k3q_merge.cuh"
 #include "k3x_merge.cuh"
 #include "msort_device.cuh"
+#include "networks.cuh"
 #include "msort_internal.h"
 
 namespace msort {
@@ -130,34 +131,56 @@ __global__ void __launch_bounds__(NT)
   }
 }
 
-// Keys-only K1.  Each thread sorts VT keys in registers (keys_network), then
-// log2(NT) merge-path rounds in shared memory double the runs.  In round r
-// (runs of w = VT << r) pair m = (run 2m = A, run 2m+1 = B) is laid out as
-//     [ B (w) | MAX | A (w) | MAX ]
-// (each sentinel slot is one 16-byte vector wide, so every run starts
-// 16-byte aligned and the VT keys of a thread leave as 16-byte vector stores,
-// see store_vec) so that a run that is used up reads as its MAX
-// sentinel: the serial merge
-// needs no end checks (merge_keys_sentinel) and no thread diverges.  (With
-// equal keys indistinguishable, taking A's sentinel on a tie with a real MAX
-// in B outputs the right value; the A cursor is clamped at its sentinel.)
-// Rounds whose merge groups fit in a warp use a per-warp region with 64
-// elements of slack (room for its sentinels) and only warp synchronisation.
+// Keys-only K1.  Each thread sorts VT keys in registers (k1_network: Batcher's
+// merge-exchange network, networks.cuh), then log2(NT) merge-path rounds in
+// shared memory double the runs.  In round r (runs of w = VT << r) pair
+// m = (run 2m = A, run 2m+1 = B) is laid out as
+//     [ B (w) | pad | A (w) | pad ]        (K1Layout, in 16-byte vectors)
+// with a MAX key right after each run and a MIN key right before it, so a run
+// that is used up reads as its sentinel and the merges (merge_keys_dual) need
+// no end checks: no thread diverges.  (With equal keys indistinguishable, a
+// sentinel that ties with a real MIN / MAX key outputs the right value; the
+// cursor that could step over its sentinel on such a tie is clamped.)  Every
+// run starts 16-byte aligned, so a thread's VT keys leave as 16-byte vector
+// stores (store_vec), and the paddings keep those stores free of bank
+// conflicts.  Rounds whose merge groups fit in a warp use a per-warp region
+// and only warp synchronisation.
+//
+// The same VT outputs as two independent chains of VT/2 (twice the loads in
+// flight per thread): the front chain from the co-rank at the thread's first
+// diagonal (oa, ob) upwards, ties to A, A clamped at its MAX sentinel ea; the
+// back chain from the co-rank at its last diagonal (oa1, ob1 = one past the
+// last elements) downwards, taking the LAST of equal keys (B's), B clamped at
+// its MIN sentinel bmin (each run has a MIN key in front of it, K1Layout).
 template <class K, int VT>
-__device__ __forceinline__ void merge_keys_sentinel(const char* s, uint32_t oa, uint32_t ea,
-                                                    uint32_t ob, K (&key)[VT]) {
+__device__ __forceinline__ void merge_keys_dual(const char* s, uint32_t oa, uint32_t ea,
+                                                uint32_t ob, uint32_t oa1, uint32_t ob1,
+                                                uint32_t bmin, K (&key)[VT]) {
+  static_assert(VT % 2 == 0, "two chains of VT/2");
+  constexpr int H = VT / 2;
+  constexpr uint32_t Z = sizeof(K);
+  uint32_t pa = oa1 - Z, pb = ob1 - Z;
   K ak = ld_off<K>(s, oa), bk = ld_off<K>(s, ob);
+  K ax = ld_off<K>(s, pa), bx = ld_off<K>(s, pb);
 #pragma unroll
-  for (int k = 0; k < VT; ++k) {
+  for (int k = 0; k < H; ++k) {
     const bool p = bk < ak;
     key[k] = p ? bk : ak;
-    if (k + 1 < VT) {
-      const uint32_t nx = min((p ? ob : oa) + (uint32_t)sizeof(K), ea);  // B lies below ea
+    const bool q = ax > bx;
+    key[VT - 1 - k] = q ? ax : bx;
+    if (k + 1 < H) {
+      const uint32_t nx = min((p ? ob : oa) + Z, ea);  // B lies below ea
       oa = p ? oa : nx;
       ob = p ? nx : ob;
+      const uint32_t ny = max((q ? pa : pb) - Z, bmin);  // A lies above bmin
+      pa = q ? ny : pa;
+      pb = q ? pb : ny;
       const K nv = ld_off<K>(s, nx);
+      const K nw = ld_off<K>(s, ny);
       ak = p ? ak : nv;
       bk = p ? nv : bk;
+      ax = q ? nw : ax;
+      bx = q ? bx : nw;
     }
   }
 }
@@ -188,15 +211,72 @@ __device__ __forceinline__ void store_vec(K* dst, const K (&key)[VT]) {
   }
 }
 
+
+// Compare-exchange of the keys-only register network (min and max; any
+// network is fine for keys only -- equal integers are indistinguishable).
+struct CmpSwapKeys {
+  template <class K>
+  __device__ __forceinline__ void operator()(K& a, K& b, int) const {
+    const K lo = a < b ? a : b, hi = a < b ? b : a;
+    a = lo;
+    b = hi;
+  }
+};
+
+template <int VT, class K>
+__device__ __forceinline__ void k1_network(K (&key)[VT]) {
+  if constexpr (MergeExchange<VT>::kHave)
+    MergeExchange<VT>::run(key, CmpSwapKeys{});
+  else
+    keys_network<VT>(key);
+}
+
+// Round-r pair layout of the keys-only K1 in 16-byte vectors (V = vectors per
+// thread).  Pair m of a region starts at start(r, m) with its B run, A follows
+// at start + aoff(r); each run is followed by >= 1 vector of MAX sentinels.
+// The paddings are chosen so that the 8 lanes of every quarter-warp store
+// their V-vector runs into 8 different bank groups when V = 1 mod 8 (V = 17:
+// 68 int32 / 34 int64 keys per thread): the thread runs start V apart, so
+// only the run / pair boundaries can collide -- round 0 staggers the pairs
+// (stride 2V+2, +1 every second pair), round 1 alternates strides 4V+6 and
+// 4V+4 with A at 2V+2, round 2 puts A at 4V+8 (a bank group half a turn from B); from round
+// 3 on a quarter-warp lies inside one run.
+struct K1Layout {
+  template <int V>
+  static constexpr __host__ __device__ int start(int r, int m) {
+    return r == 0 ? (2 * V + 2) * m + (m >> 1)
+         : r == 1 ? (4 * V + 5) * m + (m & 1)
+         : r == 2 ? (8 * V + 9) * m
+                  : ((2 * V << r) + 2) * m;
+  }
+  template <int V>
+  static constexpr __host__ __device__ int aoff(int r) {
+    return r == 0 ? V + 1 : r == 1 ? 2 * V + 2 : r == 2 ? 4 * V + 8 : (V << r) + 1;
+  }
+};
+
 template <class K, int NT, int VT>
 struct K1KeysShape {
   static constexpr int T = NT * VT;
   static constexpr int NW = NT / 32;
-  static constexpr int PADK = VecOf<K>::W;            // sentinel slot (one vector)
-  static constexpr int WREG = 32 * VT + 32 * PADK;   // per-warp region (in-warp rounds)
+  static constexpr int W = VecOf<K>::W;      // keys per vector (= sentinel slot)
+  static constexpr int V = VT / W;           // vectors per thread
   static constexpr int ROUNDS = __builtin_ctz(NT);
+  static constexpr int cmax(int a, int b) { return a > b ? a : b; }
+  // per-warp region (in-warp rounds: 16 >> r pairs) and the whole-block
+  // region (block rounds: NT >> (r+1) pairs), in vectors
+  static constexpr int wreg(int r) {
+    return r > 4 ? 0 : cmax(K1Layout::start<V>(r, 16 >> r), wreg(r + 1));
+  }
+  static constexpr int breg(int r) {
+    return r >= ROUNDS ? 0 : cmax(r > 4 ? K1Layout::start<V>(r, NT >> (r + 1)) : 0, breg(r + 1));
+  }
+  static constexpr int WREGV = wreg(0);
+  // block rounds' co-rank exchange (NT ints) after the block region, in ints
+  // from the start of shared memory (guard vector included)
+  static constexpr int CRANK = (1 + breg(0)) * 4;
   static constexpr size_t smem =
-      (size_t)(NW * WREG > T + PADK * NT ? NW * WREG : T + PADK * NT) * sizeof(K);
+      (size_t)cmax(cmax(NW * WREGV, breg(0) + NT / 4), T / W) * 16 + 16;
   static_assert((NT & (NT - 1)) == 0 && NT >= 32, "NT: power of two >= 32");
 };
 
@@ -208,8 +288,9 @@ __global__ void __launch_bounds__(NT)
   constexpr int T = SH::T;
   constexpr uint32_t Z = sizeof(K);
   extern __shared__ __align__(16) unsigned char smem[];
-  K* sk = reinterpret_cast<K*>(smem);
-  const char* sb = reinterpret_cast<const char*>(smem);
+  // one guard vector in front: the MIN sentinel of the first run
+  K* sk = reinterpret_cast<K*>(smem + 16);
+  const char* sb = reinterpret_cast<const char*>(smem);  // byte offsets include the guard
   const int tid = threadIdx.x, warp = tid >> 5;
   const int64_t base = (int64_t)blockIdx.x * T;
   const int cnt = (int)min((int64_t)T, n - base);
@@ -223,14 +304,14 @@ __global__ void __launch_bounds__(NT)
     const int i = k * NT + tid;
     key[k] = i < cnt ? in_k[base + i] : KeyTraits<K>::max_key();
   }
-  keys_network<VT>(key);
+  k1_network<VT>(key);
 
 #pragma unroll 1
   for (int r = 0; r < SH::ROUNDS; ++r) {
     const int w = VT << r;
     const bool in_warp = (2 << r) <= 32;
-    // region origin of this round's pairs (elements)
-    const int org = in_warp ? warp * SH::WREG : 0;
+    // region origin of this round's pairs (vectors)
+    const int org = in_warp ? warp * SH::WREGV : 0;
     const int mbase = in_warp ? (warp * 32) >> (r + 1) : 0;  // first pair of the region
     if (in_warp) __syncwarp();
     else __syncthreads();
@@ -239,25 +320,33 @@ __global__ void __launch_bounds__(NT)
       const int rho = tid >> r;
       const int pos = (tid & ((1 << r) - 1)) * VT;
       const int m = (rho >> 1) - mbase;
-      constexpr int PW = SH::PADK;
-      const int at = org + m * (2 * w + 2 * PW) + ((rho & 1) ? 0 : w + PW) + pos;
+      constexpr int W = SH::W;
+      const int run = org + K1Layout::start<SH::V>(r, m) + ((rho & 1) ? 0 : K1Layout::aoff<SH::V>(r));
+      const int at = run * W + pos;
       store_vec<K, VT>(sk + at, key);
-      if (pos + VT == w) {
-        KVec<K, PW> mx;
-#pragma unroll
-        for (int j = 0; j < PW; ++j) mx.x[j] = KeyTraits<K>::max_key();
-        *reinterpret_cast<KVec<K, PW>*>(sk + at + VT) = mx;
-      }
+      if (pos + VT == w) sk[at + VT] = KeyTraits<K>::max_key();  // sentinels
+      if (pos == 0) sk[at - 1] = KeyTraits<K>::min_key();
     }
     if (in_warp) __syncwarp();
     else __syncthreads();
     const int m = (tid >> (r + 1)) - mbase;
     const int d = (tid & ((2 << r) - 1)) * VT;
-    const uint32_t ob0 = (uint32_t)(org + m * (2 * w + 2 * SH::PADK)) * Z;
-    const uint32_t oa0 = ob0 + (uint32_t)(w + SH::PADK) * Z;
+    const uint32_t ob0 = (uint32_t)(1 + org + K1Layout::start<SH::V>(r, m)) * 16u;
+    const uint32_t oa0 = ob0 + (uint32_t)K1Layout::aoff<SH::V>(r) * 16u;
     const int i = merge_path_off<K>(sb, oa0, w, ob0, w, d);
-    merge_keys_sentinel<K, VT>(sb, oa0 + (uint32_t)i * Z, oa0 + (uint32_t)w * Z,
-                               ob0 + (uint32_t)(d - i) * Z, key);
+    // co-rank at my last diagonal d + VT: the next thread's (shuffle inside
+    // a warp, shared memory across warps), or w at the end of the pair
+    int i1 = __shfl_down_sync(0xffffffffu, i, 1);
+    if (!in_warp) {
+      int* cr = reinterpret_cast<int*>(smem) + SH::CRANK;
+      cr[tid] = i;
+      __syncthreads();
+      if ((tid & 31) == 31 && tid + 1 < NT) i1 = cr[tid + 1];
+    }
+    if (d + VT == 2 * w) i1 = w;
+    merge_keys_dual<K, VT>(sb, oa0 + (uint32_t)i * Z, oa0 + (uint32_t)w * Z,
+                           ob0 + (uint32_t)(d - i) * Z, oa0 + (uint32_t)i1 * Z,
+                           ob0 + (uint32_t)(d + VT - i1) * Z, ob0 - Z, key);
   }
 
   __syncthreads();
