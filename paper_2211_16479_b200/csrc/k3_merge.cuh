@@ -340,12 +340,13 @@ __device__ __forceinline__ int64_t corank_warp(const Src& src, int pass, int64_t
   const K* b = src.pb(pass, q, A0, na);
   int64_t lo = dl - nb > 0 ? dl - nb : 0;
   int64_t hi = dl < na ? dl : na;
+  const uint64_t pol = probe_policy();
   while (hi > lo) {
     const int64_t span = hi - lo;
     const int64_t step = (span + 31) >> 5;
     const int64_t off = step * (lane + 1);
     const int64_t p = lo + (off < span ? off : span) - 1;
-    const bool pred = a[p] > b[dl - 1 - p];
+    const bool pred = probe_ld(a + p, pol) > probe_ld(b + (dl - 1 - p), pol);
     const unsigned m = __ballot_sync(0xffffffffu, pred);
     if (m == 0) {
       lo = hi;

@@ -73,6 +73,42 @@ __device__ __forceinline__ int merge_path(const K* s, int a0, int na, int b0, in
   return lo;
 }
 
+// Loads of the co-rank searches in global memory (probes).  The fused merge
+// pass searches a few chunks ahead of its loads, so a probe's sector would be
+// evicted from L2 before the window holding it is staged and then read twice
+// from DRAM; with MSORT_PROBE_EVICT_LAST the probes carry an L2 evict_last
+// policy.  Plain coherent loads (not .nc): in the fused pass the data was
+// written by other CTAs of the same launch (ordered by the acquire that
+// precedes the search).
+#ifndef MSORT_PROBE_EVICT_LAST
+#define MSORT_PROBE_EVICT_LAST 1
+#endif
+__device__ __forceinline__ uint64_t probe_policy() {
+  uint64_t pol = 0;
+#if MSORT_PROBE_EVICT_LAST
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
+template <class K>
+__device__ __forceinline__ K probe_ld(const K* p, uint64_t pol) {
+  static_assert(sizeof(K) == 4 || sizeof(K) == 8, "4- or 8-byte keys");
+#if MSORT_PROBE_EVICT_LAST
+  if constexpr (sizeof(K) == 4) {
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return (K)v;
+  } else {
+    uint64_t v;
+    asm volatile("ld.global.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return (K)v;
+  }
+#else
+  (void)pol;
+  return *reinterpret_cast<const volatile K*>(p);
+#endif
+}
+
 // Same search over global memory with 64-bit indices.
 template <class K>
 __device__ __forceinline__ int64_t merge_path_global(const K* __restrict__ a, int64_t na,
@@ -80,9 +116,10 @@ __device__ __forceinline__ int64_t merge_path_global(const K* __restrict__ a, in
                                                      int64_t d) {
   int64_t lo = d - nb > 0 ? d - nb : 0;
   int64_t hi = d < na ? d : na;
+  const uint64_t pol = probe_policy();
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
-    if (__ldg(a + mid) > __ldg(b + (d - 1 - mid))) hi = mid;
+    if (probe_ld(a + mid, pol) > probe_ld(b + (d - 1 - mid), pol)) hi = mid;
     else lo = mid + 1;
   }
   return lo;
@@ -93,9 +130,10 @@ template <class K>
 __device__ __forceinline__ int64_t merge_path_global_range(const K* __restrict__ a,
                                                            const K* __restrict__ b, int64_t d,
                                                            int64_t lo, int64_t hi) {
+  const uint64_t pol = probe_policy();
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
-    if (__ldg(a + mid) > __ldg(b + (d - 1 - mid))) hi = mid;
+    if (probe_ld(a + mid, pol) > probe_ld(b + (d - 1 - mid), pol)) hi = mid;
     else lo = mid + 1;
   }
   return lo;
