@@ -259,11 +259,14 @@ def main():
     ws = ms.workspace(n, torch.int32, False, world=world, device=dev)
     stream = torch.cuda.current_stream()
 
+    last_split = [None]
+
     def step():
         if world == 1:
             ms.msort_sort_out(kin, kout, ws=ws, stream=stream)
         else:
-            ms.msort_sort_distributed_out(kin, kout, comm, ws=ws, stream=stream)
+            last_split[0] = ms.msort_sort_distributed_out(kin, kout, comm, ws=ws, stream=stream,
+                                                          return_split=True)[2]
 
     def barrier():
         if world > 1:
@@ -346,6 +349,25 @@ def main():
         t_roof += n * wk * (world - 1) / world / 770e9 + alg_bytes * 3 / (peak * 1e9)
 
     clocks = sampler.summary(t0, t1)
+
+    # N > 1: the D3 exchange against NVLink -- the bytes this rank sends and
+    # receives over NVLink (its segments to / from the other ranks, from the
+    # split matrix of the last step) per exchange, over the exchange's live
+    # CUDA-event time; the slowest rank is reported
+    xroof = None
+    if world > 1 and prof.get("exchange", (0, 0.0))[0]:
+        S = last_split[0]
+        sent = sum(int(S[j + 1][rank] - S[j][rank]) for j in range(world) if j != rank) * wk
+        recv = sum(int(S[rank + 1][j] - S[rank][j]) for j in range(world) if j != rank) * wk
+        xl, xms = prof["exchange"]
+        ach = max(sent, recv) / (xms / xl / 1e3) / 1e9
+        t = torch.tensor([ach], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ach = float(t.item())
+        xroof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 770.0, "unit": "GB/s",
+                 "frac": round(ach / 770.0, 4), "bytes_sent": sent, "bytes_received": recv,
+                 "avg_exchange_ms": round(xms / xl, 4),
+                 "peak_source": "measured peer copy per direction (B200_PROFILING.md; 900 nominal)"}
 
     # end to end through the public API with HOST buffers: every step uploads
     # its input from pinned host memory, sorts, and copies the sorted keys back
@@ -444,6 +466,7 @@ def main():
                        "parallelism": f"dp{world}" if world > 1 else "single",
                        "exchange": args.exchange if world > 1 else None},
             "roofline": roof,
+            "exchange_roofline": xroof,
             "step_roofline": {"bytes_per_gpu": step_bytes, "t_roof_ms": t_roof * 1e3,
                               "frac": round(t_roof * 1e3 / ms_step, 4),
                               "floor_frac": round(2 * n * wk / (peak * 1e9) * 1e3 / ms_step, 4)},

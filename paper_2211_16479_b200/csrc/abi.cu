@@ -58,7 +58,7 @@ static cudaEvent_t get_event() {
 }
 
 LaunchScope::LaunchScope(KernelClass k, cudaStream_t st) : kc(k), s(st), slot(-1) {
-  if (k != KC_NCCL) g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (k != KC_NCCL && k != KC_EXCHANGE) g_launches.fetch_add(1, std::memory_order_relaxed);
   if (g_profile.load(std::memory_order_relaxed)) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     EventRec r{get_event(), get_event(), kc};

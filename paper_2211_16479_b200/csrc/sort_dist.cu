@@ -263,7 +263,7 @@ struct NcclColl {
     RankIO& r0 = io[0];
     auto sp = [&](int r, int j) { return S[(size_t)r * p + j]; };
     int64_t roff = 0;
-    LaunchScope ls(KC_NCCL, s);
+    LaunchScope ls(KC_EXCHANGE, s);
     MSORT_NCCL_TRY(ncclGroupStart());
     for (int j = 0; j < p; ++j) {
       // receive run j
@@ -405,6 +405,7 @@ struct EmulColl {
                         msort_dtype vd) {
     const size_t wk = dtype_size(kd);
     auto sp = [&](int r, int j) { return S[(size_t)r * p + j]; };
+    LaunchScope ls(KC_EXCHANGE, s);
     for (int me = 0; me < p; ++me) {
       int64_t roff = 0;
       for (int j = 0; j < p; ++j) {
