@@ -111,6 +111,30 @@ msort_status msort_sort_out_ws(const void *in_keys, const void *in_vals, void *k
                                msort_dtype val_dtype, void *ws, size_t ws_bytes,
                                msort_stream_t stream);
 
+/* Batched (segmented) sort -- SURVEY.md §8(f) f3, the paper's small-array
+ * regime (below a size the parallel overhead dominates, so
+ * many small arrays are sorted in one call instead of one call each).
+ * Sorts every segment keys[off[i], off[i+1]) (and vals alike) independently,
+ * ascending and stable, in place: segment i ends as msort_sort_pairs of that
+ * slice alone (P:77-84 applied per segment).
+ *   seg_offsets  HOST array of nseg + 1 int64: off[0] = 0, non-decreasing,
+ *                off[nseg] = n (empty segments allowed); read during the call.
+ *   keys, vals   device arrays of n elements (vals NULL with MSORT_NONE).
+ *   ws           device workspace, 256-byte aligned, at least
+ *                msort_segmented_workspace_bytes(n, nseg, ...) bytes, not
+ *                overlapping keys/vals.
+ * Segments of <= 256 elements are sorted one per warp, <= msort_tile_size
+ * one per CTA, longer ones by the single-array sort (one after another).
+ * Asynchronous on `stream`; the segment table is copied to the device
+ * during the call (from pageable memory: the host thread may block briefly).
+ * Errors: INVALID_VALUE for bad offsets (not starting at 0, decreasing, not
+ * ending at n), NULL pointers with n > 0, a bad dtype or a short workspace. */
+msort_status msort_segmented_workspace_bytes(size_t n, size_t nseg, msort_dtype key_dtype,
+                                             msort_dtype val_dtype, size_t *bytes);
+msort_status msort_sort_segmented(void *keys, void *vals, size_t n, const int64_t *seg_offsets,
+                                  size_t nseg, msort_dtype key_dtype, msort_dtype val_dtype,
+                                  void *ws, size_t ws_bytes, msort_stream_t stream);
+
 /* End-to-end sort of HOST arrays (the e2e path of bench.py).  Enqueued on
  * `stream`: host_keys[0..n) (and host_vals) are copied into the caller's
  * device buffers dev_keys (dev_vals), sorted there in place (msort_sort_ws,

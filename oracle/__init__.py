@@ -89,6 +89,25 @@ def sort(keys: np.ndarray, vals: np.ndarray | None = None):
     return k if vals is None else (k, v)
 
 
+def sort_segmented(keys: np.ndarray, offsets, vals: np.ndarray | None = None):
+    """Batched sort (include/msort.h msort_sort_segmented): the stable sort of
+    P:77-84 applied to every segment keys[off[i]:off[i+1]] on its own.
+    Returns keys, or (keys, vals)."""
+    k = np.ascontiguousarray(keys).copy()
+    v = None if vals is None else np.ascontiguousarray(vals, dtype=np.uint32).copy()
+    off = np.asarray(offsets, dtype=np.int64)
+    for i in range(off.size - 1):
+        a, b = int(off[i]), int(off[i + 1])
+        if b - a >= 2:
+            ks = k[a:b].copy()
+            vs = None if v is None else v[a:b].copy()
+            sort_inplace(ks, vs)
+            k[a:b] = ks
+            if v is not None:
+                v[a:b] = vs
+    return k if vals is None else (k, v)
+
+
 def merge(a, b, av=None, bv=None):
     """merge(left, right), ties to the left run (reading R1)."""
     a = np.ascontiguousarray(a)

@@ -42,6 +42,7 @@ EXPORTED = (
     "msort_plan_narrow", "msort_plan_fill", "msort_status_string", "msort_last_error",
     "msort_profile_enable", "msort_profile_reset", "msort_profile_read", "msort_launch_count",
     "msort_tile_size", "msort_debug_set_quad", "msort_sort_host", "msort_debug_set_exchange",
+    "msort_segmented_workspace_bytes", "msort_sort_segmented",
 )
 
 
@@ -87,6 +88,10 @@ def _load():
     L.msort_profile_enable.argtypes = [i32]
     L.msort_profile_read.argtypes = [i64p, c.POINTER(c.c_double)]
     L.msort_launch_count.restype = c.c_int64
+    L.msort_segmented_workspace_bytes.argtypes = [c.c_size_t, c.c_size_t, i32, i32,
+                                                  c.POINTER(c.c_size_t)]
+    L.msort_sort_segmented.argtypes = [c.c_void_p, c.c_void_p, c.c_size_t, i64p, c.c_size_t, i32,
+                                       i32, c.c_void_p, c.c_size_t, c.c_void_p]
     L.msort_tile_size.argtypes = [i32, i32]
     L.msort_tile_size.restype = i32
     for f in ("msort_sort", "msort_sort_pairs", "msort_workspace_bytes", "msort_sort_ws",
@@ -94,7 +99,8 @@ def _load():
               "msort_comm_unique_id", "msort_comm_init", "msort_comm_destroy",
               "msort_sort_distributed", "msort_sort_distributed_ws",
               "msort_sort_distributed_emulated", "msort_plan_init", "msort_plan_candidates",
-              "msort_plan_narrow", "msort_plan_fill", "msort_profile_read"):
+              "msort_plan_narrow", "msort_plan_fill", "msort_profile_read",
+              "msort_segmented_workspace_bytes", "msort_sort_segmented"):
         getattr(L, f).restype = i32
     return L
 
@@ -134,6 +140,14 @@ def _stream(stream) -> int:
 
 def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _keep_for(ws: torch.Tensor, stream) -> None:
+    """A workspace allocated here on the current stream but used on another
+    one: keep the caching allocator from reusing it before that stream is
+    done with it."""
+    if stream is not None and isinstance(stream, torch.cuda.Stream):
+        ws.record_stream(stream)
 
 
 def _check_tensor(t: torch.Tensor, name: str):
@@ -178,6 +192,7 @@ def msort_sort_pairs(keys: torch.Tensor, vals: torch.Tensor | None, ws: torch.Te
         return keys, vals
     if ws is None:
         ws = workspace(n, keys.dtype, vals is not None, device=keys.device)
+        _keep_for(ws, stream)
     with torch.cuda.device(keys.device):
         _check(lib.msort_sort_ws(_ptr(keys), _ptr(vals), n, kd, vd, _ptr(ws), ws.numel(),
                                  ctypes.c_void_p(_stream(stream))), "msort_sort_ws")
@@ -197,6 +212,7 @@ def msort_sort_out(in_keys: torch.Tensor, keys_out: torch.Tensor, in_vals=None, 
     kd, vd = _dt(in_keys), _vdt(in_vals)
     if ws is None:
         ws = workspace(n, in_keys.dtype, in_vals is not None, device=in_keys.device)
+        _keep_for(ws, stream)
     with torch.cuda.device(in_keys.device):
         _check(lib.msort_sort_out_ws(_ptr(in_keys), _ptr(in_vals), _ptr(keys_out), _ptr(vals_out),
                                      n, kd, vd, _ptr(ws), ws.numel(),
@@ -220,12 +236,50 @@ def msort_sort_host(host_keys: torch.Tensor, host_keys_out: torch.Tensor, dev_ke
     kd, vd = _dt(dev_keys), _vdt(dev_vals)
     if ws is None:
         ws = workspace(n, dev_keys.dtype, dev_vals is not None, device=dev_keys.device)
+        _keep_for(ws, stream)
     with torch.cuda.device(dev_keys.device):
         _check(lib.msort_sort_host(_ptr(host_keys), _ptr(host_vals), _ptr(host_keys_out),
                                    _ptr(host_vals_out), n, kd, vd, _ptr(dev_keys), _ptr(dev_vals),
                                    _ptr(ws), ws.numel(), ctypes.c_void_p(_stream(stream))),
                "msort_sort_host")
     return host_keys_out, host_vals_out
+
+
+def msort_segmented_workspace_bytes(n: int, nseg: int, key_dtype: int,
+                                    val_dtype: int = MSORT_NONE) -> int:
+    out = ctypes.c_size_t()
+    _check(lib.msort_segmented_workspace_bytes(n, nseg, key_dtype, val_dtype, ctypes.byref(out)),
+           "msort_segmented_workspace_bytes")
+    return out.value
+
+
+def msort_sort_segmented(keys: torch.Tensor, seg_offsets, vals: torch.Tensor | None = None,
+                         ws: torch.Tensor | None = None, stream=None):
+    """Batched stable sort of every segment keys[off[i]:off[i+1]] (and vals)
+    in place (include/msort.h msort_sort_segmented).  seg_offsets: nseg + 1
+    int64 offsets (list, numpy array or tensor; copied to the host)."""
+    _check_tensor(keys, "keys")
+    if vals is not None:
+        _check_tensor(vals, "vals")
+        if vals.numel() != keys.numel() or vals.device != keys.device:
+            raise ValueError("keys/vals size or device mismatch")
+    if isinstance(seg_offsets, torch.Tensor):
+        seg_offsets = seg_offsets.detach().cpu().numpy()
+    off = np.ascontiguousarray(np.asarray(seg_offsets, dtype=np.int64))
+    if off.ndim != 1 or off.size < 1:
+        raise ValueError("seg_offsets must be a 1-D array of nseg + 1 offsets")
+    n, nseg = keys.numel(), off.size - 1
+    kd, vd = _dt(keys), _vdt(vals)
+    if ws is None:
+        nb = msort_segmented_workspace_bytes(n, nseg, kd, vd)
+        ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=keys.device)
+        _keep_for(ws, stream)
+    with torch.cuda.device(keys.device):
+        _check(lib.msort_sort_segmented(_ptr(keys), _ptr(vals), n,
+                                        off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), nseg,
+                                        kd, vd, _ptr(ws), ws.numel(),
+                                        ctypes.c_void_p(_stream(stream))), "msort_sort_segmented")
+    return keys, vals
 
 
 def sort(x: torch.Tensor) -> torch.Tensor:

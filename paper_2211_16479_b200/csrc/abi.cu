@@ -235,6 +235,56 @@ msort_status msort_workspace_bytes(size_t n, msort_dtype key_dtype, msort_dtype 
   return MSORT_SUCCESS;
 }
 
+static size_t seg_ws_bytes(size_t n, size_t nseg, msort_dtype kd, msort_dtype vd) {
+  // Kernels::sort_segmented: ping-pong keys (+ vals) for the segments longer
+  // than a tile T; the uploaded tables (<= 2 words per short segment, 2 per
+  // K1 tile of a long one, 3.5 + 1 per long segment); the merge completion
+  // counters (<= 48 levels x merge tiles, Tm >= T/2); the chunk counter.
+  const size_t T = (size_t)tile_size_for(kd, vd);
+  const size_t tiles = n / T + 1;
+  size_t b = align_up(n * dtype_size(kd), 256);
+  if (vd != MSORT_NONE) b += align_up(n * 4, 256);
+  b += align_up(8 * (8 * nseg + 2 * tiles + 8), 256);
+  b += align_up(4 * 48 * (2 * tiles + nseg), 256);
+  return b + 256 + 1024;
+}
+
+msort_status msort_segmented_workspace_bytes(size_t n, size_t nseg, msort_dtype key_dtype,
+                                             msort_dtype val_dtype, size_t* bytes) {
+  if (!bytes || !dtype_size(key_dtype) ||
+      (val_dtype != MSORT_NONE && val_dtype != MSORT_UINT32 && val_dtype != MSORT_INT32)) {
+    set_error("bad argument to msort_segmented_workspace_bytes");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  *bytes = seg_ws_bytes(n, nseg, key_dtype, val_dtype);
+  return MSORT_SUCCESS;
+}
+
+msort_status msort_sort_segmented(void* keys, void* vals, size_t n, const int64_t* seg_offsets,
+                                  size_t nseg, msort_dtype key_dtype, msort_dtype val_dtype,
+                                  void* ws, size_t ws_bytes, msort_stream_t stream) {
+  MSORT_TRY(validate(keys, vals, n, key_dtype, val_dtype, false));
+  if (!seg_offsets) {
+    set_error("seg_offsets is NULL");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  if (seg_offsets[0] != 0 || seg_offsets[nseg] != (int64_t)n) {
+    set_error("seg_offsets must start at 0 and end at n");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  for (size_t i = 0; i < nseg; ++i)
+    if (seg_offsets[i + 1] < seg_offsets[i]) {
+      set_error("seg_offsets decrease at segment " + std::to_string(i));
+      return MSORT_ERROR_INVALID_VALUE;
+    }
+  if (n < 2 || nseg == 0) return MSORT_SUCCESS;
+  MSORT_TRY(check_device());
+  MSORT_TRY(validate_ws(keys, vals, n, key_dtype, val_dtype, ws, ws_bytes,
+                        seg_ws_bytes(n, nseg, key_dtype, val_dtype)));
+  return sort_segmented_dispatch(keys, vals, seg_offsets, nseg, key_dtype, val_dtype, ws,
+                                 ws_bytes, (cudaStream_t)stream);
+}
+
 msort_status msort_sort_ws(void* keys, void* vals, size_t n, msort_dtype key_dtype,
                            msort_dtype val_dtype, void* ws, size_t ws_bytes,
                            msort_stream_t stream) {

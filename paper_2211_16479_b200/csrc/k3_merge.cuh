@@ -209,8 +209,8 @@ struct SinglePass {
   __device__ __forceinline__ const uint32_t* pvb(int, int64_t q, int64_t A0, int64_t na) const {
     return pm.rb(src_v, q, A0, na, true);
   }
-  __device__ __forceinline__ K* dstk(int) const { return dst_k; }
-  __device__ __forceinline__ uint32_t* dstv(int) const { return dst_v; }
+  __device__ __forceinline__ K* dstk(int, int64_t) const { return dst_k; }
+  __device__ __forceinline__ uint32_t* dstv(int, int64_t) const { return dst_v; }
   __device__ __forceinline__ void tile_done(int, int64_t, int) const {}
 };
 
@@ -289,8 +289,8 @@ struct FusedPasses {
   __device__ __forceinline__ const uint32_t* pvb(int p, int64_t, int64_t A0, int64_t na) const {
     return bv[p & 1] + A0 + na;
   }
-  __device__ __forceinline__ K* dstk(int p) const { return bk[(p + 1) & 1]; }
-  __device__ __forceinline__ uint32_t* dstv(int p) const { return bv[(p + 1) & 1]; }
+  __device__ __forceinline__ K* dstk(int p, int64_t) const { return bk[(p + 1) & 1]; }
+  __device__ __forceinline__ uint32_t* dstv(int p, int64_t) const { return bv[(p + 1) & 1]; }
   // Called by one thread after the tile's output (bulk store waited for,
   // scalar stores ordered by a CTA barrier) is complete.
   __device__ __forceinline__ void tile_done(int pass, int64_t q, int Tm) const {
@@ -298,6 +298,129 @@ struct FusedPasses {
     fence_proxy_async_global();
 #endif
     red_release_gpu_add(done + pair_base[pass] + pair_of(pass, q, Tm), 1u);
+  }
+};
+
+// All merge levels of a BATCH of segments (msort_sort_segmented, segments
+// longer than a tile) in one dataflow launch.  Segment s (in the order of the
+// host's list: level count descending) occupies [off[s], off[s] + len[s]) of
+// both buffers and tiles [tile0[s], tile0[s+1]) of every level -- a segment
+// has ceil(len / Tm) output tiles at every level, since 2L is a multiple of
+// Tm.  Level p of segment s merges runs of L_p = T * 2^p starting at off[s];
+// segments with fewer levels drop out of the tail of the tile range (level p
+// covers tiles [0, ntl[p])).  Segment s with P_s levels was tile-sorted into
+// buffer P_s & 1 and level p reads buffer (P_s - p) & 1, so its last level
+// writes buffer 0, the caller's array.  Completion counters: done[p * ntiles
+// + first tile of the level-p pair] counts that pair's finished tiles.
+constexpr int kMaxSegLevels = 48;
+template <class K>
+struct SegFused {
+  static constexpr bool kFused = true;
+  K* bk[2];
+  uint32_t* bv[2];
+  const int64_t* off;    // [nseg] first element of each segment
+  const int64_t* len;    // [nseg] its length
+  const int64_t* tile0;  // [nseg + 1] first output tile of each segment
+  const int* lev;        // [nseg] its number of merge levels P_s
+  int nseg;
+  int64_t T, ntiles;
+  int P;
+  int ch, grab;
+  unsigned* done;
+  int64_t ntl[kMaxSegLevels];          // tiles of level p (a prefix of the segments)
+  int64_t cbase[kMaxSegLevels + 1];    // first chunk of level p
+  __host__ __device__ __forceinline__ int64_t nchunks() const { return cbase[P]; }
+  __device__ __forceinline__ void chunk(int64_t g, int& pass, int64_t& q0, int& cnt) const {
+    int p = 0;
+    while (p + 1 < P && cbase[p + 1] <= g) ++p;
+    pass = p;
+    q0 = (g - cbase[p]) * ch;
+    cnt = (int)min((int64_t)ch, ntl[p] - q0);
+  }
+  __device__ __forceinline__ int64_t tiles(int pass) const { return ntl[pass]; }
+  __device__ __forceinline__ int seg_of(int64_t q) const {
+    int lo = 0, hi = nseg - 1;  // last s with tile0[s] <= q
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tile0[mid] <= q) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  }
+  __device__ __forceinline__ int64_t L(int pass) const { return T << pass; }
+  __device__ __forceinline__ void locate(int pass, int64_t q, int Tm, int64_t& A0, int64_t& na,
+                                         int64_t& nb, int64_t& dl) const {
+    const int s = seg_of(q);
+    const int64_t d = (q - tile0[s]) * Tm, l = len[s], Lp = L(pass);
+    const int64_t m = d / (2 * Lp);
+    A0 = off[s] + m * 2 * Lp;
+    na = min(Lp, l - m * 2 * Lp);
+    nb = max((int64_t)0, min(Lp, l - m * 2 * Lp - Lp));
+    dl = d - m * 2 * Lp;
+  }
+  __device__ __forceinline__ int src_buf(int pass, int64_t q) const {
+    return (lev[seg_of(q)] - pass) & 1;
+  }
+  __device__ __forceinline__ const K* pa(int p, int64_t q, int64_t A0, int64_t) const {
+    return bk[src_buf(p, q)] + A0;
+  }
+  __device__ __forceinline__ const K* pb(int p, int64_t q, int64_t A0, int64_t na) const {
+    return bk[src_buf(p, q)] + A0 + na;
+  }
+  __device__ __forceinline__ const uint32_t* pva(int p, int64_t q, int64_t A0, int64_t) const {
+    return bv[src_buf(p, q)] + A0;
+  }
+  __device__ __forceinline__ const uint32_t* pvb(int p, int64_t q, int64_t A0, int64_t na) const {
+    return bv[src_buf(p, q)] + A0 + na;
+  }
+  __device__ __forceinline__ K* dstk(int p, int64_t q) const { return bk[src_buf(p, q) ^ 1]; }
+  __device__ __forceinline__ uint32_t* dstv(int p, int64_t q) const {
+    return bv[src_buf(p, q) ^ 1];
+  }
+  // first tile and tile count of the level-p pair holding tile q
+  __device__ __forceinline__ void pair_tiles(int pass, int64_t q, int Tm, int64_t& first,
+                                             unsigned& cnt) const {
+    const int s = seg_of(q);
+    const int64_t t = q - tile0[s], per = 2 * L(pass) / Tm;  // tiles per full pair
+    first = tile0[s] + t / per * per;
+    cnt = (unsigned)min(per, tile0[s + 1] - first);
+  }
+  // Level p >= 1 reads the level-(p-1) pairs covering each tile's level-p
+  // pair: wait until they are complete (the whole warp returns together).
+  __device__ __forceinline__ void wait_ready(int pass, int64_t q0, int cnt, int lane,
+                                             int Tm) const {
+    if (pass == 0) return;  // tile-sorted before this launch
+    const int64_t half = L(pass) / Tm;  // tiles per full level-(p-1) pair
+    // every level-(p-1) pair start in [first pair of q0, end of q0+cnt-1's pair)
+    int64_t f0, f1;
+    unsigned c0, c1;
+    pair_tiles(pass, q0, Tm, f0, c0);
+    pair_tiles(pass, q0 + cnt - 1, Tm, f1, c1);
+    const int64_t end = f1 + c1;
+    for (int64_t f = f0; f < end;) {
+      // f is the first tile of a level-(p-1) pair: its segment and size
+      const int s = seg_of(f);
+      const int64_t segend = tile0[s + 1];
+      // pairs of this segment start at tile0[s] + j * half
+      const int64_t npairs = (min(end, segend) - f + half - 1) / half;
+      for (int64_t j = lane; j < npairs; j += 32) {
+        const int64_t pf = f + j * half;
+        const unsigned need = (unsigned)min(half, segend - pf);
+        const unsigned* c = done + (int64_t)(pass - 1) * ntiles + pf;
+        while (ld_acquire_gpu(c) < need) __nanosleep(256);
+      }
+      f = min(end, segend);
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ void tile_done(int pass, int64_t q, int Tm) const {
+    int64_t first;
+    unsigned cnt;
+    pair_tiles(pass, q, Tm, first, cnt);
+#ifndef MSORT_K3_NOPROXYFENCE
+    fence_proxy_async_global();
+#endif
+    red_release_gpu_add(done + (int64_t)pass * ntiles + first, 1u);
   }
 };
 
@@ -636,7 +759,7 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
         if (m.out < 0) break;
         K* sk = stk + (size_t)s * LY::SKE;
         uint32_t* sv = stv + (size_t)s * LY::SVE;
-        K* gk = src.dstk(m.pass) + m.out;
+        K* gk = src.dstk(m.pass, m.q) + m.out;
         const int phk = stage_offset(gk);
         int hk, mk;
         window_split(gk, m.tot, hk, mk);
@@ -644,7 +767,7 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
         uint32_t* gv = nullptr;
         int phv = 0, hv = 0, mv = 0;
         if constexpr (PAIRS) {
-          gv = src.dstv(m.pass) + m.out;
+          gv = src.dstv(m.pass, m.q) + m.out;
           phv = stage_offset(gv);
           window_split(gv, m.tot, hv, mv);
           if (mv) bulk_s2g(gv + hv, sv + phv + hv, (uint32_t)(mv * 4));
@@ -733,9 +856,9 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
       named_bar_sync(1, NC);  // everyone is done reading stage s: overwrite it
       // The output keeps its global 16-byte phase so the aligned middle leaves
       // by one bulk store (TMA, cp.async.bulk.global.shared).
-      const int phk = stage_offset(src.dstk(m.pass) + m.out);
+      const int phk = stage_offset(src.dstk(m.pass, m.q) + m.out);
       int phv = 0;
-      if constexpr (PAIRS) phv = stage_offset(src.dstv(m.pass) + m.out);
+      if constexpr (PAIRS) phv = stage_offset(src.dstv(m.pass, m.q) + m.out);
 #pragma unroll
       for (int t = 0; t < VT; ++t) {
         if (d + t < m.tot) {

@@ -19,6 +19,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "k3_merge.cuh"
 #include "k3q_merge.cuh"
@@ -26,6 +29,7 @@
 #include "msort_device.cuh"
 #include "networks.cuh"
 #include "msort_internal.h"
+#include "seg_sort.cuh"
 
 namespace msort {
 
@@ -35,7 +39,8 @@ namespace msort {
 template <class K, bool PAIRS, int NT, int VT>
 __global__ void __launch_bounds__(NT)
     k1_tile_sort(const K* __restrict__ in_k, const uint32_t* __restrict__ in_v,
-                 K* __restrict__ out_k, uint32_t* __restrict__ out_v, int64_t n) {
+                 K* __restrict__ out_k, uint32_t* __restrict__ out_v, int64_t n,
+                 const int64_t* __restrict__ seg) {
   constexpr int T = NT * VT;
   extern __shared__ __align__(16) unsigned char smem[];
   K* sk = reinterpret_cast<K*>(smem);                 // T keys
@@ -43,8 +48,10 @@ __global__ void __launch_bounds__(NT)
   uint32_t* sv = reinterpret_cast<uint32_t*>(si + T);  // PAIRS: payload staging
 
   const int tid = threadIdx.x;
-  const int64_t base = (int64_t)blockIdx.x * T;
-  const int cnt = (int)min((int64_t)T, n - base);
+  // tile blockIdx.x of the array, or (segmented sorts, seg_sort.cuh) the
+  // segment of descriptor blockIdx.x: (offset, length <= T)
+  const int64_t base = seg ? seg[2 * blockIdx.x] : (int64_t)blockIdx.x * T;
+  const int cnt = seg ? (int)seg[2 * blockIdx.x + 1] : (int)min((int64_t)T, n - base);
 
   K key[VT];
   int idx[VT];
@@ -282,7 +289,8 @@ struct K1KeysShape {
 
 template <class K, int NT, int VT>
 __global__ void __launch_bounds__(NT)
-    k1_tile_sort_keys(const K* __restrict__ in_k, K* __restrict__ out_k, int64_t n) {
+    k1_tile_sort_keys(const K* __restrict__ in_k, K* __restrict__ out_k, int64_t n,
+                      const int64_t* __restrict__ seg) {
   using SH = K1KeysShape<K, NT, VT>;
   static_assert(VT % VecOf<K>::W == 0, "keys-only K1 stores 16-byte vectors");
   constexpr int T = SH::T;
@@ -292,8 +300,9 @@ __global__ void __launch_bounds__(NT)
   K* sk = reinterpret_cast<K*>(smem + 16);
   const char* sb = reinterpret_cast<const char*>(smem);  // byte offsets include the guard
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int64_t base = (int64_t)blockIdx.x * T;
-  const int cnt = (int)min((int64_t)T, n - base);
+  // tile blockIdx.x, or the segment of descriptor blockIdx.x (as in k1_tile_sort)
+  const int64_t base = seg ? seg[2 * blockIdx.x] : (int64_t)blockIdx.x * T;
+  const int cnt = seg ? (int)seg[2 * blockIdx.x + 1] : (int)min((int64_t)T, n - base);
 
   // Which thread holds which key before the network does not matter (keys
   // only), so load straight into registers, striped (coalesced); the partial
@@ -427,6 +436,51 @@ static int quad_mode() {
 // sort) then the per-level, per-pair completion counters of the fused merge.
 constexpr int kMaxLaunches = 64;
 
+// Page-locked staging buffer for host tables uploaded by a call (segment
+// descriptors).  staging_acquire waits until the previous upload from it has
+// completed (an event recorded by staging_release), growing it if needed;
+// the mutex is held from acquire to release.
+static std::mutex g_stage_mu;
+static void* g_stage = nullptr;
+static size_t g_stage_cap = 0;
+static cudaEvent_t g_stage_ev = nullptr;
+static msort_status staging_acquire(size_t bytes, void** out) {
+  g_stage_mu.lock();
+  if (g_stage_ev) {
+    cudaError_t e = cudaEventSynchronize(g_stage_ev);
+    if (e != cudaSuccess) {
+      g_stage_mu.unlock();
+      return cuda_fail(e, "staging event");
+    }
+  } else {
+    cudaError_t e = cudaEventCreateWithFlags(&g_stage_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      g_stage_mu.unlock();
+      return cuda_fail(e, "cudaEventCreate");
+    }
+  }
+  if (bytes > g_stage_cap) {
+    if (g_stage) cudaFreeHost(g_stage);
+    g_stage = nullptr;
+    g_stage_cap = 0;
+    const size_t cap = std::max<size_t>(bytes + bytes / 2, 1 << 16);
+    cudaError_t e = cudaHostAlloc(&g_stage, cap, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+      g_stage_mu.unlock();
+      return cuda_fail(e, "cudaHostAlloc (staging)");
+    }
+    g_stage_cap = cap;
+  }
+  *out = g_stage;
+  return MSORT_SUCCESS;
+}
+static msort_status staging_release(cudaStream_t s) {
+  cudaError_t e = cudaEventRecord(g_stage_ev, s);
+  g_stage_mu.unlock();
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord (staging)");
+  return MSORT_SUCCESS;
+}
+
 template <class K, bool PAIRS>
 struct Kernels {
   // K1 shape.  Pairs: 512 threads x 17 (odd: conflict-free blocked shared
@@ -536,6 +590,7 @@ struct Kernels {
     MSORT_TRY(set_smem<Fused>());
     MSORT_TRY(set_smem<Explicit>());
     MSORT_TRY(set_smem<Peer>());
+    MSORT_TRY(set_smem<SegF>());
 #ifdef MSORT_K3_PERPASS
     MSORT_TRY((set_smem<SinglePass<K, UniformPairs>>()));
 #endif
@@ -652,10 +707,11 @@ struct Kernels {
       LaunchScope ls(KC_TILE_SORT, s);
       if constexpr (PAIRS)
         k1_tile_sort<K, PAIRS, NT1, VT>
-            <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, in_v, bk[cur], bv[cur], (int64_t)n);
+            <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, in_v, bk[cur], bv[cur], (int64_t)n,
+                                                     nullptr);
       else
         k1_tile_sort_keys<K, NT1, VT>
-            <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, bk[cur], (int64_t)n);
+            <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, bk[cur], (int64_t)n, nullptr);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
 #ifdef MSORT_K3_CHECK
@@ -750,6 +806,182 @@ struct Kernels {
     f.ch = chunk_tiles(f.ntiles, dev);
     f.grab = f.ch < kChunk ? 1 : kGrab;  // small sorts: one chunk per CTA at a time
     return launch_k3(f, (int64_t)left * ((f.ntiles + f.ch - 1) / f.ch), ctr, s, KC_MERGE);
+  }
+
+  // Batched sort of independent segments [off[i], off[i+1]) of keys/vals, in
+  // place (seg_sort.cuh, include/msort.h msort_sort_segmented).  Segments are
+  // binned by length: one warp per segment up to 256 elements (bitonic network
+  // with warp shuffles), one CTA per segment up to T (the tile-sort kernels
+  // reading a segment descriptor), and every longer segment through ONE
+  // tile-sort launch per buffer parity plus ONE fused merge launch over all
+  // of them (SegFused: all levels of all long segments as one dataflow).
+  static constexpr int kSegW8 = 256;  // warp classes: <= 32 (VW = 1), <= 256 (VW = 8)
+  static constexpr int kSegNTM = 128, kSegVTM = 17, kSegM = kSegNTM * kSegVTM;  // CTA class
+  using SegF = SegFused<K>;
+  static msort_status sort_segmented(K* keys, uint32_t* vals, const int64_t* off, size_t nseg,
+                                     void* ws, size_t ws_bytes, cudaStream_t s) {
+    MSORT_TRY(init());
+    int dev = 0;
+    MSORT_CUDA_TRY(cudaGetDevice(&dev));
+    const int64_t n = off[nseg];
+    // One host pass over the lengths: segments of <= 256 elements are found
+    // on the device (the warp kernel reads the uploaded offsets table); the
+    // longer ones are listed here -- CTA bins (<= T) and the long segments
+    // with their K1 tiles.
+    std::vector<int64_t> mid[2], xl;  // (offset, length) pairs: <= 2176, <= T
+    int64_t k1t = 0, nsmall = 0;
+    for (size_t i = 0; i < nseg; ++i) {
+      const int64_t len = off[i + 1] - off[i];
+      if (len <= kSegW8) {
+        nsmall += len >= 2;
+        continue;
+      }
+      if (len <= T) {
+        auto& m = mid[len <= kSegM ? 0 : 1];
+        m.push_back(off[i]);
+        m.push_back(len);
+      } else {
+        xl.push_back((int64_t)i);
+        k1t += (len + T - 1) / T;
+      }
+    }
+    const int64_t nxl = (int64_t)xl.size();
+    const int64_t nm = (int64_t)mid[0].size() / 2, nl = (int64_t)mid[1].size() / 2;
+    // staging layout (int64 words): the offsets table (only when there are
+    // short segments), CTA-bin descriptors, K1 tile descriptors of the long
+    // segments (even-level ones first), long-segment tables off[nxl] len[nxl]
+    // tile0[nxl+1] lev[nxl] (int32, packed)
+    const int64_t w_off = nsmall ? (int64_t)nseg + 1 : 0;
+    const int64_t w_desc = w_off + 2 * (nm + nl), w_k1 = 2 * k1t;
+    const int64_t w_tab = nxl ? 3 * nxl + 1 + (nxl + 1) / 2 : 0;
+    const int64_t words = w_desc + w_k1 + w_tab;
+    int64_t* h = nullptr;
+    MSORT_TRY(staging_acquire((size_t)words * 8, reinterpret_cast<void**>(&h)));
+    struct Unlock {  // early returns before staging_release
+      bool held = true;
+      ~Unlock() {
+        if (held) g_stage_mu.unlock();
+      }
+    } unlock;
+    if (w_off) std::memcpy(h, off, (size_t)w_off * 8);
+    if (nm) std::memcpy(h + w_off, mid[0].data(), (size_t)nm * 16);
+    if (nl) std::memcpy(h + w_off + 2 * nm, mid[1].data(), (size_t)nl * 16);
+    // long segments: level count P_s, ordered by it (descending, stable) so
+    // that level p's segments are a prefix of the tile range
+    auto levels = [](int64_t len) {
+      const int64_t t = (len + T - 1) / T;
+      int P = 0;
+      while ((int64_t(1) << P) < t) ++P;
+      return P;
+    };
+    std::stable_sort(xl.begin(), xl.end(), [&](int64_t x, int64_t y) {
+      return levels(off[x + 1] - off[x]) > levels(off[y + 1] - off[y]);
+    });
+    int Pmax = 0;
+    int64_t n_even_tiles = 0;
+    for (int64_t i : xl) {
+      const int P = levels(off[i + 1] - off[i]);
+      Pmax = std::max(Pmax, P);
+      if ((P & 1) == 0) n_even_tiles += (off[i + 1] - off[i] + T - 1) / T;
+    }
+    if (Pmax > kMaxSegLevels) {
+      set_error("segment too long");
+      return MSORT_ERROR_NOT_SUPPORTED;
+    }
+    {
+      int64_t pe = w_desc, po = w_desc + 2 * n_even_tiles;  // K1 tiles: even P_s, then odd
+      int64_t* toff = h + w_desc + w_k1;
+      int64_t* tlen = toff + nxl;
+      int64_t* tt0 = tlen + nxl;
+      int* tlev = reinterpret_cast<int*>(tt0 + nxl + 1);
+      int64_t tiles = 0;
+      for (int64_t j = 0; j < nxl; ++j) {
+        const int64_t i = xl[(size_t)j], o = off[i], len = off[i + 1] - o;
+        const int P = levels(len);
+        int64_t& pp = (P & 1) ? po : pe;
+        for (int64_t t = 0; t * T < len; ++t) {
+          h[pp++] = o + t * T;
+          h[pp++] = std::min<int64_t>(T, len - t * T);
+        }
+        toff[j] = o, tlen[j] = len, tt0[j] = tiles, tlev[j] = P;
+        tiles += (len + Tm - 1) / Tm;
+      }
+      tt0[nxl] = tiles;
+    }
+    // device workspace: [ping-pong keys n][vals n][staged words][done][ctr]
+    char* w = static_cast<char*>(ws);
+    K* wk = reinterpret_cast<K*>(w);
+    w += align_up((size_t)n * sizeof(K), 256);
+    uint32_t* wv = nullptr;
+    if (PAIRS) {
+      wv = reinterpret_cast<uint32_t*>(w);
+      w += align_up((size_t)n * 4, 256);
+    }
+    int64_t* dstage = reinterpret_cast<int64_t*>(w);
+    w += align_up((size_t)words * 8, 256);
+    const int64_t ntl_all = nxl ? h[w_desc + w_k1 + 2 * nxl + nxl] : 0;  // tile0[nxl]
+    unsigned* done = reinterpret_cast<unsigned*>(w);
+    w += align_up((size_t)std::max(Pmax, 1) * ntl_all * 4, 256);
+    auto* ctr = reinterpret_cast<unsigned long long*>(w);
+    w += 256;
+    if ((size_t)(w - static_cast<char*>(ws)) > ws_bytes) {
+      set_error("segmented sort: workspace too small");
+      return MSORT_ERROR_INVALID_VALUE;
+    }
+    if (words)
+      MSORT_CUDA_TRY(cudaMemcpyAsync(dstage, h, (size_t)words * 8, cudaMemcpyHostToDevice, s));
+    unlock.held = false;
+    MSORT_TRY(staging_release(s));
+    if (nsmall) {
+      LaunchScope ls(KC_TILE_SORT, s);
+      kseg_warp_sort<K, PAIRS>
+          <<<(unsigned)((nseg + 3) / 4), 128, 0, s>>>(keys, vals, dstage, (int64_t)nseg);
+    }
+    if (nm) {
+      LaunchScope ls(KC_TILE_SORT, s);
+      constexpr size_t sm = (size_t)kSegM * sizeof(K) + (PAIRS ? (size_t)kSegM * 8 : 0);
+      k1_tile_sort<K, PAIRS, kSegNTM, kSegVTM>
+          <<<(unsigned)nm, kSegNTM, sm, s>>>(keys, vals, keys, vals, 0, dstage + w_off);
+    }
+    auto k1_desc = [&](const int64_t* d, int64_t cnt_, K* ok, uint32_t* ov) {
+      LaunchScope ls(KC_TILE_SORT, s);
+      if constexpr (PAIRS)
+        k1_tile_sort<K, PAIRS, NT1, VT>
+            <<<(unsigned)cnt_, NT1, k1_smem, s>>>(keys, vals, ok, ov, 0, d);
+      else
+        k1_tile_sort_keys<K, NT1, VT><<<(unsigned)cnt_, NT1, k1_smem, s>>>(keys, ok, 0, d);
+    };
+    if (nl) k1_desc(dstage + w_off + 2 * nm, nl, keys, vals);
+    if (nxl) {
+      // long segments: K1 into buffer P_s & 1, then all levels of all of them
+      if (n_even_tiles) k1_desc(dstage + w_desc, n_even_tiles, keys, vals);
+      if (k1t > n_even_tiles)
+        k1_desc(dstage + w_desc + 2 * n_even_tiles, k1t - n_even_tiles, wk, wv);
+      MSORT_CUDA_TRY(cudaGetLastError());
+      if (Pmax > 0) {
+        SegF f{};
+        f.bk[0] = keys, f.bk[1] = wk, f.bv[0] = vals, f.bv[1] = wv;
+        const int64_t* tab = dstage + w_desc + w_k1;
+        f.off = tab, f.len = tab + nxl, f.tile0 = tab + 2 * nxl;
+        f.lev = reinterpret_cast<const int*>(tab + 3 * nxl + 1);
+        f.nseg = (int)nxl, f.T = T, f.ntiles = ntl_all, f.P = Pmax, f.done = done;
+        const int64_t* htt0 = h + w_desc + w_k1 + 2 * nxl;
+        f.ch = chunk_tiles(ntl_all, dev);
+        f.grab = f.ch < kChunk ? 1 : kGrab;
+        f.cbase[0] = 0;
+        int64_t act = nxl;  // segments with more than p levels (a prefix)
+        for (int p = 0; p < Pmax; ++p) {
+          while (act > 0 && levels(off[xl[(size_t)act - 1] + 1] - off[xl[(size_t)act - 1]]) <= p)
+            --act;
+          f.ntl[p] = htt0[act];
+          f.cbase[p + 1] = f.cbase[p] + (f.ntl[p] + f.ch - 1) / f.ch;
+        }
+        MSORT_CUDA_TRY(cudaMemsetAsync(done, 0, (size_t)Pmax * ntl_all * 4 + 256, s));
+        MSORT_TRY(launch_k3(f, f.nchunks(), ctr, s, KC_MERGE));
+      }
+    }
+    MSORT_CUDA_TRY(cudaGetLastError());
+    return MSORT_SUCCESS;
   }
 
   // First k-way round straight from the runs' owners (pull exchange): pair
@@ -880,6 +1112,28 @@ msort_status sort_single_dispatch(const void* in_keys, const void* in_vals, void
     case MSORT_UINT32: return sort_k<uint32_t>(in_keys, in_vals, keys, vals, n, ws, ws_bytes, s);
     case MSORT_INT64: return sort_k<int64_t>(in_keys, in_vals, keys, vals, n, ws, ws_bytes, s);
     case MSORT_UINT64: return sort_k<uint64_t>(in_keys, in_vals, keys, vals, n, ws, ws_bytes, s);
+    default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
+  }
+}
+
+template <class K>
+static msort_status seg_k(void* keys, void* vals, const int64_t* off, size_t nseg, void* ws,
+                          size_t ws_bytes, cudaStream_t s) {
+  if (vals)
+    return Kernels<K, true>::sort_segmented((K*)keys, (uint32_t*)vals, off, nseg, ws, ws_bytes,
+                                            s);
+  return Kernels<K, false>::sort_segmented((K*)keys, nullptr, off, nseg, ws, ws_bytes, s);
+}
+
+msort_status sort_segmented_dispatch(void* keys, void* vals, const int64_t* off, size_t nseg,
+                                     msort_dtype kd, msort_dtype vd, void* ws, size_t ws_bytes,
+                                     cudaStream_t s) {
+  if (vd == MSORT_NONE) vals = nullptr;
+  switch (kd) {
+    case MSORT_INT32: return seg_k<int32_t>(keys, vals, off, nseg, ws, ws_bytes, s);
+    case MSORT_UINT32: return seg_k<uint32_t>(keys, vals, off, nseg, ws, ws_bytes, s);
+    case MSORT_INT64: return seg_k<int64_t>(keys, vals, off, nseg, ws, ws_bytes, s);
+    case MSORT_UINT64: return seg_k<uint64_t>(keys, vals, off, nseg, ws, ws_bytes, s);
     default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
   }
 }

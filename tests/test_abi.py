@@ -49,6 +49,18 @@ def test_validation_without_device(ms):
     out = ctypes.c_size_t()
     assert L.msort_workspace_bytes(1 << 20, 0, 255, 1, ctypes.byref(out)) == 0
     assert out.value >= (1 << 20) * 4
+    # segmented sort: offsets must start at 0, not decrease and end at n
+    S = L.msort_sort_segmented
+    bad = (ctypes.c_int64 * 3)(0, 5, 4)
+    assert S(ctypes.c_void_p(4096), None, 4, bad, 2, 0, 255, None, 0, None) == 1
+    bad2 = (ctypes.c_int64 * 3)(1, 2, 4)
+    assert S(ctypes.c_void_p(4096), None, 4, bad2, 2, 0, 255, None, 0, None) == 1
+    assert S(ctypes.c_void_p(4096), None, 4, None, 2, 0, 255, None, 0, None) == 1
+    ok0 = (ctypes.c_int64 * 1)(0)
+    assert S(None, None, 0, ok0, 0, 0, 255, None, 0, None) == 0
+    sb = ctypes.c_size_t()
+    assert L.msort_segmented_workspace_bytes(1 << 20, 1000, 0, 1, ctypes.byref(sb)) == 0
+    assert sb.value >= 16 * 1000
     n2 = ctypes.c_size_t()
     assert L.msort_workspace_bytes(1 << 20, 2, 1, 8, ctypes.byref(n2)) == 0
     assert n2.value >= 2 * (1 << 20) * 12

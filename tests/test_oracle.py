@@ -279,3 +279,23 @@ def test_oracle_live_c1_matches_survey(orc):
     assert [int(s[p]) for p in (0, n // 4, n // 2, 3 * n // 4, n - 1)] == SURVEY["C1"]["sorted_at"]
     assert orc.check(k, s) == 0
     assert np.array_equal(s, np.sort(k, kind="stable"))
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.uint64])
+def test_segmented_definition(orc, dtype):
+    """Batched sort (f3): the oracle's per-segment sort equals the library
+    routine numpy.lexsort by (segment id, key) -- stable, so equal keys of a
+    segment keep their input order -- including empty and 1-element segments."""
+    rng = np.random.default_rng(7)
+    lens = np.concatenate([[0, 1, 2, 0, 3], rng.integers(0, 70, 400), [500, 0]])
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    n = int(off[-1])
+    k = rng.integers(0, 9, n).astype(dtype)  # heavy duplicates: stability is visible
+    v = np.arange(n, dtype=np.uint32)
+    seg = np.repeat(np.arange(lens.size), lens)
+    perm = np.lexsort((k, seg))  # last key primary; lexsort is stable
+    ok, ov = orc.sort_segmented(k, off, v)
+    assert np.array_equal(ok, k[perm]) and np.array_equal(ov, v[perm])
+    assert np.array_equal(orc.sort_segmented(k, off), k[perm])
+    # one segment = the plain sort
+    assert np.array_equal(orc.sort_segmented(k, [0, n]), orc.sort(k))
