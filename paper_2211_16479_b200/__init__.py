@@ -257,26 +257,37 @@ def msort_sort_segmented(keys: torch.Tensor, seg_offsets, vals: torch.Tensor | N
                          ws: torch.Tensor | None = None, stream=None):
     """Batched stable sort of every segment keys[off[i]:off[i+1]] (and vals)
     in place (include/msort.h msort_sort_segmented).  seg_offsets: nseg + 1
-    int64 offsets (list, numpy array or tensor; copied to the host)."""
+    int64 offsets -- a CUDA int64 tensor (used in place: classified on the
+    device, one stream synchronisation), or a list / numpy array / CPU tensor
+    (read on the host, fully asynchronous)."""
     _check_tensor(keys, "keys")
     if vals is not None:
         _check_tensor(vals, "vals")
         if vals.numel() != keys.numel() or vals.device != keys.device:
             raise ValueError("keys/vals size or device mismatch")
-    if isinstance(seg_offsets, torch.Tensor):
-        seg_offsets = seg_offsets.detach().cpu().numpy()
-    off = np.ascontiguousarray(np.asarray(seg_offsets, dtype=np.int64))
-    if off.ndim != 1 or off.size < 1:
-        raise ValueError("seg_offsets must be a 1-D array of nseg + 1 offsets")
-    n, nseg = keys.numel(), off.size - 1
+    dev_off = isinstance(seg_offsets, torch.Tensor) and seg_offsets.is_cuda
+    if dev_off:
+        off_t = seg_offsets.to(torch.int64).contiguous()
+        if off_t.dim() != 1 or off_t.numel() < 1 or off_t.device != keys.device:
+            raise ValueError("seg_offsets must be 1-D with nseg + 1 offsets on the keys' device")
+        off_ptr = ctypes.cast(ctypes.c_void_p(off_t.data_ptr()), ctypes.POINTER(ctypes.c_int64))
+        nseg = off_t.numel() - 1
+    else:
+        if isinstance(seg_offsets, torch.Tensor):
+            seg_offsets = seg_offsets.detach().numpy()
+        off = np.ascontiguousarray(np.asarray(seg_offsets, dtype=np.int64))
+        if off.ndim != 1 or off.size < 1:
+            raise ValueError("seg_offsets must be a 1-D array of nseg + 1 offsets")
+        off_ptr = off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+        nseg = off.size - 1
+    n = keys.numel()
     kd, vd = _dt(keys), _vdt(vals)
     if ws is None:
         nb = msort_segmented_workspace_bytes(n, nseg, kd, vd)
         ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=keys.device)
         _keep_for(ws, stream)
     with torch.cuda.device(keys.device):
-        _check(lib.msort_sort_segmented(_ptr(keys), _ptr(vals), n,
-                                        off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), nseg,
+        _check(lib.msort_sort_segmented(_ptr(keys), _ptr(vals), n, off_ptr, nseg,
                                         kd, vd, _ptr(ws), ws.numel(),
                                         ctypes.c_void_p(_stream(stream))), "msort_sort_segmented")
     return keys, vals

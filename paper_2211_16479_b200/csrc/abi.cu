@@ -245,6 +245,10 @@ static size_t seg_ws_bytes(size_t n, size_t nseg, msort_dtype kd, msort_dtype vd
   size_t b = align_up(n * dtype_size(kd), 256);
   if (vd != MSORT_NONE) b += align_up(n * 4, 256);
   b += align_up(8 * (8 * nseg + 2 * tiles + 8), 256);
+  // device-resident offsets: the classifier's lists (<= n / 257, n / 2177,
+  // n / (T + 1) entries of 16 bytes) and counters
+  b += align_up(16 * (n / 257 + 1), 256) + align_up(16 * (n / 2177 + 1), 256) +
+       align_up(16 * (n / (T + 1) + 1), 256) + 256;
   b += align_up(4 * 48 * (2 * tiles + nseg), 256);
   return b + 256 + 1024;
 }
@@ -268,21 +272,32 @@ msort_status msort_sort_segmented(void* keys, void* vals, size_t n, const int64_
     set_error("seg_offsets is NULL");
     return MSORT_ERROR_INVALID_VALUE;
   }
-  if (seg_offsets[0] != 0 || seg_offsets[nseg] != (int64_t)n) {
-    set_error("seg_offsets must start at 0 and end at n");
-    return MSORT_ERROR_INVALID_VALUE;
+  // where the table lives: device memory is classified (and checked) on the
+  // device; anything else is read here
+  bool dev_off = false;
+  {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, seg_offsets) == cudaSuccess)
+      dev_off = pa.type == cudaMemoryTypeDevice;
+    (void)cudaGetLastError();
   }
-  for (size_t i = 0; i < nseg; ++i)
-    if (seg_offsets[i + 1] < seg_offsets[i]) {
-      set_error("seg_offsets decrease at segment " + std::to_string(i));
+  if (!dev_off) {
+    if (seg_offsets[0] != 0 || seg_offsets[nseg] != (int64_t)n) {
+      set_error("seg_offsets must start at 0 and end at n");
       return MSORT_ERROR_INVALID_VALUE;
     }
+    for (size_t i = 0; i < nseg; ++i)
+      if (seg_offsets[i + 1] < seg_offsets[i]) {
+        set_error("seg_offsets decrease at segment " + std::to_string(i));
+        return MSORT_ERROR_INVALID_VALUE;
+      }
+  }
   if (n < 2 || nseg == 0) return MSORT_SUCCESS;
   MSORT_TRY(check_device());
   MSORT_TRY(validate_ws(keys, vals, n, key_dtype, val_dtype, ws, ws_bytes,
                         seg_ws_bytes(n, nseg, key_dtype, val_dtype)));
-  return sort_segmented_dispatch(keys, vals, seg_offsets, nseg, key_dtype, val_dtype, ws,
-                                 ws_bytes, (cudaStream_t)stream);
+  return sort_segmented_dispatch(keys, vals, seg_offsets, nseg, dev_off, n, key_dtype, val_dtype,
+                                 ws, ws_bytes, (cudaStream_t)stream);
 }
 
 msort_status msort_sort_ws(void* keys, void* vals, size_t n, msort_dtype key_dtype,

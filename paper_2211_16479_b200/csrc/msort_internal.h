@@ -66,8 +66,8 @@ size_t dist_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd, int world);
 // Single-GPU sort with explicit workspace (sort_single.cu): sorts in_keys/
 // in_vals into keys/vals (the same pointers for an in-place sort).
 msort_status sort_segmented_dispatch(void* keys, void* vals, const int64_t* off, size_t nseg,
-                                     msort_dtype kd, msort_dtype vd, void* ws, size_t ws_bytes,
-                                     cudaStream_t s);
+                                     bool dev_off, size_t n, msort_dtype kd, msort_dtype vd,
+                                     void* ws, size_t ws_bytes, cudaStream_t s);
 msort_status sort_single_dispatch(const void* in_keys, const void* in_vals, void* keys,
                                   void* vals, size_t n, msort_dtype kd, msort_dtype vd, void* ws,
                                   size_t ws_bytes, cudaStream_t s);

@@ -125,4 +125,43 @@ __global__ void __launch_bounds__(128)
   else warp_sort_segment<K, PAIRS, 8>(keys, vals, base, (int)len, lane);
 }
 
+// Device-resident offsets: classify every segment (and check the table:
+// off[0] = 0, non-decreasing, off[nseg] = n).  counts[0..2] = entries
+// appended to the lists of (offset, length) for lengths in (w8, m], (m, t]
+// and > t; counts[3] = segments of 2..w8 elements (the warp kernel's); counts[4]
+// != 0 flags a bad table.  List order is arbitrary (segments are independent).
+__global__ void __launch_bounds__(256)
+    kseg_classify(const int64_t* __restrict__ off, int64_t nseg, int64_t n, int64_t w8, int64_t m,
+                  int64_t t, int64_t* __restrict__ lm, int64_t* __restrict__ ll,
+                  int64_t* __restrict__ lx, unsigned long long* __restrict__ counts) {
+  // list capacities: a valid table has at most n / (bound + 1) such segments
+  const unsigned long long cap[3] = {(unsigned long long)(n / (w8 + 1) + 1),
+                                     (unsigned long long)(n / (m + 1) + 1),
+                                     (unsigned long long)(n / (t + 1) + 1)};
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // whole warps iterate together (ballot-aggregated small count)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < nseg;
+       base += stride) {
+    const int64_t i = base + lane;
+    bool small = false;
+    if (i < nseg) {
+      const int64_t o0 = off[i], o1 = off[i + 1], len = o1 - o0;
+      const bool bad = len < 0 || o0 < 0 || o1 > n || (i == 0 && o0 != 0) ||
+                       (i == nseg - 1 && o1 != n);
+      if (bad) atomicOr(counts + 4, 1ull);
+      small = !bad && len >= 2 && len <= w8;
+      if (!bad && len > w8) {
+        const int c = len <= m ? 0 : len <= t ? 1 : 2;
+        int64_t* l = c == 0 ? lm : c == 1 ? ll : lx;
+        const unsigned long long k = atomicAdd(counts + c, 1ull);
+        if (k < cap[c]) l[2 * k] = o0, l[2 * k + 1] = len;
+        else atomicOr(counts + 4, 1ull);  // overlapping segments: not a valid table
+      }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, small);
+    if (lane == 0 && b) atomicAdd(counts + 3, (unsigned long long)__popc(b));
+  }
+}
+
 }  // namespace msort

@@ -818,43 +818,118 @@ struct Kernels {
   static constexpr int kSegW8 = 256;  // warp classes: <= 32 (VW = 1), <= 256 (VW = 8)
   static constexpr int kSegNTM = 128, kSegVTM = 17, kSegM = kSegNTM * kSegVTM;  // CTA class
   using SegF = SegFused<K>;
+  // off: nseg + 1 offsets, in host memory (dev_off false) or device memory.
   static msort_status sort_segmented(K* keys, uint32_t* vals, const int64_t* off, size_t nseg,
-                                     void* ws, size_t ws_bytes, cudaStream_t s) {
+                                     bool dev_off, int64_t n, void* ws, size_t ws_bytes,
+                                     cudaStream_t s) {
     MSORT_TRY(init());
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
-    const int64_t n = off[nseg];
-    // One host pass over the lengths: segments of <= 256 elements are found
-    // on the device (the warp kernel reads the uploaded offsets table); the
-    // longer ones are listed here -- CTA bins (<= T) and the long segments
-    // with their K1 tiles.
-    std::vector<int64_t> mid[2], xl;  // (offset, length) pairs: <= 2176, <= T
-    int64_t k1t = 0, nsmall = 0;
-    for (size_t i = 0; i < nseg; ++i) {
-      const int64_t len = off[i + 1] - off[i];
-      if (len <= kSegW8) {
-        nsmall += len >= 2;
-        continue;
+    // ---- workspace: [ping-pong keys n][vals n][device lists][staged][done][ctr]
+    char* w = static_cast<char*>(ws);
+    char* const wend = w + ws_bytes;
+    K* wk = reinterpret_cast<K*>(w);
+    w += align_up((size_t)n * sizeof(K), 256);
+    uint32_t* wv = nullptr;
+    if (PAIRS) {
+      wv = reinterpret_cast<uint32_t*>(w);
+      w += align_up((size_t)n * 4, 256);
+    }
+    // ---- classification.  Segments of <= 256 elements are found by the warp
+    // kernel itself from the offsets table; the longer ones are listed: CTA
+    // bins (<= 2176, <= T) as (offset, length) descriptors, long segments as
+    // (offset, length) on the host (their tables are built here).
+    std::vector<int64_t> mid[2], xl;
+    const int64_t* md[2] = {nullptr, nullptr};
+    int64_t nm = 0, nl = 0, nsmall = 0;
+    if (!dev_off) {
+      for (size_t i = 0; i < nseg; ++i) {
+        const int64_t len = off[i + 1] - off[i];
+        if (len <= kSegW8) {
+          nsmall += len >= 2;
+          continue;
+        }
+        auto& v = len <= T ? mid[len <= kSegM ? 0 : 1] : xl;
+        v.push_back(off[i]);
+        v.push_back(len);
       }
-      if (len <= T) {
-        auto& m = mid[len <= kSegM ? 0 : 1];
-        m.push_back(off[i]);
-        m.push_back(len);
-      } else {
-        xl.push_back((int64_t)i);
-        k1t += (len + T - 1) / T;
+      nm = (int64_t)mid[0].size() / 2, nl = (int64_t)mid[1].size() / 2;
+    } else {
+      // on the device (kseg_classify), then one synchronisation for the
+      // counts and the long segments' list
+      const int64_t cap[3] = {n / (kSegW8 + 1) + 1, n / (kSegM + 1) + 1, n / (T + 1) + 1};
+      int64_t* lists[3];
+      for (int c = 0; c < 3; ++c) {
+        lists[c] = reinterpret_cast<int64_t*>(w);
+        w += align_up((size_t)cap[c] * 16, 256);
+      }
+      auto* counts = reinterpret_cast<unsigned long long*>(w);
+      w += 256;
+      if (w > wend) {
+        set_error("segmented sort: workspace too small");
+        return MSORT_ERROR_INVALID_VALUE;
+      }
+      MSORT_CUDA_TRY(cudaMemsetAsync(counts, 0, 5 * 8, s));
+      {
+        LaunchScope ls(KC_PARTITION, s);
+        const int64_t blocks = std::min<int64_t>(((int64_t)nseg + 255) / 256, 148 * 8);
+        kseg_classify<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
+            off, (int64_t)nseg, n, kSegW8, kSegM, T, lists[0], lists[1], lists[2], counts);
+      }
+      MSORT_CUDA_TRY(cudaGetLastError());
+      unsigned long long hc[5];
+      MSORT_CUDA_TRY(cudaMemcpyAsync(hc, counts, sizeof(hc), cudaMemcpyDeviceToHost, s));
+      MSORT_CUDA_TRY(cudaStreamSynchronize(s));
+      if (hc[4]) {
+        set_error("seg_offsets must start at 0, not decrease and end at n");
+        return MSORT_ERROR_INVALID_VALUE;
+      }
+      nsmall = (int64_t)hc[3];
+      nm = (int64_t)hc[0], nl = (int64_t)hc[1];
+      md[0] = lists[0], md[1] = lists[1];
+      xl.resize(2 * hc[2]);
+      if (hc[2]) {
+        MSORT_CUDA_TRY(cudaMemcpyAsync(xl.data(), lists[2], hc[2] * 16, cudaMemcpyDeviceToHost, s));
+        MSORT_CUDA_TRY(cudaStreamSynchronize(s));
       }
     }
-    const int64_t nxl = (int64_t)xl.size();
-    const int64_t nm = (int64_t)mid[0].size() / 2, nl = (int64_t)mid[1].size() / 2;
-    // staging layout (int64 words): the offsets table (only when there are
-    // short segments), CTA-bin descriptors, K1 tile descriptors of the long
-    // segments (even-level ones first), long-segment tables off[nxl] len[nxl]
-    // tile0[nxl+1] lev[nxl] (int32, packed)
-    const int64_t w_off = nsmall ? (int64_t)nseg + 1 : 0;
-    const int64_t w_desc = w_off + 2 * (nm + nl), w_k1 = 2 * k1t;
+    const int64_t nxl = (int64_t)xl.size() / 2;
+    // long segments: level count P_s, ordered by it (descending, stable) so
+    // that level p's segments are a prefix of the tile range
+    auto levels = [](int64_t len) {
+      const int64_t t = (len + T - 1) / T;
+      int P = 0;
+      while ((int64_t(1) << P) < t) ++P;
+      return P;
+    };
+    std::vector<int64_t> xo(nxl);
+    for (int64_t j = 0; j < nxl; ++j) xo[j] = j;
+    std::stable_sort(xo.begin(), xo.end(), [&](int64_t x, int64_t y) {
+      return levels(xl[2 * x + 1]) > levels(xl[2 * y + 1]);
+    });
+    int Pmax = 0;
+    int64_t k1t = 0, n_even_tiles = 0;
+    for (int64_t j = 0; j < nxl; ++j) {
+      const int64_t len = xl[2 * j + 1], t = (len + T - 1) / T;
+      const int P = levels(len);
+      Pmax = std::max(Pmax, P);
+      k1t += t;
+      if ((P & 1) == 0) n_even_tiles += t;
+    }
+    if (Pmax > kMaxSegLevels) {
+      set_error("segment too long");
+      return MSORT_ERROR_NOT_SUPPORTED;
+    }
+    // ---- staging (int64 words): [host offsets only: the offsets table (when
+    // there are short segments), CTA-bin descriptors] K1 tile descriptors of
+    // the long segments (even-level ones first), long-segment tables off[nxl]
+    // len[nxl] tile0[nxl+1] lev[nxl] (int32, packed)
+    const int64_t w_off = (!dev_off && nsmall) ? (int64_t)nseg + 1 : 0;
+    const int64_t w_desc = w_off + (dev_off ? 0 : 2 * (nm + nl)), w_k1 = 2 * k1t;
     const int64_t w_tab = nxl ? 3 * nxl + 1 + (nxl + 1) / 2 : 0;
     const int64_t words = w_desc + w_k1 + w_tab;
+    int64_t* dstage = reinterpret_cast<int64_t*>(w);
+    w += align_up((size_t)words * 8, 256);
     int64_t* h = nullptr;
     MSORT_TRY(staging_acquire((size_t)words * 8, reinterpret_cast<void**>(&h)));
     struct Unlock {  // early returns before staging_release
@@ -864,67 +939,36 @@ struct Kernels {
       }
     } unlock;
     if (w_off) std::memcpy(h, off, (size_t)w_off * 8);
-    if (nm) std::memcpy(h + w_off, mid[0].data(), (size_t)nm * 16);
-    if (nl) std::memcpy(h + w_off + 2 * nm, mid[1].data(), (size_t)nl * 16);
-    // long segments: level count P_s, ordered by it (descending, stable) so
-    // that level p's segments are a prefix of the tile range
-    auto levels = [](int64_t len) {
-      const int64_t t = (len + T - 1) / T;
-      int P = 0;
-      while ((int64_t(1) << P) < t) ++P;
-      return P;
-    };
-    std::stable_sort(xl.begin(), xl.end(), [&](int64_t x, int64_t y) {
-      return levels(off[x + 1] - off[x]) > levels(off[y + 1] - off[y]);
-    });
-    int Pmax = 0;
-    int64_t n_even_tiles = 0;
-    for (int64_t i : xl) {
-      const int P = levels(off[i + 1] - off[i]);
-      Pmax = std::max(Pmax, P);
-      if ((P & 1) == 0) n_even_tiles += (off[i + 1] - off[i] + T - 1) / T;
+    if (!dev_off) {
+      if (nm) std::memcpy(h + w_off, mid[0].data(), (size_t)nm * 16);
+      if (nl) std::memcpy(h + w_off + 2 * nm, mid[1].data(), (size_t)nl * 16);
+      md[0] = dstage + w_off, md[1] = dstage + w_off + 2 * nm;
     }
-    if (Pmax > kMaxSegLevels) {
-      set_error("segment too long");
-      return MSORT_ERROR_NOT_SUPPORTED;
-    }
+    int64_t ntl_all = 0;
     {
       int64_t pe = w_desc, po = w_desc + 2 * n_even_tiles;  // K1 tiles: even P_s, then odd
       int64_t* toff = h + w_desc + w_k1;
       int64_t* tlen = toff + nxl;
       int64_t* tt0 = tlen + nxl;
       int* tlev = reinterpret_cast<int*>(tt0 + nxl + 1);
-      int64_t tiles = 0;
       for (int64_t j = 0; j < nxl; ++j) {
-        const int64_t i = xl[(size_t)j], o = off[i], len = off[i + 1] - o;
+        const int64_t o = xl[2 * xo[j]], len = xl[2 * xo[j] + 1];
         const int P = levels(len);
         int64_t& pp = (P & 1) ? po : pe;
         for (int64_t t = 0; t * T < len; ++t) {
           h[pp++] = o + t * T;
           h[pp++] = std::min<int64_t>(T, len - t * T);
         }
-        toff[j] = o, tlen[j] = len, tt0[j] = tiles, tlev[j] = P;
-        tiles += (len + Tm - 1) / Tm;
+        toff[j] = o, tlen[j] = len, tt0[j] = ntl_all, tlev[j] = P;
+        ntl_all += (len + Tm - 1) / Tm;
       }
-      tt0[nxl] = tiles;
+      if (nxl) tt0[nxl] = ntl_all;
     }
-    // device workspace: [ping-pong keys n][vals n][staged words][done][ctr]
-    char* w = static_cast<char*>(ws);
-    K* wk = reinterpret_cast<K*>(w);
-    w += align_up((size_t)n * sizeof(K), 256);
-    uint32_t* wv = nullptr;
-    if (PAIRS) {
-      wv = reinterpret_cast<uint32_t*>(w);
-      w += align_up((size_t)n * 4, 256);
-    }
-    int64_t* dstage = reinterpret_cast<int64_t*>(w);
-    w += align_up((size_t)words * 8, 256);
-    const int64_t ntl_all = nxl ? h[w_desc + w_k1 + 2 * nxl + nxl] : 0;  // tile0[nxl]
     unsigned* done = reinterpret_cast<unsigned*>(w);
     w += align_up((size_t)std::max(Pmax, 1) * ntl_all * 4, 256);
     auto* ctr = reinterpret_cast<unsigned long long*>(w);
     w += 256;
-    if ((size_t)(w - static_cast<char*>(ws)) > ws_bytes) {
+    if (w > wend) {
       set_error("segmented sort: workspace too small");
       return MSORT_ERROR_INVALID_VALUE;
     }
@@ -932,16 +976,17 @@ struct Kernels {
       MSORT_CUDA_TRY(cudaMemcpyAsync(dstage, h, (size_t)words * 8, cudaMemcpyHostToDevice, s));
     unlock.held = false;
     MSORT_TRY(staging_release(s));
+    // ---- launches
     if (nsmall) {
       LaunchScope ls(KC_TILE_SORT, s);
-      kseg_warp_sort<K, PAIRS>
-          <<<(unsigned)((nseg + 3) / 4), 128, 0, s>>>(keys, vals, dstage, (int64_t)nseg);
+      kseg_warp_sort<K, PAIRS><<<(unsigned)((nseg + 3) / 4), 128, 0, s>>>(
+          keys, vals, dev_off ? off : dstage, (int64_t)nseg);
     }
     if (nm) {
       LaunchScope ls(KC_TILE_SORT, s);
       constexpr size_t sm = (size_t)kSegM * sizeof(K) + (PAIRS ? (size_t)kSegM * 8 : 0);
       k1_tile_sort<K, PAIRS, kSegNTM, kSegVTM>
-          <<<(unsigned)nm, kSegNTM, sm, s>>>(keys, vals, keys, vals, 0, dstage + w_off);
+          <<<(unsigned)nm, kSegNTM, sm, s>>>(keys, vals, keys, vals, 0, md[0]);
     }
     auto k1_desc = [&](const int64_t* d, int64_t cnt_, K* ok, uint32_t* ov) {
       LaunchScope ls(KC_TILE_SORT, s);
@@ -951,34 +996,31 @@ struct Kernels {
       else
         k1_tile_sort_keys<K, NT1, VT><<<(unsigned)cnt_, NT1, k1_smem, s>>>(keys, ok, 0, d);
     };
-    if (nl) k1_desc(dstage + w_off + 2 * nm, nl, keys, vals);
+    if (nl) k1_desc(md[1], nl, keys, vals);
     if (nxl) {
       // long segments: K1 into buffer P_s & 1, then all levels of all of them
       if (n_even_tiles) k1_desc(dstage + w_desc, n_even_tiles, keys, vals);
       if (k1t > n_even_tiles)
         k1_desc(dstage + w_desc + 2 * n_even_tiles, k1t - n_even_tiles, wk, wv);
       MSORT_CUDA_TRY(cudaGetLastError());
-      if (Pmax > 0) {
-        SegF f{};
-        f.bk[0] = keys, f.bk[1] = wk, f.bv[0] = vals, f.bv[1] = wv;
-        const int64_t* tab = dstage + w_desc + w_k1;
-        f.off = tab, f.len = tab + nxl, f.tile0 = tab + 2 * nxl;
-        f.lev = reinterpret_cast<const int*>(tab + 3 * nxl + 1);
-        f.nseg = (int)nxl, f.T = T, f.ntiles = ntl_all, f.P = Pmax, f.done = done;
-        const int64_t* htt0 = h + w_desc + w_k1 + 2 * nxl;
-        f.ch = chunk_tiles(ntl_all, dev);
-        f.grab = f.ch < kChunk ? 1 : kGrab;
-        f.cbase[0] = 0;
-        int64_t act = nxl;  // segments with more than p levels (a prefix)
-        for (int p = 0; p < Pmax; ++p) {
-          while (act > 0 && levels(off[xl[(size_t)act - 1] + 1] - off[xl[(size_t)act - 1]]) <= p)
-            --act;
-          f.ntl[p] = htt0[act];
-          f.cbase[p + 1] = f.cbase[p] + (f.ntl[p] + f.ch - 1) / f.ch;
-        }
-        MSORT_CUDA_TRY(cudaMemsetAsync(done, 0, (size_t)Pmax * ntl_all * 4 + 256, s));
-        MSORT_TRY(launch_k3(f, f.nchunks(), ctr, s, KC_MERGE));
+      SegF f{};
+      f.bk[0] = keys, f.bk[1] = wk, f.bv[0] = vals, f.bv[1] = wv;
+      const int64_t* tab = dstage + w_desc + w_k1;
+      f.off = tab, f.len = tab + nxl, f.tile0 = tab + 2 * nxl;
+      f.lev = reinterpret_cast<const int*>(tab + 3 * nxl + 1);
+      f.nseg = (int)nxl, f.T = T, f.ntiles = ntl_all, f.P = Pmax, f.done = done;
+      f.ch = chunk_tiles(ntl_all, dev);
+      f.grab = f.ch < kChunk ? 1 : kGrab;
+      f.cbase[0] = 0;
+      int64_t act = nxl;  // segments with more than p levels (a prefix of xo)
+      for (int p = 0; p < Pmax; ++p) {
+        while (act > 0 && levels(xl[2 * xo[act - 1] + 1]) <= p) --act;
+        f.ntl[p] = 0;
+        for (int64_t j = 0; j < act; ++j) f.ntl[p] += (xl[2 * xo[j] + 1] + Tm - 1) / Tm;
+        f.cbase[p + 1] = f.cbase[p] + (f.ntl[p] + f.ch - 1) / f.ch;
       }
+      MSORT_CUDA_TRY(cudaMemsetAsync(done, 0, (size_t)Pmax * ntl_all * 4 + 256, s));
+      MSORT_TRY(launch_k3(f, f.nchunks(), ctr, s, KC_MERGE));
     }
     MSORT_CUDA_TRY(cudaGetLastError());
     return MSORT_SUCCESS;
@@ -1117,23 +1159,25 @@ msort_status sort_single_dispatch(const void* in_keys, const void* in_vals, void
 }
 
 template <class K>
-static msort_status seg_k(void* keys, void* vals, const int64_t* off, size_t nseg, void* ws,
-                          size_t ws_bytes, cudaStream_t s) {
+static msort_status seg_k(void* keys, void* vals, const int64_t* off, size_t nseg, bool dev_off,
+                          int64_t n, void* ws, size_t ws_bytes, cudaStream_t s) {
   if (vals)
-    return Kernels<K, true>::sort_segmented((K*)keys, (uint32_t*)vals, off, nseg, ws, ws_bytes,
-                                            s);
-  return Kernels<K, false>::sort_segmented((K*)keys, nullptr, off, nseg, ws, ws_bytes, s);
+    return Kernels<K, true>::sort_segmented((K*)keys, (uint32_t*)vals, off, nseg, dev_off, n, ws,
+                                            ws_bytes, s);
+  return Kernels<K, false>::sort_segmented((K*)keys, nullptr, off, nseg, dev_off, n, ws, ws_bytes,
+                                           s);
 }
 
 msort_status sort_segmented_dispatch(void* keys, void* vals, const int64_t* off, size_t nseg,
-                                     msort_dtype kd, msort_dtype vd, void* ws, size_t ws_bytes,
-                                     cudaStream_t s) {
+                                     bool dev_off, size_t n, msort_dtype kd, msort_dtype vd,
+                                     void* ws, size_t ws_bytes, cudaStream_t s) {
   if (vd == MSORT_NONE) vals = nullptr;
+  const int64_t nn = (int64_t)n;
   switch (kd) {
-    case MSORT_INT32: return seg_k<int32_t>(keys, vals, off, nseg, ws, ws_bytes, s);
-    case MSORT_UINT32: return seg_k<uint32_t>(keys, vals, off, nseg, ws, ws_bytes, s);
-    case MSORT_INT64: return seg_k<int64_t>(keys, vals, off, nseg, ws, ws_bytes, s);
-    case MSORT_UINT64: return seg_k<uint64_t>(keys, vals, off, nseg, ws, ws_bytes, s);
+    case MSORT_INT32: return seg_k<int32_t>(keys, vals, off, nseg, dev_off, nn, ws, ws_bytes, s);
+    case MSORT_UINT32: return seg_k<uint32_t>(keys, vals, off, nseg, dev_off, nn, ws, ws_bytes, s);
+    case MSORT_INT64: return seg_k<int64_t>(keys, vals, off, nseg, dev_off, nn, ws, ws_bytes, s);
+    case MSORT_UINT64: return seg_k<uint64_t>(keys, vals, off, nseg, dev_off, nn, ws, ws_bytes, s);
     default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
   }
 }

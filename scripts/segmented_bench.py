@@ -46,14 +46,16 @@ for L, rand in ((16, False), (32, True), (100, False), (256, False), (256, True)
             lens = np.append(lens, n - lens.sum())
     off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     assert off[-1] == n
-    for pairs in (False, True):
+    off_dev = torch.from_numpy(off).cuda()
+    for pairs, dev in ((False, False), (True, False), (False, True), (True, True)):
         k = base.clone()
         v = torch.arange(n, dtype=torch.int32, device="cuda") if pairs else None
         v0 = v.clone() if pairs else None
         nb = ms.msort_segmented_workspace_bytes(n, off.size - 1, ms.MSORT_INT32,
                                                 ms.MSORT_UINT32 if pairs else ms.MSORT_NONE)
         ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
-        ms.msort_sort_segmented(k, off, v, ws=ws)
+        offs = off_dev if dev else off
+        ms.msort_sort_segmented(k, offs, v, ws=ws)
         torch.cuda.synchronize()
         ts, hs = [], []
         for _ in range(a.reps):
@@ -64,7 +66,7 @@ for L, rand in ((16, False), (32, True), (100, False), (256, False), (256, True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
             h0 = time.perf_counter()
-            ms.msort_sort_segmented(k, off, v, ws=ws)
+            ms.msort_sort_segmented(k, offs, v, ws=ws)
             hs.append((time.perf_counter() - h0) * 1e3)
             e1.record()
             e1.synchronize()
@@ -76,7 +78,8 @@ for L, rand in ((16, False), (32, True), (100, False), (256, False), (256, True)
             ok &= bool((s[1:] >= s[:-1]).all()) if s.numel() > 1 else True
         rec = 4 + (4 if pairs else 0)
         print(json.dumps({"seg_len": ("uniform 1.." if rand else "") + str(L), "nseg": int(off.size - 1),
-                          "n": n, "pairs": pairs, "ms": round(med, 4),
+                          "n": n, "pairs": pairs,
+                          "offsets": "device" if dev else "host", "ms": round(med, 4),
                           "host_enqueue_ms": round(statistics.median(hs), 4),
                           "gkeys_s": round(n / med / 1e6, 2),
                           "hbm_floor_frac": round(2 * n * rec / (med / 1e3) / 1e9 / peak, 3),

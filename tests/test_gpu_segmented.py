@@ -26,11 +26,12 @@ def ms():
     return m
 
 
-def _run(ms, orc, k, off, pairs):
+def _run(ms, orc, k, off, pairs, dev_off=False):
     v = mi.index_payload(k.size) if pairs else None
     kd = to_dev(k)
     vd = to_dev(v) if pairs else None
-    ms.msort_sort_segmented(kd, off, vd)
+    o = torch.as_tensor(np.asarray(off, dtype=np.int64)).cuda() if dev_off else off
+    ms.msort_sort_segmented(kd, o, vd)
     torch.cuda.synchronize()
     if pairs:
         ek, ev = orc.sort_segmented(k, off, v)
@@ -54,22 +55,24 @@ def _edges(ms, dtype, pairs):
 @pytest.mark.parametrize("dtype", [np.int32, np.uint32, np.int64, np.uint64])
 @pytest.mark.parametrize("pairs", [False, True])
 @pytest.mark.parametrize("dist", ["rand", "dup"])
-def test_segment_bins(ms, orc, dtype, pairs, dist):
+@pytest.mark.parametrize("dev_off", [False, True])
+def test_segment_bins(ms, orc, dtype, pairs, dist, dev_off):
     lens = _edges(ms, dtype, pairs)
     off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     k = _keys(int(off[-1]), 11, dist, dtype)
-    _run(ms, orc, k, off, pairs)
+    _run(ms, orc, k, off, pairs, dev_off)
 
 
 @pytest.mark.parametrize("dtype", [np.int32, np.int64])
 @pytest.mark.parametrize("pairs", [False, True])
-def test_many_small_segments(ms, orc, dtype, pairs):
+@pytest.mark.parametrize("dev_off", [False, True])
+def test_many_small_segments(ms, orc, dtype, pairs, dev_off):
     """20000 segments of 0..300 elements (the warp bins, many CTAs of 4 warps)."""
     rng = np.random.default_rng(3)
     lens = rng.integers(0, 301, 20000)
     off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     k = _keys(int(off[-1]), 12, "dup", dtype)
-    _run(ms, orc, k, off, pairs)
+    _run(ms, orc, k, off, pairs, dev_off)
 
 
 @pytest.mark.parametrize("dist", ["eq", "asc", "desc", "ext"])
@@ -117,11 +120,22 @@ def test_empty_and_invalid(ms):
         ms.msort_sort_segmented(x, [0, 6, 5, 10])
     with pytest.raises(ms.MsortError):
         ms.msort_sort_segmented(x, [0, 9])
+    # device tables are checked on the device, before any key moves
+    x0 = x.clone()
+    for bad in ([0, 6, 5, 10], [0, 9], [1, 10], [0, 300, 0, 10]):
+        with pytest.raises(ms.MsortError):
+            ms.msort_sort_segmented(x, torch.tensor(bad, dtype=torch.int64, device="cuda"))
+        assert torch.equal(x, x0)
+    y = torch.randint(0, 1 << 30, (5000,), dtype=torch.int32, device="cuda")
+    bad = torch.tensor([0] + [300, 0] * 20 + [5000], dtype=torch.int64, device="cuda")
+    with pytest.raises(ms.MsortError):  # overlapping segments would overflow the lists
+        ms.msort_sort_segmented(y, bad)
 
 
 @pytest.mark.parametrize("dtype", [np.int32, np.uint32, np.int64])
 @pytest.mark.parametrize("pairs", [False, True])
-def test_many_long_segments(ms, orc, dtype, pairs):
+@pytest.mark.parametrize("dev_off", [False, True])
+def test_many_long_segments(ms, orc, dtype, pairs, dev_off):
     """Segments longer than a tile with 1..6 merge levels (both buffer
     parities) mixed with short ones: one fused merge launch over all of them."""
     rng = np.random.default_rng(21)
@@ -130,7 +144,7 @@ def test_many_long_segments(ms, orc, dtype, pairs):
     rng.shuffle(lens)
     off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     k = _keys(int(off[-1]), 22, "dup" if pairs else "rand", dtype)
-    _run(ms, orc, k, off, pairs)
+    _run(ms, orc, k, off, pairs, dev_off)
 
 
 def test_segmented_repeat_and_streams(ms, orc):
