@@ -76,7 +76,10 @@ typedef struct msort_comm_s *msort_comm_t;
 
 /* Stable ascending sort of keys[0..n) in place.  Workspace of
  * msort_workspace_bytes(n, key_dtype, MSORT_NONE, 1) bytes is taken with
- * cudaMallocAsync/cudaFreeAsync on `stream`. */
+ * cudaMallocAsync/cudaFreeAsync on `stream`, from the device's default memory
+ * pool; the library raises that pool's release threshold once (its freed
+ * blocks stay reserved for the next call; cudaMemPoolTrimTo returns them).
+ * The same holds for every call that allocates scratch itself. */
 msort_status msort_sort(void *keys, size_t n, msort_dtype key_dtype, msort_stream_t stream);
 
 /* Stable ascending sort of (keys, vals) pairs by key; vals travel with their
@@ -213,6 +216,40 @@ msort_status msort_sort_distributed_emulated(void *const *keys, void *const *val
                                              void *const *ws, size_t ws_bytes,
                                              msort_stream_t stream,
                                              int64_t *split_matrix_out);
+
+/* The paper's own distribution, as an output mode:
+ * rank-tree gather to rank 0 (the loop of fig. mpi-merge-code).
+ * Every rank sorts its shard (in_keys/in_vals, read only); then, while more
+ * than one rank is active, the upper half of the active ranks send their
+ * sorted arrays to rank - split over NCCL (NVLink) and the lower half merge
+ * their own array with the received one (merge() of P:516: the parent's own
+ * elements first on ties).  Rank 0 ends with all sum(n_local) elements in
+ * root_keys/root_vals (root_capacity elements available there; other ranks
+ * may pass NULL and 0).  Ties therefore come out in the TREE's rank order --
+ * for p = 2^k the bit-reversed rank order (0, 4, 2, 6, 1, 5, 3, 7 at p = 8),
+ * not the balanced call's natural order.  p is any world size: the paper's
+ * split = p / 2 halving for powers of two, ceil(active / 2) parents otherwise.
+ * Collective; synchronises once (the shard sizes); buffers are allocated on
+ * `stream` (cudaMallocAsync) and freed when the call's work completes.
+ * *total_out (host, may be NULL) receives sum(n_local).  Errors: as
+ * msort_sort_distributed, INVALID_VALUE when root_capacity is too small. */
+msort_status msort_sort_distributed_tree(const void *in_keys, const void *in_vals, size_t n_local,
+                                         msort_dtype key_dtype, msort_dtype val_dtype,
+                                         msort_comm_t comm, void *root_keys, void *root_vals,
+                                         size_t root_capacity, msort_stream_t stream,
+                                         int64_t *total_out);
+
+/* Single-process emulation of msort_sort_distributed_tree for `world`
+ * virtual ranks on the current device (device-to-device copies instead of
+ * NCCL send/recv): shards keys[r], vals[r] (host arrays of device pointers,
+ * read only), n_local[r]; root_keys/root_vals receive sum(n_local).
+ * Asynchronous on `stream`. */
+msort_status msort_sort_distributed_tree_emulated(const void *const *keys,
+                                                  const void *const *vals,
+                                                  const size_t *n_local, int world,
+                                                  msort_dtype key_dtype, msort_dtype val_dtype,
+                                                  void *root_keys, void *root_vals,
+                                                  msort_stream_t stream);
 
 /* --------------------------------------------- splitter planning (host side)
  * The host-side arithmetic of the splitter co-rank, the same

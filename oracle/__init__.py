@@ -123,6 +123,46 @@ def merge(a, b, av=None, bv=None):
     return out if not withv else (out, outv)
 
 
+def sort_tree(shards, vals=None):
+    """The paper's MPI merge (fig. mpi-merge-code) run literally on
+    host arrays: every rank's array sorted (the subsort), then
+        split = size / 2
+        while split >= 1:
+            ranks in [split, 2 split) send `local` to rank - split;
+            ranks < split: local = merge(local, received)   (P:516)
+            split = split / 2
+    Rank 0's final array is returned (keys, or (keys, vals)).  For world sizes
+    that are not powers of two the halving keeps ceil(active / 2) parents with
+    the same pairing rank <- rank + split (reading R13)."""
+    local = [sort(np.asarray(k)) if vals is None else sort(np.asarray(k), np.asarray(v))
+             for k, v in zip(shards, vals if vals is not None else [None] * len(shards))]
+    active = len(local)
+    while active > 1:
+        split = (active + 1) // 2  # = size / 2 when active is a power of two
+        for rank in range(active - split):
+            child = rank + split
+            if vals is None:
+                local[rank] = merge(local[rank], local[child])
+            else:
+                local[rank] = merge(local[rank][0], local[child][0], local[rank][1],
+                                    local[child][1])
+        active = split
+    return local[0]
+
+
+def tree_rank_order(p: int) -> list:
+    """The order in which sort_tree's merges leave the ranks' elements among
+    equal keys: rank 0's parent-first merges concatenate subtrees."""
+    order = [[r] for r in range(p)]
+    active = p
+    while active > 1:
+        split = (active + 1) // 2
+        for rank in range(active - split):
+            order[rank] = order[rank] + order[rank + split]
+        active = split
+    return order[0]
+
+
 def split_matrix(shards) -> np.ndarray:
     """(p+1) x p reference split matrix of the distributed sort (reading R10/R11)."""
     p = len(shards)

@@ -43,6 +43,7 @@ EXPORTED = (
     "msort_profile_enable", "msort_profile_reset", "msort_profile_read", "msort_launch_count",
     "msort_tile_size", "msort_debug_set_quad", "msort_sort_host", "msort_debug_set_exchange",
     "msort_segmented_workspace_bytes", "msort_sort_segmented",
+    "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
 )
 
 
@@ -92,6 +93,10 @@ def _load():
                                                   c.POINTER(c.c_size_t)]
     L.msort_sort_segmented.argtypes = [c.c_void_p, c.c_void_p, c.c_size_t, i64p, c.c_size_t, i32,
                                        i32, c.c_void_p, c.c_size_t, c.c_void_p]
+    L.msort_sort_distributed_tree.argtypes = [vp, vp, sz, i32, i32, vp, vp, vp, sz, vp, i64p]
+    L.msort_sort_distributed_tree_emulated.argtypes = [c.POINTER(vp), c.POINTER(vp),
+                                                       c.POINTER(c.c_size_t), i32, i32, i32, vp,
+                                                       vp, vp]
     L.msort_tile_size.argtypes = [i32, i32]
     L.msort_tile_size.restype = i32
     for f in ("msort_sort", "msort_sort_pairs", "msort_workspace_bytes", "msort_sort_ws",
@@ -100,7 +105,8 @@ def _load():
               "msort_sort_distributed", "msort_sort_distributed_ws",
               "msort_sort_distributed_emulated", "msort_plan_init", "msort_plan_candidates",
               "msort_plan_narrow", "msort_plan_fill", "msort_profile_read",
-              "msort_segmented_workspace_bytes", "msort_sort_segmented"):
+              "msort_segmented_workspace_bytes", "msort_sort_segmented",
+              "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated"):
         getattr(L, f).restype = i32
     return L
 
@@ -395,6 +401,57 @@ def msort_sort_distributed_emulated(keys: list, vals: list | None = None, stream
             split.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
             "msort_sort_distributed_emulated")
     return split.reshape(p + 1, p)
+
+
+def msort_sort_distributed_tree(in_keys: torch.Tensor, comm: Comm, in_vals=None,
+                                root_keys: torch.Tensor | None = None, root_vals=None,
+                                stream=None):
+    """The paper's rank-tree gather (include/msort.h msort_sort_distributed_tree):
+    collective; rank 0 receives every rank's keys, sorted, in root_keys (allocated
+    here with the global size when None).  Returns (root_keys, root_vals) on rank 0,
+    (None, None) elsewhere.  Ties come out in the tree's rank order."""
+    import torch.distributed as dist
+
+    _check_tensor(in_keys, "in_keys")
+    n = in_keys.numel()
+    kd, vd = _dt(in_keys), _vdt(in_vals)
+    t = torch.tensor([n], dtype=torch.int64, device=in_keys.device)
+    dist.all_reduce(t)  # every rank: the global size
+    total = int(t.item())
+    if comm.rank == 0 and root_keys is None:
+        root_keys = torch.empty(total, dtype=in_keys.dtype, device=in_keys.device)
+        if in_vals is not None:
+            root_vals = torch.empty(total, dtype=in_vals.dtype, device=in_keys.device)
+    cap = root_keys.numel() if root_keys is not None else 0
+    tot = ctypes.c_int64()
+    with torch.cuda.device(in_keys.device):
+        _check(lib.msort_sort_distributed_tree(
+            _ptr(in_keys), _ptr(in_vals), n, kd, vd, comm.handle, _ptr(root_keys),
+            _ptr(root_vals), cap, ctypes.c_void_p(_stream(stream)), ctypes.byref(tot)),
+            "msort_sort_distributed_tree")
+    return (root_keys, root_vals) if comm.rank == 0 else (None, None)
+
+
+def msort_sort_distributed_tree_emulated(keys: list, vals: list | None = None, stream=None):
+    """The rank-tree gather for p virtual ranks on one GPU: returns the root's
+    (keys, vals) -- every shard's elements, sorted, ties in the tree's rank order."""
+    p = len(keys)
+    for k in keys:
+        _check_tensor(k, "keys")
+    kd = _dt(keys[0])
+    vd = _vdt(vals[0]) if vals else MSORT_NONE
+    total = sum(k.numel() for k in keys)
+    rk = torch.empty(total, dtype=keys[0].dtype, device=keys[0].device)
+    rv = torch.empty(total, dtype=vals[0].dtype, device=keys[0].device) if vals else None
+    VP = ctypes.c_void_p * p
+    kp = VP(*[k.data_ptr() for k in keys])
+    vp = VP(*[v.data_ptr() for v in vals]) if vals else None
+    np_ = (ctypes.c_size_t * p)(*[k.numel() for k in keys])
+    with torch.cuda.device(keys[0].device):
+        _check(lib.msort_sort_distributed_tree_emulated(
+            kp, vp, np_, p, kd, vd, _ptr(rk), _ptr(rv), ctypes.c_void_p(_stream(stream))),
+            "msort_sort_distributed_tree_emulated")
+    return rk, rv
 
 
 # --------------------------------------------------- planning (host side)

@@ -16,6 +16,9 @@ namespace msort {
 msort_status dist_nccl(const void* in_keys, const void* in_vals, void* keys, void* vals, size_t n,
                        msort_dtype kd, msort_dtype vd, msort_comm_s* comm, void* ws,
                        cudaStream_t s, int64_t* split_out);
+msort_status tree_nccl(const void* in_keys, const void* in_vals, size_t n, msort_dtype kd,
+                       msort_dtype vd, msort_comm_s* comm, void* root_k, void* root_v,
+                       size_t root_cap, cudaStream_t s, int64_t* total_out);
 msort_status dist_emulated(void* const* keys, void* const* vals, const size_t* n, int world,
                            msort_dtype kd, msort_dtype vd, void* const* ws, cudaStream_t s,
                            int64_t* split_out);
@@ -72,6 +75,23 @@ LaunchScope::~LaunchScope() {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaEventRecord(g_pending[slot].b, s);
   }
+}
+
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static bool done[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && !done[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    (void)cudaGetLastError();
+    done[dev] = true;
+  }
+  return cudaMallocAsync(p, bytes, s);
 }
 
 // ------------------------------------------------------------- helpers
@@ -195,7 +215,7 @@ static msort_status sort_alloc(void* keys, void* vals, size_t n, msort_dtype kd,
   MSORT_TRY(check_device());
   size_t need = single_ws_bytes(n, kd, vd);
   void* ws = nullptr;
-  MSORT_CUDA_TRY(cudaMallocAsync(&ws, need, s));
+  MSORT_CUDA_TRY(scratch_alloc(&ws, need, s));
   msort_status st = sort_single_dispatch(keys, vals, keys, vals, n, kd, vd, ws, need, s);
   cudaError_t e = cudaFreeAsync(ws, s);
   if (st != MSORT_SUCCESS) return st;
@@ -444,13 +464,55 @@ msort_status msort_sort_distributed(void* keys, void* vals, size_t n_local,
   cudaStream_t s = (cudaStream_t)stream;
   size_t need = dist_ws_bytes(n_local, key_dtype, val_dtype, comm_world(comm));
   void* ws = nullptr;
-  MSORT_CUDA_TRY(cudaMallocAsync(&ws, need, s));
+  MSORT_CUDA_TRY(scratch_alloc(&ws, need, s));
   msort_status st = dist_nccl(keys, vals, keys, vals, n_local, key_dtype, val_dtype, comm, ws, s,
                               split_matrix_out);
   cudaError_t e = cudaFreeAsync(ws, s);
   if (st != MSORT_SUCCESS) return st;
   if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
   return MSORT_SUCCESS;
+}
+
+msort_status msort_sort_distributed_tree(const void* in_keys, const void* in_vals, size_t n_local,
+                                         msort_dtype key_dtype, msort_dtype val_dtype,
+                                         msort_comm_t comm, void* root_keys, void* root_vals,
+                                         size_t root_capacity, msort_stream_t stream,
+                                         int64_t* total_out) {
+  if (!comm) {
+    set_error("comm is NULL");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  if (val_dtype == MSORT_NONE) in_vals = nullptr, root_vals = nullptr;
+  MSORT_TRY(validate(const_cast<void*>(in_keys), const_cast<void*>(in_vals), n_local, key_dtype,
+                     val_dtype, false));
+  MSORT_TRY(validate(root_keys, root_vals, root_capacity, key_dtype, val_dtype, false));
+  MSORT_TRY(check_device());
+  return tree_nccl(in_keys, in_vals, n_local, key_dtype, val_dtype, comm, root_keys, root_vals,
+                   root_capacity, (cudaStream_t)stream, total_out);
+}
+
+msort_status msort_sort_distributed_tree_emulated(const void* const* keys,
+                                                  const void* const* vals,
+                                                  const size_t* n_local, int world,
+                                                  msort_dtype key_dtype, msort_dtype val_dtype,
+                                                  void* root_keys, void* root_vals,
+                                                  msort_stream_t stream) {
+  if (!keys || !n_local || world < 1 || world > 1024 || (val_dtype != MSORT_NONE && !vals)) {
+    set_error("bad argument to msort_sort_distributed_tree_emulated");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  if (val_dtype == MSORT_NONE) vals = nullptr, root_vals = nullptr;
+  size_t total = 0;
+  for (int r = 0; r < world; ++r) {
+    MSORT_TRY(validate(const_cast<void*>(keys[r]), vals ? const_cast<void*>(vals[r]) : nullptr,
+                       n_local[r], key_dtype, val_dtype, false));
+    total += n_local[r];
+  }
+  MSORT_TRY(validate(root_keys, root_vals, total, key_dtype, val_dtype, false));
+  if (total == 0) return MSORT_SUCCESS;
+  MSORT_TRY(check_device());
+  return tree_emulated(keys, vals, n_local, world, key_dtype, val_dtype, root_keys, root_vals,
+                       (cudaStream_t)stream);
 }
 
 msort_status msort_sort_distributed_emulated(void* const* keys, void* const* vals,

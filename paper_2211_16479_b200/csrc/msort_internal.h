@@ -53,6 +53,13 @@ struct Geometry {
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// The library's own scratch allocations (the calls without a caller
+// workspace): stream-ordered from the current device's default memory pool,
+// whose release threshold is raised once so freed blocks are reused by the
+// next call instead of being unmapped and mapped again (cudaMemPoolTrimTo on
+// that pool hands them back).
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
+
 size_t dtype_size(msort_dtype d);
 int tile_size_for(msort_dtype kd, msort_dtype vd);
 
@@ -65,6 +72,9 @@ size_t dist_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd, int world);
 
 // Single-GPU sort with explicit workspace (sort_single.cu): sorts in_keys/
 // in_vals into keys/vals (the same pointers for an in-place sort).
+msort_status tree_emulated(const void* const* keys, const void* const* vals, const size_t* n,
+                           int world, msort_dtype kd, msort_dtype vd, void* root_k, void* root_v,
+                           cudaStream_t s);
 msort_status sort_segmented_dispatch(void* keys, void* vals, const int64_t* off, size_t nseg,
                                      bool dev_off, size_t n, msort_dtype kd, msort_dtype vd,
                                      void* ws, size_t ws_bytes, cudaStream_t s);

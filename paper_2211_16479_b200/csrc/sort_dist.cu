@@ -632,6 +632,207 @@ msort_status dist_emulated(void* const* keys, void* const* vals, const size_t* n
   return dist_run(C, io.data(), world, kd, vd, s, split_out, exchange_mode() == 1 && world > 1);
 }
 
+// ------------------------------------------------ rank-tree gather (f4)
+// The paper's own distribution (fig. mpi-merge-code): every rank
+// sorts its shard; then, while more than one rank is active, the upper half
+// of the active ranks (right children) send their sorted arrays to rank -
+// split and the lower half (left children / parents) merge their own array
+// (left, first on ties: merge() of P:516) with the received one.  Rank 0 ends
+// with everything.  `split` = active / 2 for the paper's power-of-two worlds
+// (P:402); other worlds use ceil(active / 2) parents, the same pairing
+// rank <- rank + split with an odd rank out (R12/R13).
+// Order of the shards after the tree (ties resolve in this order).
+static void tree_rounds(int p, std::vector<std::vector<std::pair<int, int>>>& rounds) {
+  rounds.clear();
+  int active = p;
+  while (active > 1) {
+    const int split = (active + 1) / 2;
+    std::vector<std::pair<int, int>> r;  // (parent, child)
+    for (int c = split; c < active; ++c) r.push_back({c - split, c});
+    rounds.push_back(r);
+    active = split;
+  }
+}
+
+struct TreeBufs {
+  void *ak, *av, *bk, *bv;  // [own | received] and the merge target
+  void* part;               // K3 scheduler counters
+  int64_t cnt;              // elements currently held
+};
+
+// Collective-specific pieces of the tree: NCCL send/recv, or device copies
+// between the virtual ranks' buffers.
+struct TreeNccl {
+  msort_comm_s* c;
+  cudaStream_t s;
+  msort_status move(std::vector<TreeBufs>& tb, int parent, int child, int64_t cnt, msort_dtype kd,
+                    msort_dtype vd) {
+    const int me = c->rank;
+    if (me != parent && me != child) return MSORT_SUCCESS;
+    TreeBufs& b = tb[0];
+    const size_t wk = dtype_size(kd);
+    LaunchScope ls(KC_EXCHANGE, s);
+    MSORT_NCCL_TRY(ncclGroupStart());
+    if (me == child) {
+      MSORT_NCCL_TRY(ncclSend(b.ak, (size_t)cnt, nccl_type(kd), parent, c->comm, s));
+      if (vd != MSORT_NONE)
+        MSORT_NCCL_TRY(ncclSend(b.av, (size_t)cnt, ncclUint32, parent, c->comm, s));
+    } else {
+      MSORT_NCCL_TRY(ncclRecv((char*)b.ak + b.cnt * wk, (size_t)cnt, nccl_type(kd), child,
+                              c->comm, s));
+      if (vd != MSORT_NONE)
+        MSORT_NCCL_TRY(ncclRecv((char*)b.av + b.cnt * 4, (size_t)cnt, ncclUint32, child, c->comm,
+                                s));
+    }
+    MSORT_NCCL_TRY(ncclGroupEnd());
+    return MSORT_SUCCESS;
+  }
+  int local(int rank) const { return rank == c->rank ? 0 : -1; }
+};
+struct TreeEmul {
+  cudaStream_t s;
+  msort_status move(std::vector<TreeBufs>& tb, int parent, int child, int64_t cnt, msort_dtype kd,
+                    msort_dtype vd) {
+    const size_t wk = dtype_size(kd);
+    LaunchScope ls(KC_EXCHANGE, s);
+    MSORT_CUDA_TRY(cudaMemcpyAsync((char*)tb[parent].ak + tb[parent].cnt * wk, tb[child].ak,
+                                   cnt * wk, cudaMemcpyDeviceToDevice, s));
+    if (vd != MSORT_NONE)
+      MSORT_CUDA_TRY(cudaMemcpyAsync((char*)tb[parent].av + tb[parent].cnt * 4, tb[child].av,
+                                     cnt * 4, cudaMemcpyDeviceToDevice, s));
+    return MSORT_SUCCESS;
+  }
+  int local(int rank) const { return rank; }
+};
+
+// ranks: the global ranks this process drives (one for NCCL, all for the
+// emulation); in_k/in_v per driven rank; nall: every rank's shard size.
+template <class Coll>
+static msort_status tree_run(Coll& C, const std::vector<int>& ranks,
+                             const std::vector<const void*>& in_k,
+                             const std::vector<const void*>& in_v,
+                             const std::vector<int64_t>& nall, msort_dtype kd, msort_dtype vd,
+                             void* root_k, void* root_v, cudaStream_t s) {
+  const int p = (int)nall.size();
+  const size_t wk = dtype_size(kd);
+  const bool pairs = vd != MSORT_NONE;
+  std::vector<std::vector<std::pair<int, int>>> rounds;
+  tree_rounds(p, rounds);
+  // subtree sizes: what each parent will hold at most
+  std::vector<int64_t> sub(nall);
+  for (auto& r : rounds)
+    for (auto& pc : r) sub[pc.first] += sub[pc.second];
+  std::vector<TreeBufs> tb(ranks.size());
+  std::vector<void*> allocs;
+  auto alloc = [&](size_t bytes) -> void* {
+    void* q = nullptr;
+    if (scratch_alloc(&q, std::max<size_t>(bytes, 256), s) != cudaSuccess) return nullptr;
+    allocs.push_back(q);
+    return q;
+  };
+  struct Freer {
+    std::vector<void*>* a;
+    cudaStream_t s;
+    ~Freer() {
+      for (void* q : *a) cudaFreeAsync(q, s);
+    }
+  } freer{&allocs, s};
+  for (size_t l = 0; l < ranks.size(); ++l) {
+    const int r = ranks[l];
+    const size_t cap = (size_t)sub[r];
+    TreeBufs& b = tb[l];
+    b.ak = alloc(cap * wk), b.bk = alloc(cap * wk);
+    b.av = pairs ? alloc(cap * 4) : nullptr, b.bv = pairs ? alloc(cap * 4) : nullptr;
+    b.part = alloc(4096);
+    void* sws = alloc(single_ws_bytes((size_t)nall[r], kd, vd));
+    if (!b.ak || !b.bk || (pairs && (!b.av || !b.bv)) || !b.part || !sws) {
+      set_error("tree sort: out of device memory");
+      return MSORT_ERROR_OUT_OF_MEMORY;
+    }
+    // D1: the local sort (the paper's subsort), into [own | ...]
+    MSORT_TRY(sort_single_dispatch(in_k[l], pairs ? in_v[l] : nullptr, b.ak, b.av,
+                                   (size_t)nall[r], kd, vd, sws,
+                                   single_ws_bytes((size_t)nall[r], kd, vd), s));
+    b.cnt = nall[r];
+  }
+  std::vector<int64_t> cnt(nall);  // every rank's count, tracked on every process
+  for (size_t t = 0; t < rounds.size(); ++t) {
+    const bool last = t + 1 == rounds.size();
+    for (auto& pc : rounds[t]) {
+      const int parent = pc.first, child = pc.second;
+      if (cnt[child] > 0) MSORT_TRY(C.move(tb, parent, child, cnt[child], kd, vd));
+      const int lp = C.local(parent);
+      // nothing received: nothing to merge, except that the root's last round
+      // writes the output
+      if (lp >= 0 && (cnt[child] > 0 || (last && parent == 0))) {
+        // merge(local, tmp) -> result: runs [0, own) and [own, own + recv)
+        TreeBufs& b = tb[(size_t)lp];
+        const int64_t off[3] = {0, cnt[parent], cnt[parent] + cnt[child]};
+        void* dk = (last && parent == 0) ? root_k : b.bk;
+        void* dv = (last && parent == 0) ? root_v : b.bv;
+        MSORT_TRY(kway_merge_dispatch(b.ak, b.av, b.bk, b.bv, dk, dv, off, 2, kd, vd, b.part, s));
+        if (!(last && parent == 0)) std::swap(b.ak, b.bk), std::swap(b.av, b.bv);
+        b.cnt = off[2];
+      }
+      cnt[parent] += cnt[child];
+    }
+  }
+  const int l0 = C.local(0);
+  if (rounds.empty() && l0 >= 0 && nall[0] > 0) {  // one rank: the sorted shard is the result
+    MSORT_CUDA_TRY(cudaMemcpyAsync(root_k, tb[(size_t)l0].ak, nall[0] * wk,
+                                   cudaMemcpyDeviceToDevice, s));
+    if (pairs)
+      MSORT_CUDA_TRY(cudaMemcpyAsync(root_v, tb[(size_t)l0].av, nall[0] * 4,
+                                     cudaMemcpyDeviceToDevice, s));
+  }
+  // the buffers are freed on the stream (stream-ordered) by the Freer
+  return MSORT_SUCCESS;
+}
+
+msort_status tree_nccl(const void* in_keys, const void* in_vals, size_t n, msort_dtype kd,
+                       msort_dtype vd, msort_comm_s* comm, void* root_k, void* root_v,
+                       size_t root_cap, cudaStream_t s, int64_t* total_out) {
+  const int p = comm->world;
+  // every rank's size (one allgather, one host sync)
+  uint64_t* d = nullptr;
+  MSORT_CUDA_TRY(scratch_alloc((void**)&d, 8 * (size_t)(p + 1), s));
+  std::vector<uint64_t> hn((size_t)p);
+  uint64_t mine = n;
+  cudaError_t e = cudaMemcpyAsync(d + p, &mine, 8, cudaMemcpyHostToDevice, s);
+  ncclResult_t nr = e == cudaSuccess ? ncclAllGather(d + p, d, 1, ncclUint64, comm->comm, s)
+                                     : ncclSuccess;
+  if (e == cudaSuccess && nr == ncclSuccess)
+    e = cudaMemcpyAsync(hn.data(), d, 8 * (size_t)p, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && nr == ncclSuccess) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(d, s);
+  if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather (tree sizes)");
+  if (e != cudaSuccess) return cuda_fail(e, "tree sizes");
+  std::vector<int64_t> nall(hn.begin(), hn.end());
+  int64_t total = 0;
+  for (int64_t v : nall) total += v;
+  if (total_out) *total_out = total;
+  if (comm->rank == 0 && (size_t)total > root_cap) {
+    set_error("tree sort: root output holds " + std::to_string(root_cap) + " elements, need " +
+              std::to_string(total));
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  TreeNccl C{comm, s};
+  return tree_run(C, {comm->rank}, {in_keys}, {in_vals}, nall, kd, vd, root_k, root_v, s);
+}
+
+msort_status tree_emulated(const void* const* keys, const void* const* vals, const size_t* n,
+                           int world, msort_dtype kd, msort_dtype vd, void* root_k, void* root_v,
+                           cudaStream_t s) {
+  std::vector<int> ranks(world);
+  std::vector<const void*> ik(world), iv(world);
+  std::vector<int64_t> nall(world);
+  for (int r = 0; r < world; ++r) {
+    ranks[r] = r, ik[r] = keys[r], iv[r] = vals ? vals[r] : nullptr, nall[r] = (int64_t)n[r];
+  }
+  TreeEmul C{s};
+  return tree_run(C, ranks, ik, iv, nall, kd, vd, root_k, root_v, s);
+}
+
 static int g_exchange_mode = -1;
 int exchange_mode() {
   if (g_exchange_mode < 0) {

@@ -1,5 +1,7 @@
 """Distributed sort in the one-GPU emulation (p virtual ranks, same kernels):
-time per call for both exchange modes (include/msort.h msort_debug_set_exchange).
+time per call for both exchange modes (include/msort.h msort_debug_set_exchange)
+and for the paper's rank-tree gather to rank 0 (msort_sort_distributed_tree,
+mode "tree": the root ends with all p * n keys).
 
     python scripts/dist_emul_bench.py [--log2n 26] [--ps 2,4,8] [--reps 5]
 All p ranks run on one GPU in sequence, so the time is p x (one rank's work)
@@ -49,5 +51,22 @@ for p in [int(x) for x in a.ps.split(",")]:
                           "sorted": ok}), flush=True)
         del kd
     ms.set_exchange_mode(0)
+    # the paper's rank-tree gather (all data ends on the root)
+    ts = []
+    for rep in range(a.reps + 2):
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rk, _ = ms.msort_sort_distributed_tree_emulated(src)
+        e1.record()
+        e1.synchronize()
+        if rep >= 2:
+            ts.append(e0.elapsed_time(e1))
+    ok = bool((rk[1:] >= rk[:-1]).all())
+    med = statistics.median(ts)
+    print(json.dumps({"p": p, "n_per_rank": n, "mode": "tree", "ms_all_ranks": round(med, 3),
+                      "ms_per_rank": round(med / p, 3), "sorted": ok}), flush=True)
+    del rk
     del src
     torch.cuda.empty_cache()

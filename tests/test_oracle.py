@@ -299,3 +299,36 @@ def test_segmented_definition(orc, dtype):
     assert np.array_equal(orc.sort_segmented(k, off), k[perm])
     # one segment = the plain sort
     assert np.array_equal(orc.sort_segmented(k, [0, n]), orc.sort(k))
+
+
+def test_tree_rank_order_closed_form(orc):
+    """For p = 2^k the paper's tree leaves ties in bit-reversed rank
+    order (SURVEY ledger L11); p = 1 and p = 2 are the identity."""
+    assert orc.tree_rank_order(1) == [0]
+    assert orc.tree_rank_order(2) == [0, 1]
+    assert orc.tree_rank_order(4) == [0, 2, 1, 3]
+    for k in range(1, 7):
+        p = 1 << k
+        rev = [int(format(r, f"0{k}b")[::-1], 2) for r in range(p)]
+        assert orc.tree_rank_order(p) == rev
+    # non powers of two: a permutation of the ranks, rank 0 first
+    for p in (3, 5, 6, 7, 12):
+        o = orc.tree_rank_order(p)
+        assert sorted(o) == list(range(p)) and o[0] == 0
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 8])
+def test_sort_tree_is_stable_sort_in_tree_order(orc, p):
+    """The literal tree of merges equals numpy's stable argsort of the shards
+    concatenated in tree order (a library routine), payload = (rank, index)."""
+    rng = np.random.default_rng(p)
+    shards = [rng.integers(0, 6, int(rng.integers(0, 40))).astype(np.int32) for _ in range(p)]
+    vals = [(np.uint32(r) << np.uint32(16)) + np.arange(s.size, dtype=np.uint32)
+            for r, s in enumerate(shards)]
+    ok, ov = orc.sort_tree(shards, vals)
+    order = orc.tree_rank_order(p)
+    cat = np.concatenate([shards[r] for r in order])
+    catv = np.concatenate([vals[r] for r in order])
+    perm = np.argsort(cat, kind="stable")
+    assert np.array_equal(ok, cat[perm]) and np.array_equal(ov, catv[perm])
+    assert np.array_equal(orc.sort_tree(shards), cat[perm])
