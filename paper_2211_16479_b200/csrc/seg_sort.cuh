@@ -3,11 +3,14 @@
 // P:332 / P:565, where per-array parallel overhead dominates).
 //
 // Segments are binned by length (Kernels::sort_segmented):
-//   len <= 256       one WARP per segment (this file), found on the device
-//                    from the offsets table: the warp holds the segment in
-//                    registers (1 or 8 keys per lane for <= 32 / <= 256) and
-//                    sorts it with a bitonic network whose cross-lane stages
-//                    are __shfl_xor_sync exchanges;
+//   len <= 32        kseg_tiny_sort, found on the device from the offsets
+//                    table: a warp sorts 4 segments at once, one register
+//                    each, with a 32-element bitonic network whose stages are
+//                    __shfl_xor_sync exchanges between lanes;
+//   len <= 256       kseg_mid_sort: one warp per segment, 2/4/8 keys per
+//                    lane, a 64/128/256-element bitonic network (in-lane
+//                    stages for strides below the keys per lane, shuffles
+//                    above);
 //   len <= T         one CTA per segment: the tile-sort kernels (K1) with a
 //                    segment descriptor instead of a tile index (128 x 17
 //                    threads x keys up to 2176, the K1 tile shape up to T);
@@ -107,60 +110,131 @@ __device__ __forceinline__ void warp_sort_segment(K* __restrict__ keys,
   }
 }
 
-// Segments of 2..256 elements straight from the offsets table: warp w of the
-// grid takes segment w, sorts it with a 32- or 256-element network by its
-// length (warp-uniform), and leaves longer or trivial segments alone (the
-// CTA-per-segment and merge paths take those).
+// Segments of 2..32 elements straight from the offsets table.  Warp w of the
+// grid takes segments [w*S, w*S + S) and sorts the short ones TOGETHER:
+// register j of every lane holds element `lane` of segment j, and one
+// 32-element bitonic network runs on all S registers (S independent shuffle
+// chains: S loads in flight and S-way ILP for these latency-bound segments).
+// Longer or trivial segments are left to the other kernels.
+constexpr int kSegPerWarp = 4;
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(128)
-    kseg_warp_sort(K* __restrict__ keys, uint32_t* __restrict__ vals,
+    kseg_tiny_sort(K* __restrict__ keys, uint32_t* __restrict__ vals,
                    const int64_t* __restrict__ off, int64_t nseg) {
+  constexpr int S = kSegPerWarp;
   const int lane = threadIdx.x & 31;
-  const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (s >= nseg) return;  // warp-uniform
-  const int64_t base = off[s];
-  const int64_t len = off[s + 1] - base;
-  if (len < 2 || len > 256) return;
-  if (len <= 32) warp_sort_segment<K, PAIRS, 1>(keys, vals, base, (int)len, lane);
-  else warp_sort_segment<K, PAIRS, 8>(keys, vals, base, (int)len, lane);
+  const int64_t s0 = ((int64_t)blockIdx.x * 4 + (threadIdx.x >> 5)) * S;
+  if (s0 >= nseg) return;  // warp-uniform
+  // the S + 1 boundaries, one lane each
+  int64_t ob = 0;
+  if (lane <= S && s0 + lane <= nseg) ob = off[s0 + lane];
+  int64_t base[S];
+  int cnt[S];
+  K key[S];
+  int idx[S];
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    const int64_t a = __shfl_sync(0xffffffffu, ob, j), e = __shfl_sync(0xffffffffu, ob, j + 1);
+    const int64_t l = s0 + j < nseg ? e - a : 0;
+    base[j] = a;
+    cnt[j] = l >= 2 && l <= 32 ? (int)l : 0;
+    key[j] = lane < cnt[j] ? keys[a + lane] : KeyTraits<K>::max_key();
+    idx[j] = lane;
+  }
+  // one 32-element bitonic network per register (element index = lane)
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int st = size >> 1; st > 0; st >>= 1) {
+      // the lower lane of an ascending pair keeps the smaller element
+      const bool keep_small = ((lane & size) == 0) == ((lane & st) == 0);
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        const K ok = __shfl_xor_sync(0xffffffffu, key[j], st);
+        int oi = idx[j];
+        if constexpr (PAIRS) oi = __shfl_xor_sync(0xffffffffu, idx[j], st);
+        if (keep_small == seg_less<K, PAIRS>(ok, oi, key[j], idx[j])) key[j] = ok, idx[j] = oi;
+      }
+    }
+  }
+  uint32_t v[PAIRS ? S : 1];
+  if constexpr (PAIRS) {
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (lane < cnt[j]) v[j] = vals[base[j] + idx[j]];
+    __syncwarp();  // all payloads read before any is overwritten
+  }
+#pragma unroll
+  for (int j = 0; j < S; ++j)
+    if (lane < cnt[j]) {
+      keys[base[j] + lane] = key[j];
+      if constexpr (PAIRS) vals[base[j] + lane] = v[j];
+    }
+}
+
+// Segments of 33..256 elements: one warp per (offset, length) descriptor,
+// the smallest network that holds the segment: 64, 128 or 256 elements (2, 4
+// or 8 keys per lane; the choice is warp-uniform).
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(128)
+    kseg_mid_sort(K* __restrict__ keys, uint32_t* __restrict__ vals,
+                  const int64_t* __restrict__ desc, int64_t cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t d = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (d >= cnt) return;
+  const int64_t base = desc[2 * d];
+  const int len = (int)desc[2 * d + 1];
+  if (len <= 64) warp_sort_segment<K, PAIRS, 2>(keys, vals, base, len, lane);
+  else if (len <= 128) warp_sort_segment<K, PAIRS, 4>(keys, vals, base, len, lane);
+  else warp_sort_segment<K, PAIRS, 8>(keys, vals, base, len, lane);
 }
 
 // Device-resident offsets: classify every segment (and check the table:
-// off[0] = 0, non-decreasing, off[nseg] = n).  counts[0..2] = entries
-// appended to the lists of (offset, length) for lengths in (w8, m], (m, t]
-// and > t; counts[3] = segments of 2..w8 elements (the warp kernel's); counts[4]
-// != 0 flags a bad table.  List order is arbitrary (segments are independent).
+// off[0] = 0, non-decreasing, off[nseg] = n).  counts[c] = entries appended to
+// list c of (offset, length) for lengths in (32, 256], (256, m], (m, t] and
+// > t; counts[4] = segments of 2..32 elements (kseg_tiny_sort reads those from
+// the table itself); counts[5] != 0 flags a bad table.  List order is
+// arbitrary (segments are independent).
 __global__ void __launch_bounds__(256)
-    kseg_classify(const int64_t* __restrict__ off, int64_t nseg, int64_t n, int64_t w8, int64_t m,
-                  int64_t t, int64_t* __restrict__ lm, int64_t* __restrict__ ll,
-                  int64_t* __restrict__ lx, unsigned long long* __restrict__ counts) {
-  // list capacities: a valid table has at most n / (bound + 1) such segments
-  const unsigned long long cap[3] = {(unsigned long long)(n / (w8 + 1) + 1),
-                                     (unsigned long long)(n / (m + 1) + 1),
-                                     (unsigned long long)(n / (t + 1) + 1)};
+    kseg_classify(const int64_t* __restrict__ off, int64_t nseg, int64_t n, int64_t m, int64_t t,
+                  int64_t* __restrict__ l0, int64_t* __restrict__ l1, int64_t* __restrict__ l2,
+                  int64_t* __restrict__ l3, unsigned long long* __restrict__ counts) {
+  // list capacities: a valid table has at most n / (lower bound + 1) such segments
+  const unsigned long long cap[4] = {
+      (unsigned long long)(n / 33 + 1), (unsigned long long)(n / 257 + 1),
+      (unsigned long long)(n / (m + 1) + 1), (unsigned long long)(n / (t + 1) + 1)};
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // whole warps iterate together (ballot-aggregated small count)
+  // whole warps iterate together (ballot-aggregated tiny count)
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < nseg;
        base += stride) {
     const int64_t i = base + lane;
-    bool small = false;
+    int c = -1;  // list of this lane's segment (4: tiny, counted only)
+    int64_t o0 = 0, len = 0;
     if (i < nseg) {
-      const int64_t o0 = off[i], o1 = off[i + 1], len = o1 - o0;
+      o0 = off[i];
+      const int64_t o1 = off[i + 1];
+      len = o1 - o0;
       const bool bad = len < 0 || o0 < 0 || o1 > n || (i == 0 && o0 != 0) ||
                        (i == nseg - 1 && o1 != n);
-      if (bad) atomicOr(counts + 4, 1ull);
-      small = !bad && len >= 2 && len <= w8;
-      if (!bad && len > w8) {
-        const int c = len <= m ? 0 : len <= t ? 1 : 2;
-        int64_t* l = c == 0 ? lm : c == 1 ? ll : lx;
-        const unsigned long long k = atomicAdd(counts + c, 1ull);
-        if (k < cap[c]) l[2 * k] = o0, l[2 * k + 1] = len;
-        else atomicOr(counts + 4, 1ull);  // overlapping segments: not a valid table
+      if (bad) atomicOr(counts + 5, 1ull);
+      else if (len >= 2) c = len <= 32 ? 4 : len <= 256 ? 0 : len <= m ? 1 : len <= t ? 2 : 3;
+    }
+    // one atomic per class per warp; lanes of a class write at base + rank
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const unsigned b = __ballot_sync(0xffffffffu, c == k);
+      if (!b) continue;
+      unsigned long long at = 0;
+      if (lane == __ffs(b) - 1) at = atomicAdd(counts + k, (unsigned long long)__popc(b));
+      at = __shfl_sync(0xffffffffu, at, __ffs(b) - 1);
+      if (c == k && k < 4) {
+        const unsigned long long slot = at + __popc(b & ((1u << lane) - 1));
+        int64_t* l = k == 0 ? l0 : k == 1 ? l1 : k == 2 ? l2 : l3;
+        if (slot < cap[k]) l[2 * slot] = o0, l[2 * slot + 1] = len;
+        else atomicOr(counts + 5, 1ull);  // overlapping segments: not a valid table
       }
     }
-    const unsigned b = __ballot_sync(0xffffffffu, small);
-    if (lane == 0 && b) atomicAdd(counts + 3, (unsigned long long)__popc(b));
   }
 }
 

@@ -835,31 +835,33 @@ struct Kernels {
       wv = reinterpret_cast<uint32_t*>(w);
       w += align_up((size_t)n * 4, 256);
     }
-    // ---- classification.  Segments of <= 256 elements are found by the warp
-    // kernel itself from the offsets table; the longer ones are listed: CTA
-    // bins (<= 2176, <= T) as (offset, length) descriptors, long segments as
-    // (offset, length) on the host (their tables are built here).
-    std::vector<int64_t> mid[2], xl;
-    const int64_t* md[2] = {nullptr, nullptr};
-    int64_t nm = 0, nl = 0, nsmall = 0;
+    // ---- classification.  Segments of <= 32 elements are found by the tiny
+    // kernel itself from the offsets table; the longer ones are listed: the
+    // warp bin (<= 256) and the CTA bins (<= 2176, <= T) as (offset, length)
+    // descriptors, long segments as (offset, length) on the host (their
+    // tables are built here).
+    std::vector<int64_t> mid[3], xl;  // bins: <= 256, <= 2176, <= T
+    const int64_t* md[3] = {nullptr, nullptr, nullptr};
+    int64_t nb[3] = {0, 0, 0}, ntiny = 0;
     if (!dev_off) {
       for (size_t i = 0; i < nseg; ++i) {
         const int64_t len = off[i + 1] - off[i];
-        if (len <= kSegW8) {
-          nsmall += len >= 2;
+        if (len <= 32) {
+          ntiny += len >= 2;
           continue;
         }
-        auto& v = len <= T ? mid[len <= kSegM ? 0 : 1] : xl;
+        auto& v = len <= T ? mid[len <= kSegW8 ? 0 : len <= kSegM ? 1 : 2] : xl;
         v.push_back(off[i]);
         v.push_back(len);
       }
-      nm = (int64_t)mid[0].size() / 2, nl = (int64_t)mid[1].size() / 2;
+      for (int c = 0; c < 3; ++c) nb[c] = (int64_t)mid[c].size() / 2;
     } else {
       // on the device (kseg_classify), then one synchronisation for the
       // counts and the long segments' list
-      const int64_t cap[3] = {n / (kSegW8 + 1) + 1, n / (kSegM + 1) + 1, n / (T + 1) + 1};
-      int64_t* lists[3];
-      for (int c = 0; c < 3; ++c) {
+      const int64_t cap[4] = {n / 33 + 1, n / (kSegW8 + 1) + 1, n / (kSegM + 1) + 1,
+                              n / (T + 1) + 1};
+      int64_t* lists[4];
+      for (int c = 0; c < 4; ++c) {
         lists[c] = reinterpret_cast<int64_t*>(w);
         w += align_up((size_t)cap[c] * 16, 256);
       }
@@ -869,27 +871,26 @@ struct Kernels {
         set_error("segmented sort: workspace too small");
         return MSORT_ERROR_INVALID_VALUE;
       }
-      MSORT_CUDA_TRY(cudaMemsetAsync(counts, 0, 5 * 8, s));
+      MSORT_CUDA_TRY(cudaMemsetAsync(counts, 0, 6 * 8, s));
       {
         LaunchScope ls(KC_PARTITION, s);
         const int64_t blocks = std::min<int64_t>(((int64_t)nseg + 255) / 256, 148 * 8);
         kseg_classify<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
-            off, (int64_t)nseg, n, kSegW8, kSegM, T, lists[0], lists[1], lists[2], counts);
+            off, (int64_t)nseg, n, kSegM, T, lists[0], lists[1], lists[2], lists[3], counts);
       }
       MSORT_CUDA_TRY(cudaGetLastError());
-      unsigned long long hc[5];
+      unsigned long long hc[6];
       MSORT_CUDA_TRY(cudaMemcpyAsync(hc, counts, sizeof(hc), cudaMemcpyDeviceToHost, s));
       MSORT_CUDA_TRY(cudaStreamSynchronize(s));
-      if (hc[4]) {
+      if (hc[5]) {
         set_error("seg_offsets must start at 0, not decrease and end at n");
         return MSORT_ERROR_INVALID_VALUE;
       }
-      nsmall = (int64_t)hc[3];
-      nm = (int64_t)hc[0], nl = (int64_t)hc[1];
-      md[0] = lists[0], md[1] = lists[1];
-      xl.resize(2 * hc[2]);
-      if (hc[2]) {
-        MSORT_CUDA_TRY(cudaMemcpyAsync(xl.data(), lists[2], hc[2] * 16, cudaMemcpyDeviceToHost, s));
+      ntiny = (int64_t)hc[4];
+      for (int c = 0; c < 3; ++c) nb[c] = (int64_t)hc[c], md[c] = lists[c];
+      xl.resize(2 * hc[3]);
+      if (hc[3]) {
+        MSORT_CUDA_TRY(cudaMemcpyAsync(xl.data(), lists[3], hc[3] * 16, cudaMemcpyDeviceToHost, s));
         MSORT_CUDA_TRY(cudaStreamSynchronize(s));
       }
     }
@@ -924,8 +925,8 @@ struct Kernels {
     // there are short segments), CTA-bin descriptors] K1 tile descriptors of
     // the long segments (even-level ones first), long-segment tables off[nxl]
     // len[nxl] tile0[nxl+1] lev[nxl] (int32, packed)
-    const int64_t w_off = (!dev_off && nsmall) ? (int64_t)nseg + 1 : 0;
-    const int64_t w_desc = w_off + (dev_off ? 0 : 2 * (nm + nl)), w_k1 = 2 * k1t;
+    const int64_t w_off = (!dev_off && ntiny) ? (int64_t)nseg + 1 : 0;
+    const int64_t w_desc = w_off + (dev_off ? 0 : 2 * (nb[0] + nb[1] + nb[2])), w_k1 = 2 * k1t;
     const int64_t w_tab = nxl ? 3 * nxl + 1 + (nxl + 1) / 2 : 0;
     const int64_t words = w_desc + w_k1 + w_tab;
     int64_t* dstage = reinterpret_cast<int64_t*>(w);
@@ -940,9 +941,12 @@ struct Kernels {
     } unlock;
     if (w_off) std::memcpy(h, off, (size_t)w_off * 8);
     if (!dev_off) {
-      if (nm) std::memcpy(h + w_off, mid[0].data(), (size_t)nm * 16);
-      if (nl) std::memcpy(h + w_off + 2 * nm, mid[1].data(), (size_t)nl * 16);
-      md[0] = dstage + w_off, md[1] = dstage + w_off + 2 * nm;
+      int64_t at = w_off;
+      for (int c = 0; c < 3; ++c) {
+        if (nb[c]) std::memcpy(h + at, mid[c].data(), (size_t)nb[c] * 16);
+        md[c] = dstage + at;
+        at += 2 * nb[c];
+      }
     }
     int64_t ntl_all = 0;
     {
@@ -977,16 +981,21 @@ struct Kernels {
     unlock.held = false;
     MSORT_TRY(staging_release(s));
     // ---- launches
-    if (nsmall) {
+    if (ntiny) {
       LaunchScope ls(KC_TILE_SORT, s);
-      kseg_warp_sort<K, PAIRS><<<(unsigned)((nseg + 3) / 4), 128, 0, s>>>(
+      const int64_t per_cta = 4 * kSegPerWarp;  // 4 warps x kSegPerWarp segments
+      kseg_tiny_sort<K, PAIRS><<<(unsigned)((nseg + per_cta - 1) / per_cta), 128, 0, s>>>(
           keys, vals, dev_off ? off : dstage, (int64_t)nseg);
     }
-    if (nm) {
+    if (nb[0]) {
+      LaunchScope ls(KC_TILE_SORT, s);
+      kseg_mid_sort<K, PAIRS><<<(unsigned)((nb[0] + 3) / 4), 128, 0, s>>>(keys, vals, md[0], nb[0]);
+    }
+    if (nb[1]) {
       LaunchScope ls(KC_TILE_SORT, s);
       constexpr size_t sm = (size_t)kSegM * sizeof(K) + (PAIRS ? (size_t)kSegM * 8 : 0);
       k1_tile_sort<K, PAIRS, kSegNTM, kSegVTM>
-          <<<(unsigned)nm, kSegNTM, sm, s>>>(keys, vals, keys, vals, 0, md[0]);
+          <<<(unsigned)nb[1], kSegNTM, sm, s>>>(keys, vals, keys, vals, 0, md[1]);
     }
     auto k1_desc = [&](const int64_t* d, int64_t cnt_, K* ok, uint32_t* ov) {
       LaunchScope ls(KC_TILE_SORT, s);
@@ -996,7 +1005,7 @@ struct Kernels {
       else
         k1_tile_sort_keys<K, NT1, VT><<<(unsigned)cnt_, NT1, k1_smem, s>>>(keys, ok, 0, d);
     };
-    if (nl) k1_desc(md[1], nl, keys, vals);
+    if (nb[2]) k1_desc(md[2], nb[2], keys, vals);
     if (nxl) {
       // long segments: K1 into buffer P_s & 1, then all levels of all of them
       if (n_even_tiles) k1_desc(dstage + w_desc, n_even_tiles, keys, vals);
