@@ -286,6 +286,13 @@ msort_status msort_plan_narrow(int world, const uint64_t *K, const uint64_t *tot
 msort_status msort_plan_fill(int world, const uint64_t *K, const uint64_t *lteq,
                              int64_t *out);
 
+/* The rank-tree schedule of msort_sort_distributed_tree: the
+ * number of rounds for `world` ranks, and this rank's role in round t
+ * (0 idle, 1 parent: receives from *peer and merges [own | received], own
+ * elements first on ties; 2 child: sends its array to *peer).  Host only. */
+int msort_plan_tree_rounds(int world);
+int msort_plan_tree_role(int world, int rank, int round, int *peer);
+
 /* ------------------------------------------------------- status and timing */
 
 const char *msort_status_string(msort_status s);

@@ -44,6 +44,7 @@ EXPORTED = (
     "msort_tile_size", "msort_debug_set_quad", "msort_sort_host", "msort_debug_set_exchange",
     "msort_segmented_workspace_bytes", "msort_sort_segmented",
     "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
+    "msort_plan_tree_rounds", "msort_plan_tree_role",
 )
 
 
@@ -97,6 +98,10 @@ def _load():
     L.msort_sort_distributed_tree_emulated.argtypes = [c.POINTER(vp), c.POINTER(vp),
                                                        c.POINTER(c.c_size_t), i32, i32, i32, vp,
                                                        vp, vp]
+    L.msort_plan_tree_rounds.argtypes = [i32]
+    L.msort_plan_tree_rounds.restype = i32
+    L.msort_plan_tree_role.argtypes = [i32, i32, i32, c.POINTER(i32)]
+    L.msort_plan_tree_role.restype = i32
     L.msort_tile_size.argtypes = [i32, i32]
     L.msort_tile_size.restype = i32
     for f in ("msort_sort", "msort_sort_pairs", "msort_workspace_bytes", "msort_sort_ws",
@@ -499,6 +504,18 @@ def plan_fill(world: int, K: np.ndarray, lteq: np.ndarray) -> np.ndarray:
                                out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
            "msort_plan_fill")
     return out.reshape(world + 1, world)
+
+
+def plan_tree(world: int, rank: int):
+    """[(role, peer)] per round of the rank tree (include/msort.h
+    msort_plan_tree_role): role 0 idle, 1 parent (receive from peer), 2 child
+    (send to peer)."""
+    out = []
+    for t in range(lib.msort_plan_tree_rounds(world)):
+        peer = ctypes.c_int(-1)
+        role = lib.msort_plan_tree_role(world, rank, t, ctypes.byref(peer))
+        out.append((role, peer.value))
+    return out
 
 
 # --------------------------------------------------------------- profiling

@@ -592,6 +592,17 @@ msort_status msort_plan_fill(int world, const uint64_t* K, const uint64_t* lteq,
   return MSORT_SUCCESS;
 }
 
+int msort_plan_tree_rounds(int world) { return world < 1 ? 0 : plan::tree_rounds(world); }
+
+int msort_plan_tree_role(int world, int rank, int round, int* peer) {
+  int q = -1;
+  const int r = (world < 1 || rank < 0 || rank >= world || round < 0)
+                    ? 0
+                    : plan::tree_role(world, rank, round, &q);
+  if (peer) *peer = q;
+  return r;
+}
+
 // ------------------------------------------------------- status / timing
 const char* msort_status_string(msort_status s) {
   switch (s) {

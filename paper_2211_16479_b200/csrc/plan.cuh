@@ -73,5 +73,32 @@ MSORT_HD int64_t fill_one(uint64_t K, const uint64_t* lteq, int world, int r, in
   return (int64_t)lt + rem;
 }
 
+// The paper's merge tree (f4): with `active` ranks left, split =
+// ceil(active / 2) (= active / 2, the paper's, for powers of two); ranks in
+// [split, active) send to rank - split, ranks below active - split receive
+// from rank + split.  Rounds until one rank is active:
+inline int tree_rounds(int world) {
+  int r = 0;
+  for (int a = world; a > 1; a = (a + 1) / 2) ++r;
+  return r;
+}
+// This rank's role in round t: 0 idle, 1 parent (receives from *peer and
+// merges [own | received], own first on ties), 2 child (sends to *peer).
+inline int tree_role(int world, int rank, int t, int* peer) {
+  int a = world;
+  for (int i = 0; i < t; ++i) a = (a + 1) / 2;
+  if (a <= 1) return 0;
+  const int split = (a + 1) / 2;
+  if (rank >= split && rank < a) {
+    *peer = rank - split;
+    return 2;
+  }
+  if (rank < a - split) {
+    *peer = rank + split;
+    return 1;
+  }
+  return 0;
+}
+
 }  // namespace plan
 }  // namespace msort

@@ -643,15 +643,12 @@ msort_status dist_emulated(void* const* keys, void* const* vals, const size_t* n
 // rank <- rank + split with an odd rank out (R12/R13).
 // Order of the shards after the tree (ties resolve in this order).
 static void tree_rounds(int p, std::vector<std::vector<std::pair<int, int>>>& rounds) {
-  rounds.clear();
-  int active = p;
-  while (active > 1) {
-    const int split = (active + 1) / 2;
-    std::vector<std::pair<int, int>> r;  // (parent, child)
-    for (int c = split; c < active; ++c) r.push_back({c - split, c});
-    rounds.push_back(r);
-    active = split;
-  }
+  rounds.assign(plan::tree_rounds(p), {});
+  for (int t = 0; t < (int)rounds.size(); ++t)
+    for (int r = 0; r < p; ++r) {
+      int peer = -1;
+      if (plan::tree_role(p, r, t, &peer) == 1) rounds[t].push_back({r, peer});  // (parent, child)
+    }
 }
 
 struct TreeBufs {

@@ -166,3 +166,104 @@ def test_gloo_world2(orc):
 
 def test_gloo_world3(orc):
     _run(3, CASES3, orc)
+
+
+# ---------------------------------------------------------------- rank tree
+def _tree_worker(rank, world, port, cases, q):
+    """The rank-tree gather (msort_sort_distributed_tree) on CPU: the library's
+    own schedule (msort_plan_tree_role), arrays moved point to point over
+    gloo (sizes first), merged by the oracle's merge() as the stand-in for K3,
+    local sorts by the oracle."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+
+    import oracle
+    import paper_2211_16479_b200 as ms
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        for ci, case in enumerate(cases):
+            k = make_shard(case, rank)
+            v = ((np.uint32(rank) << np.uint32(24)) + np.arange(k.size, dtype=np.uint32))
+            k, v = oracle.sort(k, v)
+            for role, peer in ms.plan_tree(world, rank):
+                if role == 2:  # child: size, keys, payload to the parent
+                    dist.send(torch.tensor([k.size], dtype=torch.int64), peer)
+                    if k.size:
+                        dist.send(torch.from_numpy(k.copy()), peer)
+                        dist.send(torch.from_numpy(v.view(np.int32).copy()), peer)
+                elif role == 1:  # parent: receive, merge(own, received)
+                    m = torch.zeros(1, dtype=torch.int64)
+                    dist.recv(m, peer)
+                    m = int(m.item())
+                    if m:
+                        rk = torch.from_numpy(np.zeros(m, dtype=k.dtype))
+                        rv = torch.zeros(m, dtype=torch.int32)
+                        dist.recv(rk, peer)
+                        dist.recv(rv, peer)
+                        k, v = oracle.merge(k, rk.numpy(), v, rv.numpy().view(np.uint32))
+            q.put((ci, rank, k.tobytes() if rank == 0 else b"", v.tobytes() if rank == 0 else b"",
+                   k.dtype.str))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_gloo_tree(orc, world):
+    cases = [([1000 * (r + 1) for r in range(world)], ("mod", 5), np.int64),
+             ([0] + [777] * (world - 1), "u31", np.int32)]
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_tree_worker, args=(r, world, port, cases, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(world * len(cases)):
+        ci, rank, kb, vb, dt = q.get(timeout=300)
+        got[(ci, rank)] = (kb, vb, dt)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for ci, case in enumerate(cases):
+        shards = [make_shard(case, r) for r in range(world)]
+        vals = [((np.uint32(r) << np.uint32(24)) + np.arange(s.size, dtype=np.uint32))
+                for r, s in enumerate(shards)]
+        ek, ev = orc.sort_tree(shards, vals)
+        kb, vb, dt = got[(ci, 0)]
+        assert np.array_equal(np.frombuffer(kb, dtype=np.dtype(dt)), ek)
+        assert np.array_equal(np.frombuffer(vb, dtype=np.uint32), ev)
+
+
+@pytest.fixture(scope="module")
+def ms():
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import paper_2211_16479_b200 as m
+
+    return m
+
+
+def test_plan_tree_schedule(ms):
+    """Every round pairs each child with exactly one parent; after the rounds
+    only rank 0 holds data; powers of two follow the paper's split = size/2."""
+    for p in range(1, 20):
+        holds = set(range(p))
+        rounds = ms.lib.msort_plan_tree_rounds(p)
+        assert rounds == (p - 1).bit_length()
+        for t in range(rounds):
+            roles = [ms.plan_tree(p, r)[t] for r in range(p)]
+            parents = {r: peer for r, (role, peer) in enumerate(roles) if role == 1}
+            children = {r: peer for r, (role, peer) in enumerate(roles) if role == 2}
+            assert {c: par for par, c in parents.items()} == children
+            assert set(children) <= holds
+            holds -= set(children)
+            if p & (p - 1) == 0:  # the paper's split = size / 2^(t+1)
+                split = p >> (t + 1)
+                assert all(par == c - split for c, par in children.items())
+        assert holds == {0}
