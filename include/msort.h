@@ -324,7 +324,10 @@ int msort_tile_size(msort_dtype key_dtype, msort_dtype val_dtype);
  * CTA gets >= 2 segments, the remaining levels 2-way; 2: 4-way passes whenever
  * >= 2 levels remain (small inputs too -- for tests); 4: every pair of levels
  * as a K3X pass (4-way super-tiles between X-/Y-side boundary states found
- * just in time by a searcher warp, no nested searches).  The result is the same
+ * just in time by a searcher warp, no nested searches); 5: every pair of levels
+ * as a K6 pass (4-byte keys: tiles between X-side states computed by a
+ * partition kernel, cut at Y-side states when oversized, merged in two rounds
+ * by the tile sort's merge engine; 8-byte keys fall back to mode 0).  The result is the same
  * in every mode (the stable sort is unique); process-wide, not thread-safe
  * against concurrent sorts.  Overrides the MSORT_QUAD environment variable.
  * Returns 0. */

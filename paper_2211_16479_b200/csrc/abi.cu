@@ -2,6 +2,7 @@
 // dispatch, workspace handling, error text and kernel accounting.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -112,8 +113,15 @@ size_t single_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd) {
   // partitions: one per output tile (+ slack for the k-way merge's extra tiles)
   b += align_up((n / (size_t)T + 2 + 2 * 64) * sizeof(int64_t), 256);
   // 4-way pass segment boundaries (4 x int64 each)
-  b += align_up((2 * (n / (size_t)T) + 64) * 4 * sizeof(int64_t), 256);
-  return b;
+  size_t q = align_up((2 * (n / (size_t)T) + 64) * 4 * sizeof(int64_t), 256);
+  if (dtype_size(kd) == 4 && vd == MSORT_NONE) {
+    // K6 partition (Kernels::k6_*): unit states (32 B) and tiles (72 B) per
+    // unit, cut records (16 B) and piece tiles (72 B) per piece, a counter
+    const size_t nu = n / 3998 + n / (4 * (size_t)T) + 2, ex = n / 4568 + nu + 1;
+    q = std::max(q, align_up(32 * nu, 256) + align_up(72 * nu, 256) + align_up(16 * ex, 256) +
+                        align_up(72 * ex, 256) + 256);
+  }
+  return b + q;
 }
 
 static msort_status check_device() {

@@ -218,6 +218,9 @@ __device__ __forceinline__ void store_vec(K* dst, const K (&key)[VT]) {
   }
 }
 
+}  // namespace msort
+#include "k6_quad.cuh"
+namespace msort {
 
 // Compare-exchange of the keys-only register network (min and max; any
 // network is fine for keys only -- equal integers are indistinguishable).
@@ -540,6 +543,22 @@ struct Kernels {
     return g[dev & 63];
   }
 
+  // K6 (4-byte keys only, quad mode 5): 128 threads x 68 keys, tiles of
+  // <= XS keys of X plus <= YS keys of Y (XS + YS = Tm = 126 x 68)
+  static constexpr int kK6NT2 = MSORT_K6_NT2, kK6VT = 68;
+  using K6S = K6Shape<kK6NT2, kK6VT>;
+  // X keys per unit: 7/15 of the tile, so a unit of random keys (as many Y
+  // keys as X keys, +- a few sqrt) fits without a cut
+  static constexpr int kK6XS = K6S::Tm * 7 / 15, kK6YS = K6S::Tm - kK6XS;
+  static bool k6_mode() { return sizeof(K) == 4 && quad_mode() == 5; }
+  static int64_t k6_units_max(int64_t n) { return n / kK6XS + n / (4 * (int64_t)T) + 2; }
+  static_assert(kK6XS >= 3998, "msort_workspace_bytes sizes the K6 area for XS >= 3998");
+  static int64_t k6_extra_max(int64_t n) { return n / kK6YS + k6_units_max(n) + 1; }
+  static int& k6_grid(int dev) {
+    static int g[64] = {};
+    return g[dev & 63];
+  }
+
   static int& grid3(int dev) {
     static int g[64] = {};
     return g[dev & 63];
@@ -605,6 +624,15 @@ struct Kernels {
     // every CTA of the persistent merge kernel must be resident (the fused
     // levels wait on each other's progress): grid = SMs x occupancy
     grid3(dev) = sms * occ;
+    if constexpr (!PAIRS && sizeof(K) == 4) {
+      auto k6 = k6_quad_pass<K, kK6NT2, kK6VT>;
+      MSORT_CUDA_TRY(cudaFuncSetAttribute(k6, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(K6S::KEYS * sizeof(K))));
+      int o6 = 0;
+      MSORT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o6, k6, K6S::NT1,
+                                                                   K6S::KEYS * sizeof(K)));
+      k6_grid(dev) = sms * std::max(o6, 1);
+    }
     if constexpr (!PAIRS) {
       auto kq = k3q_pass<K, NTQ, VTQ>;
       MSORT_CUDA_TRY(
@@ -669,9 +697,10 @@ struct Kernels {
     int nq = 0;
     int64_t Lq = T;
     if constexpr (!PAIRS) {
-      const int mode = quad_mode();
-      if (mode == 4) nq = passes / 2, Lq = (int64_t)T << (2 * nq);  // K3X: every pair of levels
-      while (mode && mode != 4 && passes - 2 * nq >= 2) {
+      const int mode = k6_mode() ? 5 : quad_mode();
+      if (mode == 4 || mode == 5)
+        nq = passes / 2, Lq = (int64_t)T << (2 * nq);  // K3X / K6: every pair of levels
+      while (mode && mode < 4 && passes - 2 * nq >= 2) {
         int64_t ng, nseg;
         int sf, sl;
         quad_geometry((int64_t)n, Lq, ng, sf, sl, nseg);
@@ -726,7 +755,62 @@ struct Kernels {
       if (nq > 0)
         MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * sizeof(unsigned long long), s));
       int64_t L = T;
-      if (quad_mode() == 4) {
+      if constexpr (sizeof(K) == 4) {
+      if (k6_mode() && nq > 0) {
+        // K6 (k6_quad.cuh): partition (unit states, tiles, cut pieces), then
+        // the 4-way pass over the unit tiles and over the pieces
+        char* kw = reinterpret_cast<char*>(qstates);
+        int64_t* states = reinterpret_cast<int64_t*>(kw);
+        const int64_t NUmax = k6_units_max((int64_t)n);
+        K6Tile* tiles = reinterpret_cast<K6Tile*>(kw + align_up(32 * NUmax, 256));
+        int64_t* cuts = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(tiles) +
+                                                   align_up(sizeof(K6Tile) * NUmax, 256));
+        const int64_t EXmax = k6_extra_max((int64_t)n);
+        K6Tile* extra = reinterpret_cast<K6Tile*>(reinterpret_cast<char*>(cuts) +
+                                                  align_up(16 * EXmax, 256));
+        auto* ncut = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(extra) +
+                                                            align_up(sizeof(K6Tile) * EXmax, 256));
+        for (int q = 0; q < nq; ++q, L *= 4) {
+          K6Pass P{};
+          P.src = bk[cur], P.n = (int64_t)n, P.L = L;
+          P.groups = ((int64_t)n + 4 * L - 1) / (4 * L);
+          P.xs = kK6XS, P.ys = kK6YS;
+          P.upg = (2 * L + kK6XS - 1) / kK6XS;
+          const int64_t last0 = (P.groups - 1) * 4 * L;
+          const int64_t nx_last = std::min<int64_t>((int64_t)n, last0 + 2 * L) - last0;
+          P.nunits = (P.groups - 1) * P.upg + std::max<int64_t>(1, (nx_last + kK6XS - 1) / kK6XS);
+          MSORT_CUDA_TRY(cudaMemsetAsync(ncut, 0, 8, s));
+          const unsigned gb = (unsigned)((P.nunits + 127) / 128);
+          {
+            LaunchScope ls(KC_PARTITION, s);
+            k6_states<K, true><<<gb, 128, 0, s>>>(P, states);
+            k6_states<K, false><<<gb, 128, 0, s>>>(P, states);
+            k6_tiles<K><<<gb, 128, 0, s>>>(P, states, tiles, cuts, ncut);
+            k6_cut_tiles<K><<<(unsigned)(k6_grid(dev) / 8 + 1), 128, 0, s>>>(P, states, cuts, ncut,
+                                                                           extra);
+          }
+          MSORT_CUDA_TRY(cudaGetLastError());
+          {
+            LaunchScope ls(KC_MERGE, s);
+            k6_quad_pass<K, kK6NT2, kK6VT><<<(unsigned)P.nunits, K6S::NT1, K6S::KEYS * sizeof(K),
+                                             s>>>(bk[cur], bk[cur ^ 1], tiles, nullptr);
+            k6_quad_pass<K, kK6NT2, kK6VT><<<(unsigned)k6_grid(dev), K6S::NT1,
+                                             K6S::KEYS * sizeof(K), s>>>(bk[cur], bk[cur ^ 1],
+                                                                         extra, ncut);
+          }
+          MSORT_CUDA_TRY(cudaGetLastError());
+#ifdef MSORT_K3_CHECK
+          {
+            cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) return cuda_fail(e, "k6 (debug sync)");
+          }
+#endif
+          cur ^= 1;
+        }
+        if (left == 0) return MSORT_SUCCESS;
+      }
+      }
+      if (quad_mode() == 4 && !k6_mode()) {
         for (int q = 0; q < nq; ++q, L *= 4) {
           const int64_t ng = ((int64_t)n + 4 * L - 1) / (4 * L);
           const int64_t upg = (2 * L + LX::XS - 1) / LX::XS + 1;
@@ -747,7 +831,7 @@ struct Kernels {
         }
         if (left == 0) return MSORT_SUCCESS;
       }
-      for (int q = 0; q < nq && quad_mode() != 4; ++q, L *= 4) {
+      for (int q = 0; q < nq && quad_mode() != 4 && !k6_mode(); ++q, L *= 4) {
         int64_t ng, nseg;
         int sf, sl;
         quad_geometry((int64_t)n, L, ng, sf, sl, nseg);
@@ -1252,6 +1336,25 @@ int tile_size_for(msort_dtype kd, msort_dtype vd) {
 }
 
 }  // namespace msort
+
+// Experiment (K6, k6_quad.cuh): one 4-way pass over int32 keys with
+// caller-computed tiles (K6Tile[ntiles], device memory).  Not declared in
+// include/msort.h: a tuning entry point for scripts/k6_experiment.py.
+extern "C" int msort_debug_k6_pass(const void* src, void* dst, const void* tiles, int64_t ntiles,
+                                   void* stream) {
+  using namespace msort;
+  constexpr int NT2 = 126, VT = 68;
+  using SH = K6Shape<NT2, VT>;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k6_quad_pass<int32_t, NT2, VT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SH::KEYS * 4));
+    init = true;
+  }
+  k6_quad_pass<int32_t, NT2, VT><<<(unsigned)ntiles, SH::NT1, SH::KEYS * 4, (cudaStream_t)stream>>>(
+      (const int32_t*)src, (int32_t*)dst, (const K6Tile*)tiles, nullptr);
+  return (int)cudaGetLastError();
+}
 
 extern "C" int msort_debug_set_quad(int mode) {
   msort::g_quad_mode = mode;

@@ -19,11 +19,13 @@ pytestmark = pytest.mark.gpu
 DTYPES = [np.int32, np.uint32, np.int64, np.uint64]
 
 
-@pytest.fixture(scope="module", params=[2, 4], ids=["k3q", "k3x"])
+@pytest.fixture(scope="module", params=[2, 4, 5], ids=["k3q", "k3x", "k6"])
 def ms(request):
     """Mode 2: K3Q (4-way merge tree, sampled segment splitters) whenever two
     levels remain; mode 4: K3X (4-way super-tiles between X-/Y-side boundary
-    states found just in time) for every pair of levels."""
+    states found just in time) for every pair of levels; mode 5: K6 (unit
+    tiles between X-side states, cut at Y-side states, merged with the
+    tile-sort engine; 4-byte keys -- 8-byte keys take mode 0)."""
     import paper_2211_16479_b200 as m
 
     assert torch.cuda.is_available()
@@ -78,7 +80,7 @@ def test_quad_modes_agree(ms):
     n = 1 << 22
     src = mi.keys_torch(n, 5, "u31", device="cuda")
     outs = []
-    for mode in (0, 1, 2, 4):
+    for mode in (0, 1, 2, 4, 5):
         ms.set_quad_mode(mode)
         t = src.clone()
         ms.msort_sort(t)
