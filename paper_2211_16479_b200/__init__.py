@@ -161,6 +161,25 @@ def _keep_for(ws: torch.Tensor, stream) -> None:
         ws.record_stream(stream)
 
 
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+_NULL = _Null()
+
+
+def _on(device):
+    """torch.cuda.device(device), skipped when it is already current (the
+    context manager costs microseconds per call; small sorts notice)."""
+    if device.index is None or device.index == torch.cuda.current_device():
+        return _NULL
+    return torch.cuda.device(device)
+
+
 def _check_tensor(t: torch.Tensor, name: str):
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor")
@@ -204,7 +223,7 @@ def msort_sort_pairs(keys: torch.Tensor, vals: torch.Tensor | None, ws: torch.Te
     if ws is None:
         ws = workspace(n, keys.dtype, vals is not None, device=keys.device)
         _keep_for(ws, stream)
-    with torch.cuda.device(keys.device):
+    with _on(keys.device):
         _check(lib.msort_sort_ws(_ptr(keys), _ptr(vals), n, kd, vd, _ptr(ws), ws.numel(),
                                  ctypes.c_void_p(_stream(stream))), "msort_sort_ws")
     return keys, vals
@@ -224,7 +243,7 @@ def msort_sort_out(in_keys: torch.Tensor, keys_out: torch.Tensor, in_vals=None, 
     if ws is None:
         ws = workspace(n, in_keys.dtype, in_vals is not None, device=in_keys.device)
         _keep_for(ws, stream)
-    with torch.cuda.device(in_keys.device):
+    with _on(in_keys.device):
         _check(lib.msort_sort_out_ws(_ptr(in_keys), _ptr(in_vals), _ptr(keys_out), _ptr(vals_out),
                                      n, kd, vd, _ptr(ws), ws.numel(),
                                      ctypes.c_void_p(_stream(stream))), "msort_sort_out_ws")
@@ -248,7 +267,7 @@ def msort_sort_host(host_keys: torch.Tensor, host_keys_out: torch.Tensor, dev_ke
     if ws is None:
         ws = workspace(n, dev_keys.dtype, dev_vals is not None, device=dev_keys.device)
         _keep_for(ws, stream)
-    with torch.cuda.device(dev_keys.device):
+    with _on(dev_keys.device):
         _check(lib.msort_sort_host(_ptr(host_keys), _ptr(host_vals), _ptr(host_keys_out),
                                    _ptr(host_vals_out), n, kd, vd, _ptr(dev_keys), _ptr(dev_vals),
                                    _ptr(ws), ws.numel(), ctypes.c_void_p(_stream(stream))),
@@ -297,7 +316,7 @@ def msort_sort_segmented(keys: torch.Tensor, seg_offsets, vals: torch.Tensor | N
         nb = msort_segmented_workspace_bytes(n, nseg, kd, vd)
         ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=keys.device)
         _keep_for(ws, stream)
-    with torch.cuda.device(keys.device):
+    with _on(keys.device):
         _check(lib.msort_sort_segmented(_ptr(keys), _ptr(vals), n, off_ptr, nseg,
                                         kd, vd, _ptr(ws), ws.numel(),
                                         ctypes.c_void_p(_stream(stream))), "msort_sort_segmented")
@@ -352,7 +371,7 @@ def msort_sort_distributed(keys: torch.Tensor, comm: Comm, vals: torch.Tensor | 
     if ws is None:
         ws = workspace(n, keys.dtype, vals is not None, world=comm.world, device=keys.device)
     split = np.zeros((comm.world + 1) * comm.world, dtype=np.int64)
-    with torch.cuda.device(keys.device):
+    with _on(keys.device):
         _check(lib.msort_sort_distributed_ws(
             _ptr(keys), _ptr(vals), n, kd, vd, comm.handle, _ptr(ws), ws.numel(),
             ctypes.c_void_p(_stream(stream)),
@@ -373,7 +392,7 @@ def msort_sort_distributed_out(in_keys: torch.Tensor, keys_out: torch.Tensor, co
         ws = workspace(n, in_keys.dtype, in_vals is not None, world=comm.world,
                        device=in_keys.device)
     split = np.zeros((comm.world + 1) * comm.world, dtype=np.int64)
-    with torch.cuda.device(in_keys.device):
+    with _on(in_keys.device):
         _check(lib.msort_sort_distributed_out_ws(
             _ptr(in_keys), _ptr(in_vals), _ptr(keys_out), _ptr(vals_out), n, kd, vd, comm.handle,
             _ptr(ws), ws.numel(), ctypes.c_void_p(_stream(stream)),
@@ -400,7 +419,7 @@ def msort_sort_distributed_emulated(keys: list, vals: list | None = None, stream
     np_ = (ctypes.c_size_t * p)(*[k.numel() for k in keys])
     wp = VP(*[w.data_ptr() for w in wss])
     split = np.zeros((p + 1) * p, dtype=np.int64)
-    with torch.cuda.device(keys[0].device):
+    with _on(keys[0].device):
         _check(lib.msort_sort_distributed_emulated(
             kp, vp, np_, p, kd, vd, wp, wsb, ctypes.c_void_p(_stream(stream)),
             split.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
@@ -429,7 +448,7 @@ def msort_sort_distributed_tree(in_keys: torch.Tensor, comm: Comm, in_vals=None,
             root_vals = torch.empty(total, dtype=in_vals.dtype, device=in_keys.device)
     cap = root_keys.numel() if root_keys is not None else 0
     tot = ctypes.c_int64()
-    with torch.cuda.device(in_keys.device):
+    with _on(in_keys.device):
         _check(lib.msort_sort_distributed_tree(
             _ptr(in_keys), _ptr(in_vals), n, kd, vd, comm.handle, _ptr(root_keys),
             _ptr(root_vals), cap, ctypes.c_void_p(_stream(stream)), ctypes.byref(tot)),
@@ -452,7 +471,7 @@ def msort_sort_distributed_tree_emulated(keys: list, vals: list | None = None, s
     kp = VP(*[k.data_ptr() for k in keys])
     vp = VP(*[v.data_ptr() for v in vals]) if vals else None
     np_ = (ctypes.c_size_t * p)(*[k.numel() for k in keys])
-    with torch.cuda.device(keys[0].device):
+    with _on(keys[0].device):
         _check(lib.msort_sort_distributed_tree_emulated(
             kp, vp, np_, p, kd, vd, _ptr(rk), _ptr(rv), ctypes.c_void_p(_stream(stream))),
             "msort_sort_distributed_tree_emulated")
