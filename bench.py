@@ -18,6 +18,10 @@ no L2 flush is done between steps.  Timing: W untimed steps, then K steps
 between a barrier + cuda.synchronize on both sides, CUDA events on the
 launching stream, max over ranks.  Rank 0 prints one JSON line.
 
+N = 1 also reports "batched_sort" (outside the timed region
+and the headline): 2^24 keys in 2^20 x 16, 2^16 x 256 and 256 x 65536 segments
+sorted by one msort_sort_segmented call each (--no-batched skips it).
+
 --impl reference times the CPU oracle (oracle/, textbook top-down merge sort)
 on a bounded sample of the same workload on this host's cores (rank 0 only).
 """
@@ -50,6 +54,8 @@ def parse():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU (default 2^28)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-batched", action="store_true",
+                    help="skip the batched (segmented) sort lines (SURVEY §8(f) f3)")
     ap.add_argument("--e2e-streams", type=int, default=3, help="streams the e2e steps rotate over")
     ap.add_argument("--exchange", choices=["alltoall", "pull"], default="alltoall",
                     help="N > 1: NCCL all-to-all + k-way merge, or the fused pull exchange")
@@ -224,6 +230,47 @@ def pcie_duplex_ms(h_in, h_out, d_a, d_b, strs, reps=4):
     f2.record(s2)
     torch.cuda.synchronize()
     return max(e0.elapsed_time(f1), e0.elapsed_time(f2)) / reps
+
+
+def batched_bench(ms, mi, dev, reps=10):
+    """SURVEY §8(f) f3 beside the headline: batched sorts of 2^24 int32 keys
+    (seed 1) cut into equal segments, offsets in device memory
+    (msort_sort_segmented).  Per workload: median ms of `reps` calls (CUDA
+    events around the call, input restored untimed before each), G keys/s,
+    and a check that every segment came out non-decreasing with its sum
+    unchanged."""
+    import torch
+
+    n = 1 << 24
+    base = mi.keys_torch(n, 1, "u31", device=dev)
+    out = {}
+    for seg in (16, 256, 65536):
+        nseg = n // seg
+        off = torch.arange(0, n + 1, seg, dtype=torch.int64, device=dev)
+        k = base.clone()
+        nb = ms.msort_segmented_workspace_bytes(n, nseg, ms.MSORT_INT32)
+        ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+        for _ in range(3):
+            k.copy_(base)
+            ms.msort_sort_segmented(k, off, ws=ws)
+        ts = []
+        for _ in range(reps):
+            k.copy_(base)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ms.msort_sort_segmented(k, off, ws=ws)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ts.sort()
+        med = ts[len(ts) // 2]
+        v = k.view(nseg, seg)
+        ok = bool((v[:, 1:] >= v[:, :-1]).all()) and bool(
+            torch.equal(v.to(torch.int64).sum(1), base.view(nseg, seg).to(torch.int64).sum(1)))
+        out[f"{nseg}x{seg}"] = {"ms": round(med, 4), "gkeys_s": round(n / med / 1e6, 2),
+                                "verified": ok}
+    return {"workload": "2^24 int32 keys uniform [0,2^31) (seed 1) in equal segments, "
+                        "offsets on the device; msort_sort_segmented", "results": out}
 
 
 def main():
@@ -444,6 +491,10 @@ def main():
             e2e["pcie_duplex_ms"] = fl
             e2e["frac_of_pcie"] = round(fl / (te / ke), 4)
 
+    batched = None
+    if rank == 0 and world == 1 and not args.no_batched:
+        batched = batched_bench(ms, mi, dev)
+
     cpu = cpu_mp = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(1 << 24, 3)
@@ -474,6 +525,7 @@ def main():
             "cpu_baseline": cpu,
             "cpu_paper_mp": cpu_mp,
             "e2e": e2e,
+            "batched_sort": batched,
             "gpu_launches": launches,
             "clocks": clocks,
             "verified": ok,
