@@ -99,7 +99,11 @@ msort_status msort_workspace_bytes(size_t n, msort_dtype key_dtype, msort_dtype 
  * (e.g. from the PyTorch caching allocator).  vals may be NULL with
  * val_dtype == MSORT_NONE.  ws must be 256-byte aligned and at least
  * msort_workspace_bytes(n, key_dtype, val_dtype, 1) bytes; it must not overlap
- * keys/vals.  Nothing is allocated. */
+ * keys/vals.  Nothing is allocated and nothing synchronises, so this call (and
+ * msort_sort_out_ws) can be captured into a CUDA graph: a replay sorts whatever
+ * the buffers hold (after one uncaptured call has done the library's one-time
+ * kernel setup).  The segmented, distributed and host-buffer calls are not
+ * capturable (host-side tables / synchronisation). */
 msort_status msort_sort_ws(void *keys, void *vals, size_t n, msort_dtype key_dtype,
                            msort_dtype val_dtype, void *ws, size_t ws_bytes,
                            msort_stream_t stream);
