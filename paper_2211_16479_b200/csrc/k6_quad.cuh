@@ -5,13 +5,15 @@
 // A 4-way pass merges groups of four consecutive runs A, B, C, D of length L
 // into runs of 4L: X = merge(A, B), Y = merge(C, D), out = merge(X, Y), every
 // merge the stable merge() of P:107 (ties to the left run, R1).
-// Output tile q of a group covers Tm = NT2 * VT outputs; its input windows
-// are given by the 4-way co-ranks ("states") at its two boundaries.  One CTA
-// per tile, K1-style: the four windows are loaded into shared memory between
-// MIN/MAX sentinels, round 1 merges A+B and C+D (each thread VT outputs of X
-// or of Y as two merge chains, merge_keys_dual) into registers, they go back
-// to shared memory as the round-2 pair, round 2 merges X+Y, and the tile
-// leaves with coalesced stores.
+// A tile is the stretch of the output between two 4-way prefix "states"
+// (keys of A, B, C, D before it) found by the partition kernels below; it
+// holds at most Tm = NT2 * VT keys.  One CTA per tile, K1-style: the four
+// windows arrive by TMA bulk copies between MIN/MAX sentinels, round 1 merges
+// A+B and C+D (each thread VT outputs of X or of Y as two merge chains,
+// merge_keys_dual) into registers, they go back to shared memory as 16-byte
+// vectors for the round-2 pair, round 2 merges X+Y at the destination's
+// 16-byte phase, and the tile leaves by one bulk store.  Opt-in (quad mode 5):
+// 2% faster than the fused 2-way levels on 2^28 int32.
 #pragma once
 
 #ifndef MSORT_K6_NT2
