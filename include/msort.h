@@ -184,7 +184,12 @@ msort_status msort_comm_destroy(msort_comm_t comm);
  * vals: NULL (val_dtype MSORT_NONE) or 4-byte payloads.
  * split_matrix_out: NULL or host (world+1)*world int64: entry (r, j) = number
  * of rank j's elements among the first K_r outputs.
- * Synchronises `stream` once (the exchange sizes are needed on the host). */
+ * Synchronises `stream` once (the exchange sizes are needed on the host).
+ * Failure detection: that wait polls the stream and ncclCommGetAsyncError
+ * instead of blocking; an NCCL error -- or, with the environment variable
+ * MSORT_NCCL_TIMEOUT_S set, a wait longer than that many seconds (a dead or
+ * missing peer) -- aborts the communicator (ncclCommAbort) and returns
+ * MSORT_ERROR_NCCL; later calls on it return MSORT_ERROR_NCCL at once. */
 msort_status msort_sort_distributed(void *keys, void *vals, size_t n_local,
                                     msort_dtype key_dtype, msort_dtype val_dtype,
                                     msort_comm_t comm, msort_stream_t stream,

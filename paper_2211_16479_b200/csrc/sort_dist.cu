@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
+#include <chrono>
 #include <map>
 #include <string>
 #include <vector>
@@ -35,6 +37,12 @@ struct msort_comm_s {
   // pull exchange: peers' exchange buffers opened through CUDA IPC, cached by
   // (rank, handle) -- the workspace allocation is normally reused call to call
   std::map<std::pair<int, std::string>, void*> ipc_open;
+  bool aborted = false;  // set when a failure aborted the NCCL communicator
+  // page-locked staging for the small host<->device copies of a call (split
+  // matrix, sizes, IPC records): copies from/to pageable memory would block
+  // the host inside cudaMemcpyAsync, out of reach of the failure detection
+  unsigned char* pinned = nullptr;
+  size_t pinned_bytes = 0;
 };
 
 namespace msort {
@@ -51,6 +59,42 @@ static msort_status nccl_fail(ncclResult_t r, const char* what) {
     ncclResult_t _r = (expr);                                 \
     if (_r != ncclSuccess) return ::msort::nccl_fail(_r, #expr); \
   } while (0)
+
+// Host wait for the distributed call's stream with failure detection
+// (SURVEY.md §5): instead of blocking in cudaStreamSynchronize -- which never
+// returns if a peer died inside a collective -- poll the stream and the
+// communicator's asynchronous error state; on an NCCL error, or after
+// MSORT_NCCL_TIMEOUT_S seconds (environment, default 0 = no timeout), abort
+// the communicator (it is unusable afterwards) and return MSORT_ERROR_NCCL.
+static msort_status wait_stream_nccl(msort_comm_s* c, cudaStream_t s, const char* what) {
+  static double limit = -1.0;
+  if (limit < 0) {
+    const char* e = getenv("MSORT_NCCL_TIMEOUT_S");
+    limit = e ? atof(e) : 0.0;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return MSORT_SUCCESS;
+    if (q != cudaErrorNotReady) return cuda_fail(q, what);
+    ncclResult_t ae = ncclSuccess;
+    if (ncclCommGetAsyncError(c->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress) {
+      ncclCommAbort(c->comm);
+      c->aborted = true;
+      return nccl_fail(ae, what);
+    }
+    const double el =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (limit > 0 && el > limit) {
+      ncclCommAbort(c->comm);
+      c->aborted = true;
+      set_error(std::string(what) + ": timed out after " + std::to_string(el) +
+                " s (MSORT_NCCL_TIMEOUT_S); communicator aborted");
+      return MSORT_ERROR_NCCL;
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
 
 // ------------------------------------------------------------- K4 kernels
 __global__ void k4_set_u64(uint64_t* p, uint64_t v) { *p = v; }
@@ -301,6 +345,18 @@ struct NcclColl {
     return MSORT_SUCCESS;
   }
   int rank_of(int local) const { return c->rank + local; }
+  msort_status wait(const char* what) { return wait_stream_nccl(c, s, what); }
+  // device -> host copy of `bytes` through the pinned staging, then the wait
+  msort_status fetch(void* host, const void* dev, size_t bytes, const char* what) {
+    if (bytes > c->pinned_bytes) {
+      set_error(std::string(what) + ": staging too small");
+      return MSORT_ERROR_NOT_SUPPORTED;
+    }
+    MSORT_CUDA_TRY(cudaMemcpyAsync(c->pinned, dev, bytes, cudaMemcpyDeviceToHost, s));
+    MSORT_TRY(wait(what));
+    memcpy(host, c->pinned, bytes);
+    return MSORT_SUCCESS;
+  }
   // pull exchange: after the peers' reads, nobody may reuse its buffer
   msort_status barrier(RankIO* io) {
     LaunchScope ls(KC_NCCL, s);
@@ -335,16 +391,16 @@ struct NcclColl {
       (which == 0 ? me.hk : me.hv) = h;
       (which == 0 ? me.ok : me.ov) = (int64_t)((CUdeviceptr)p - base);
     }
-    MSORT_CUDA_TRY(cudaMemcpyAsync(io[0].ws.ipc_send, &me, sizeof(me), cudaMemcpyHostToDevice, s));
+    memcpy(c->pinned, &me, sizeof(me));
+    MSORT_CUDA_TRY(
+        cudaMemcpyAsync(io[0].ws.ipc_send, c->pinned, sizeof(me), cudaMemcpyHostToDevice, s));
     {
       LaunchScope ls(KC_NCCL, s);
       MSORT_NCCL_TRY(ncclAllGather(io[0].ws.ipc_send, io[0].ws.ipc_all, kIpcBytes, ncclUint8,
                                    c->comm, s));
     }
-    MSORT_CUDA_TRY(cudaMemcpyAsync(host, io[0].ws.ipc_all, kIpcBytes * c->world,
-                                   cudaMemcpyDeviceToHost, s));
-    // the host copy of `me` must outlive the async copy: wait for it here
-    MSORT_CUDA_TRY(cudaStreamSynchronize(s));
+    // (the pinned record must outlive the async upload: fetch waits for both)
+    MSORT_TRY(fetch(host, io[0].ws.ipc_all, kIpcBytes * c->world, "ipc handle gather"));
     return MSORT_SUCCESS;
   }
   // step 2 (after the sync): map every peer's exchange buffers (cached).
@@ -425,6 +481,14 @@ struct EmulColl {
     return MSORT_SUCCESS;
   }
   int rank_of(int local) const { return local; }
+  msort_status wait(const char* what) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    return e == cudaSuccess ? MSORT_SUCCESS : cuda_fail(e, what);
+  }
+  msort_status fetch(void* host, const void* dev, size_t bytes, const char* what) {
+    MSORT_CUDA_TRY(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s));
+    return wait(what);
+  }
   msort_status barrier(RankIO*) { return MSORT_SUCCESS; }  // one stream: program order
   msort_status ipc_publish(RankIO*, unsigned char*) { return MSORT_SUCCESS; }
   msort_status peer_bases(RankIO* io, const unsigned char*, bool,
@@ -514,8 +578,7 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
   const bool pull = pull_mode;
   std::vector<unsigned char> ipc_host(pull ? kIpcBytes * (size_t)p : 0);
   if (pull) MSORT_TRY(C.ipc_publish(io, ipc_host.data()));
-  MSORT_CUDA_TRY(cudaMemcpyAsync(S.data(), io[0].ws.split, S.size() * 8, cudaMemcpyDeviceToHost, s));
-  MSORT_CUDA_TRY(cudaStreamSynchronize(s));
+  MSORT_TRY(C.fetch(S.data(), io[0].ws.split, S.size() * 8, "split matrix"));
   if (split_out) memcpy(split_out, S.data(), S.size() * 8);
   // sanity: every rank's output count equals its input count
   for (int l = 0; l < nloc; ++l) {
@@ -597,6 +660,10 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
 msort_status dist_nccl(const void* in_keys, const void* in_vals, void* keys, void* vals, size_t n,
                        msort_dtype kd, msort_dtype vd, msort_comm_s* comm, void* ws,
                        cudaStream_t s, int64_t* split_out) {
+  if (comm->aborted) {
+    set_error("communicator was aborted after an earlier failure");
+    return MSORT_ERROR_NCCL;
+  }
   if (comm->world > kMaxWorld) {
     set_error("world too large");
     return MSORT_ERROR_NOT_SUPPORTED;
@@ -789,21 +856,29 @@ static msort_status tree_run(Coll& C, const std::vector<int>& ranks,
 msort_status tree_nccl(const void* in_keys, const void* in_vals, size_t n, msort_dtype kd,
                        msort_dtype vd, msort_comm_s* comm, void* root_k, void* root_v,
                        size_t root_cap, cudaStream_t s, int64_t* total_out) {
+  if (comm->aborted) {
+    set_error("communicator was aborted after an earlier failure");
+    return MSORT_ERROR_NCCL;
+  }
   const int p = comm->world;
   // every rank's size (one allgather, one host sync)
   uint64_t* d = nullptr;
   MSORT_CUDA_TRY(scratch_alloc((void**)&d, 8 * (size_t)(p + 1), s));
   std::vector<uint64_t> hn((size_t)p);
-  uint64_t mine = n;
-  cudaError_t e = cudaMemcpyAsync(d + p, &mine, 8, cudaMemcpyHostToDevice, s);
+  memcpy(comm->pinned, &n, 8);  // page-locked: no blocking copies (failure detection)
+  cudaError_t e = cudaMemcpyAsync(d + p, comm->pinned, 8, cudaMemcpyHostToDevice, s);
   ncclResult_t nr = e == cudaSuccess ? ncclAllGather(d + p, d, 1, ncclUint64, comm->comm, s)
                                      : ncclSuccess;
   if (e == cudaSuccess && nr == ncclSuccess)
-    e = cudaMemcpyAsync(hn.data(), d, 8 * (size_t)p, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && nr == ncclSuccess) e = cudaStreamSynchronize(s);
+    e = cudaMemcpyAsync(comm->pinned + 64, d, 8 * (size_t)p, cudaMemcpyDeviceToHost, s);
+  if (nr != ncclSuccess || e != cudaSuccess) {
+    cudaFreeAsync(d, s);
+    if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather (tree sizes)");
+    return cuda_fail(e, "tree sizes");
+  }
+  MSORT_TRY(wait_stream_nccl(comm, s, "tree sizes"));
+  memcpy(hn.data(), comm->pinned + 64, 8 * (size_t)p);
   cudaFreeAsync(d, s);
-  if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather (tree sizes)");
-  if (e != cudaSuccess) return cuda_fail(e, "tree sizes");
   std::vector<int64_t> nall(hn.begin(), hn.end());
   int64_t total = 0;
   for (int64_t v : nall) total += v;
@@ -852,14 +927,23 @@ msort_status comm_init(const void* idp, int rank, int world, msort_comm_s** out)
   memcpy(&id, idp, sizeof(id));
   ncclComm_t c;
   MSORT_NCCL_TRY(ncclCommInitRank(&c, world, id, rank));
-  *out = new msort_comm_s{c, rank, world, {}};
+  auto* cs = new msort_comm_s{c, rank, world, {}};
+  cs->pinned_bytes = std::max<size_t>(8 * (size_t)(world + 1) * world, kIpcBytes * world) + 4096;
+  if (cudaMallocHost(reinterpret_cast<void**>(&cs->pinned), cs->pinned_bytes) != cudaSuccess) {
+    ncclCommDestroy(c);
+    delete cs;
+    set_error("cudaMallocHost (communicator staging)");
+    return MSORT_ERROR_OUT_OF_MEMORY;
+  }
+  *out = cs;
   return MSORT_SUCCESS;
 }
 
 msort_status comm_destroy(msort_comm_s* c) {
   if (!c) return MSORT_SUCCESS;
   for (auto& kv : c->ipc_open) cudaIpcCloseMemHandle(kv.second);
-  ncclResult_t r = ncclCommDestroy(c->comm);
+  ncclResult_t r = c->aborted ? ncclSuccess : ncclCommDestroy(c->comm);
+  if (c->pinned) cudaFreeHost(c->pinned);
   delete c;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
   return MSORT_SUCCESS;

@@ -164,3 +164,46 @@ def test_nccl_one_rank(ms, orc):
     assert np.array_equal(_host(kd, np.int64), ek)
     assert np.array_equal(_host(vd, np.uint32), ev)
     comm.close()
+
+
+def test_nccl_wait_timeout_aborts(tmp_path):
+    """Failure detection (include/msort.h): with MSORT_NCCL_TIMEOUT_S set, a
+    distributed call whose stream does not drain in time (here: held up by a
+    1 s sleep kernel, standing in for a dead peer) returns MSORT_ERROR_NCCL,
+    aborts the communicator, and later calls on it fail at once.  (With one
+    rank the balanced sort needs no host wait, so the rank-tree call -- which
+    always waits for the shard sizes -- is the one that can be held up.)"""
+    import subprocess
+    import sys
+
+    code = r'''
+import os, sys, torch, torch.distributed as dist
+sys.path.insert(0, os.environ["ROOT"])
+import paper_2211_16479_b200 as ms
+dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29541", rank=0, world_size=1,
+                        device_id=torch.device("cuda", 0))
+comm = ms.Comm()
+k = torch.randint(0, 1000, (1 << 16,), dtype=torch.int32, device="cuda")
+s2 = torch.cuda.Stream()
+with torch.cuda.stream(s2):
+    torch.cuda._sleep(2_000_000_000)  # ~1 s on the call's stream
+try:
+    ms.msort_sort_distributed_tree(k, comm, stream=s2)
+    print("NO-ERROR")
+except ms.MsortError as e:
+    print("ERR1", "timed out" in str(e))
+try:
+    ms.msort_sort_distributed_tree(k, comm, stream=s2)
+    print("NO-ERROR2")
+except ms.MsortError as e:
+    print("ERR2", "aborted" in str(e))
+torch.cuda.synchronize()
+comm.close()
+'''
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MSORT_NCCL_TIMEOUT_S="0.05", ROOT=root)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=240)
+    assert "ERR1 True" in r.stdout and "ERR2 True" in r.stdout, r.stdout + r.stderr[-2000:]
