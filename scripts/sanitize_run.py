@@ -49,3 +49,25 @@ for mode in (0, 1):
 ms.set_exchange_mode(0)
 torch.cuda.synchronize()
 print("sanitize workload ok")
+
+# batched sorts (every length bin, host and device offsets), K6 mode, rank tree
+import numpy as np  # noqa: E402
+
+lens = [0, 1, 7, 32, 33, 100, 256, 1000, 2176, 5000, 8704, 20000, 3]
+off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+for dev_off in (False, True):
+    k = mi.keys_torch(int(off[-1]), 6, "u31", device="cuda")
+    v = torch.arange(k.numel(), dtype=torch.int32, device="cuda")
+    ms.msort_sort_segmented(k, torch.from_numpy(off).cuda() if dev_off else off, v)
+    for i in range(len(lens)):
+        check_sorted(k[off[i]:off[i + 1]]) if lens[i] > 1 else None
+ms.set_quad_mode(5)
+k = mi.keys_torch(8704 * 40 + 5, 7, "u31", device="cuda")
+ms.msort_sort(k)
+check_sorted(k)
+ms.set_quad_mode(0)
+rk, _ = ms.msort_sort_distributed_tree_emulated(
+    [mi.keys_torch(50000 + r, 8 + r, "u31", device="cuda") for r in range(3)])
+check_sorted(rk)
+torch.cuda.synchronize()
+print("sanitize workload ok")
