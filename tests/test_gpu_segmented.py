@@ -164,3 +164,38 @@ def test_segmented_repeat_and_streams(ms, orc):
     torch.cuda.synchronize()
     for k, off, kd in outs:
         assert np.array_equal(to_host(kd, np.int32), orc.sort_segmented(k, off))
+
+
+def test_segmented_concurrent_host_threads(ms, orc):
+    """Host threads calling the batched sort at once on their own streams share
+    the page-locked staging buffer (a mutex and an upload event order them);
+    every result must be its own table's."""
+    import threading
+
+    rng = np.random.default_rng(77)
+    jobs = []
+    for t in range(8):
+        lens = rng.integers(0, 12000, 150)
+        off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        k = _keys(int(off[-1]), 900 + t, "rand", np.int32)
+        jobs.append((k, off, to_dev(k), torch.cuda.Stream()))
+    torch.cuda.synchronize()
+    errs = []
+
+    def run(job):
+        k, off, kd, st = job
+        try:
+            for _ in range(3):  # re-sorting sorted segments is idempotent
+                ms.msort_sort_segmented(kd, off, stream=st)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(j,)) for j in jobs]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errs, errs
+    for k, off, kd, _ in jobs:
+        assert np.array_equal(to_host(kd, np.int32), orc.sort_segmented(k, off))
