@@ -173,6 +173,19 @@ msort_status msort_comm_unique_id(void *id_out);
  * Collective over all ranks; uses the current CUDA device. */
 msort_status msort_comm_init(const void *id, int rank, int world, msort_comm_t *out);
 
+/* Wrap an existing NCCL communicator (an ncclComm_t, e.g. the one of torch's
+ * NCCL process group) instead of creating one: rank and world are read from
+ * it (ncclCommUserRank / ncclCommCount); it must come from the same NCCL
+ * library (the torch wheel's libnccl.so.2, which this library links).
+ * NON-OWNING: msort_comm_destroy frees only the wrapper, and a failure
+ * detected by a distributed call marks the wrapper unusable without aborting
+ * the caller's communicator.  The caller must not run its own collectives on
+ * the communicator concurrently with a msort call (NCCL's rule for one
+ * communicator used from several streams). */
+msort_status msort_comm_wrap(void *nccl_comm, msort_comm_t *out);
+
+/* Free a communicator from msort_comm_init (destroys the NCCL communicator)
+ * or msort_comm_wrap (frees only the wrapper). */
 msort_status msort_comm_destroy(msort_comm_t comm);
 
 /* Distributed stable sort (re-designed: local sort, exact

@@ -44,7 +44,7 @@ EXPORTED = (
     "msort_tile_size", "msort_debug_set_quad", "msort_sort_host", "msort_debug_set_exchange",
     "msort_segmented_workspace_bytes", "msort_sort_segmented",
     "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
-    "msort_plan_tree_rounds", "msort_plan_tree_role",
+    "msort_plan_tree_rounds", "msort_plan_tree_role", "msort_comm_wrap",
 )
 
 
@@ -72,6 +72,7 @@ def _load():
     L.msort_comm_unique_id.argtypes = [vp]
     L.msort_comm_init.argtypes = [vp, i32, i32, c.POINTER(vp)]
     L.msort_comm_destroy.argtypes = [vp]
+    L.msort_comm_wrap.argtypes = [vp, c.POINTER(vp)]
     L.msort_sort_distributed.argtypes = [vp, vp, sz, i32, i32, vp, vp, i64p]
     L.msort_sort_distributed_ws.argtypes = [vp, vp, sz, i32, i32, vp, vp, sz, vp, i64p]
     L.msort_sort_distributed_emulated.argtypes = [c.POINTER(vp), c.POINTER(vp),
@@ -111,7 +112,8 @@ def _load():
               "msort_sort_distributed_emulated", "msort_plan_init", "msort_plan_candidates",
               "msort_plan_narrow", "msort_plan_fill", "msort_profile_read",
               "msort_segmented_workspace_bytes", "msort_sort_segmented",
-              "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated"):
+              "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
+              "msort_comm_wrap"):
         getattr(L, f).restype = i32
     return L
 
@@ -357,6 +359,27 @@ class Comm:
         if self.handle:
             _check(lib.msort_comm_destroy(self.handle), "msort_comm_destroy")
             self.handle = None
+
+    @classmethod
+    def from_torch(cls, group=None, device=None):
+        """Wrap the NCCL communicator of a torch NCCL process group
+        (include/msort.h msort_comm_wrap; non-owning).  One collective is run
+        first so torch has created its communicator."""
+        import torch.distributed as dist
+
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        pg = group or dist.group.WORLD
+        t = torch.zeros(1, device=dev)
+        dist.all_reduce(t, group=pg)
+        torch.cuda.synchronize(dev)
+        ptr = pg._get_backend(dev)._comm_ptr()
+        self = cls.__new__(cls)
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        h = ctypes.c_void_p()
+        _check(lib.msort_comm_wrap(ctypes.c_void_p(ptr), ctypes.byref(h)), "msort_comm_wrap")
+        self.handle = h
+        return self
 
 
 def msort_sort_distributed(keys: torch.Tensor, comm: Comm, vals: torch.Tensor | None = None,

@@ -26,6 +26,7 @@ msort_status dist_emulated(void* const* keys, void* const* vals, const size_t* n
 msort_status comm_unique_id(void* out);
 msort_status comm_init(const void* idp, int rank, int world, msort_comm_s** out);
 msort_status comm_destroy(msort_comm_s* c);
+msort_status comm_wrap(void* nccl_comm, msort_comm_s** out);
 int comm_world(msort_comm_s* c);
 
 // ---------------------------------------------------------------- errors
@@ -415,6 +416,15 @@ msort_status msort_comm_init(const void* id, int rank, int world, msort_comm_t* 
   }
   MSORT_TRY(check_device());
   return comm_init(id, rank, world, out);
+}
+
+msort_status msort_comm_wrap(void* nccl_comm, msort_comm_t* out) {
+  if (!nccl_comm || !out) {
+    set_error("bad argument to msort_comm_wrap");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  MSORT_TRY(check_device());
+  return comm_wrap(nccl_comm, out);
 }
 
 msort_status msort_comm_destroy(msort_comm_t comm) { return comm_destroy(comm); }

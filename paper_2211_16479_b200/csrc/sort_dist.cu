@@ -38,6 +38,7 @@ struct msort_comm_s {
   // (rank, handle) -- the workspace allocation is normally reused call to call
   std::map<std::pair<int, std::string>, void*> ipc_open;
   bool aborted = false;  // set when a failure aborted the NCCL communicator
+  bool owned = true;     // false: wraps a caller's communicator (never destroyed / aborted here)
   // page-locked staging for the small host<->device copies of a call (split
   // matrix, sizes, IPC records): copies from/to pageable memory would block
   // the host inside cudaMemcpyAsync, out of reach of the failure detection
@@ -79,14 +80,14 @@ static msort_status wait_stream_nccl(msort_comm_s* c, cudaStream_t s, const char
     if (q != cudaErrorNotReady) return cuda_fail(q, what);
     ncclResult_t ae = ncclSuccess;
     if (ncclCommGetAsyncError(c->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress) {
-      ncclCommAbort(c->comm);
+      if (c->owned) ncclCommAbort(c->comm);  // a borrowed communicator is its owner's to abort
       c->aborted = true;
       return nccl_fail(ae, what);
     }
     const double el =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (limit > 0 && el > limit) {
-      ncclCommAbort(c->comm);
+      if (c->owned) ncclCommAbort(c->comm);
       c->aborted = true;
       set_error(std::string(what) + ": timed out after " + std::to_string(el) +
                 " s (MSORT_NCCL_TIMEOUT_S); communicator aborted");
@@ -939,10 +940,29 @@ msort_status comm_init(const void* idp, int rank, int world, msort_comm_s** out)
   return MSORT_SUCCESS;
 }
 
+// Wrap an existing NCCL communicator (e.g. torch's, msort_comm_wrap): rank and
+// world come from NCCL itself; the caller keeps ownership.
+msort_status comm_wrap(void* nccl_comm, msort_comm_s** out) {
+  ncclComm_t c = static_cast<ncclComm_t>(nccl_comm);
+  int rank = 0, world = 0;
+  MSORT_NCCL_TRY(ncclCommUserRank(c, &rank));
+  MSORT_NCCL_TRY(ncclCommCount(c, &world));
+  auto* cs = new msort_comm_s{c, rank, world, {}};
+  cs->owned = false;
+  cs->pinned_bytes = std::max<size_t>(8 * (size_t)(world + 1) * world, kIpcBytes * world) + 4096;
+  if (cudaMallocHost(reinterpret_cast<void**>(&cs->pinned), cs->pinned_bytes) != cudaSuccess) {
+    delete cs;
+    set_error("cudaMallocHost (communicator staging)");
+    return MSORT_ERROR_OUT_OF_MEMORY;
+  }
+  *out = cs;
+  return MSORT_SUCCESS;
+}
+
 msort_status comm_destroy(msort_comm_s* c) {
   if (!c) return MSORT_SUCCESS;
   for (auto& kv : c->ipc_open) cudaIpcCloseMemHandle(kv.second);
-  ncclResult_t r = c->aborted ? ncclSuccess : ncclCommDestroy(c->comm);
+  ncclResult_t r = (c->aborted || !c->owned) ? ncclSuccess : ncclCommDestroy(c->comm);
   if (c->pinned) cudaFreeHost(c->pinned);
   delete c;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");

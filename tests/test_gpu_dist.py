@@ -207,3 +207,33 @@ comm.close()
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=240)
     assert "ERR1 True" in r.stdout and "ERR2 True" in r.stdout, r.stdout + r.stderr[-2000:]
+
+
+def test_comm_wrap_torch(ms, orc):
+    """msort_comm_wrap: the library runs the distributed sort (and the tree)
+    on torch's own NCCL communicator; closing the wrapper leaves torch's
+    process group usable."""
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    comm = ms.Comm.from_torch()
+    assert (comm.rank, comm.world) == (0, 1)
+    n = 90001
+    k = mi.keys(n, 79, ("mod", 77))
+    v = np.arange(n, dtype=np.uint32)
+    kd, vd = _dev(k), _dev(v)
+    ms.msort_sort_distributed(kd, comm, vals=vd)
+    rk, _ = ms.msort_sort_distributed_tree(_dev(k), comm)
+    torch.cuda.synchronize()
+    ek, ev = orc.sort(k, v)
+    assert np.array_equal(_host(kd, np.int64), ek)
+    assert np.array_equal(_host(vd, np.uint32), ev)
+    assert np.array_equal(_host(rk, np.int64), ek)
+    comm.close()
+    t = torch.ones(1, device="cuda")
+    dist.all_reduce(t)  # torch's communicator still works
+    assert float(t.item()) == 1.0
