@@ -330,8 +330,32 @@ def sort(x: torch.Tensor) -> torch.Tensor:
     return msort_sort_out(x, torch.empty_like(x))[0]
 
 
+def sort_(x: torch.Tensor) -> torch.Tensor:
+    """In-place stable sort on the current stream (SURVEY §8(b) Python layer)."""
+    return msort_sort(x)
+
+
 def sort_pairs(k: torch.Tensor, v: torch.Tensor):
+    """Functional stable sort of (k, v) by key: sorted copies (inputs unchanged)."""
     return msort_sort_pairs(k.clone(), v.clone())
+
+
+_COMMS = {}
+
+
+def sort_distributed(x: torch.Tensor, group=None, vals: torch.Tensor | None = None):
+    """In-place collective stable sort over a torch NCCL process group (default:
+    the world): rank r ends with the global positions [K_r, K_r + n_r) of the
+    rank-major concatenation.  The library's own NCCL communicator for the
+    group is created on first use (id broadcast over the group) and cached."""
+    import torch.distributed as dist
+
+    key = (id(group), x.device.index)
+    comm = _COMMS.get(key)
+    if comm is None:
+        comm = _COMMS[key] = Comm(group)
+    msort_sort_distributed(x, comm, vals=vals)
+    return (x, vals) if vals is not None else x
 
 
 # ------------------------------------------------------------- distributed

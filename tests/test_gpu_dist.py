@@ -237,3 +237,32 @@ def test_comm_wrap_torch(ms, orc):
     t = torch.ones(1, device="cuda")
     dist.all_reduce(t)  # torch's communicator still works
     assert float(t.item()) == 1.0
+
+
+def test_python_layer_calls(ms, orc):
+    """SURVEY §8(b) Python layer: sort (clone), sort_ (in place), sort_pairs,
+    sort_distributed (in place, cached communicator)."""
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    n = 30011
+    k = mi.keys(n, 81, ("mod", 500))
+    v = np.arange(n, dtype=np.uint32)
+    kd = _dev(k)
+    out = ms.sort(kd)
+    assert np.array_equal(_host(out, np.int64), orc.sort(k))
+    assert np.array_equal(_host(kd, np.int64), k)  # unchanged
+    ms.sort_(kd)
+    assert np.array_equal(_host(kd, np.int64), orc.sort(k))
+    sk, sv = ms.sort_pairs(_dev(k), _dev(v))
+    ek, ev = orc.sort(k, v)
+    assert np.array_equal(_host(sk, np.int64), ek) and np.array_equal(_host(sv, np.uint32), ev)
+    kd2, vd2 = _dev(k), _dev(v)
+    for _ in range(2):  # second call reuses the cached communicator
+        kk, vv = ms.sort_distributed(kd2, vals=vd2)
+    torch.cuda.synchronize()
+    assert np.array_equal(_host(kk, np.int64), ek) and np.array_equal(_host(vv, np.uint32), ev)
