@@ -126,18 +126,21 @@ msort_status msort_sort_out_ws(const void *in_keys, const void *in_vals, void *k
  * slice alone (P:77-84 applied per segment).
  *   seg_offsets  nseg + 1 int64: off[0] = 0, non-decreasing, off[nseg] = n
  *                (empty segments allowed).  In HOST memory it is read during
- *                the call; in DEVICE memory (cudaPointerGetAttributes says
- *                so) the segments are classified and the table checked on the
- *                device, and the call synchronises `stream` once to learn how
- *                many long segments there are.
+ *                the call (from 2^15 segments on it is copied up and
+ *                classified on the device, as below); in DEVICE memory
+ *                (cudaPointerGetAttributes says so) the segments are
+ *                classified and the table checked on the device, and the call
+ *                synchronises `stream` once to learn how many long segments
+ *                there are.
  *   keys, vals   device arrays of n elements (vals NULL with MSORT_NONE).
  *   ws           device workspace, 256-byte aligned, at least
  *                msort_segmented_workspace_bytes(n, nseg, ...) bytes, not
  *                overlapping keys/vals.
  * Segments of <= 256 elements are sorted one per warp, <= msort_tile_size
  * one per CTA, longer ones by the single-array sort (one after another).
- * With host offsets the call is asynchronous on `stream` (its tables are
- * staged through page-locked memory and uploaded on the stream).
+ * With a host table of fewer than 2^15 segments the call is asynchronous on
+ * `stream` (its tables are staged through page-locked memory and uploaded on
+ * the stream).
  * Errors: INVALID_VALUE for bad offsets (not starting at 0, decreasing, not
  * ending at n -- found on the device for device offsets, before any key is
  * touched), NULL pointers with n > 0, a bad dtype or a short workspace. */

@@ -274,6 +274,7 @@ static size_t seg_ws_bytes(size_t n, size_t nseg, msort_dtype kd, msort_dtype vd
   size_t b = align_up(n * dtype_size(kd), 256);
   if (vd != MSORT_NONE) b += align_up(n * 4, 256);
   b += align_up(8 * (8 * nseg + 2 * tiles + 8), 256);  // host tables (mid bins included)
+  b += align_up(8 * (nseg + 1), 256);  // a long host offsets table, uploaded
   // device-resident offsets: the classifier's lists (<= n / 257, n / 2177,
   // n / (T + 1) entries of 16 bytes) and counters
   b += align_up(16 * (n / 33 + 1), 256) + align_up(16 * (n / 257 + 1), 256) +

@@ -900,6 +900,7 @@ struct Kernels {
   // tile-sort launch per buffer parity plus ONE fused merge launch over all
   // of them (SegFused: all levels of all long segments as one dataflow).
   static constexpr int kSegW8 = 256;  // warp classes: <= 32 (VW = 1), <= 256 (VW = 8)
+  static constexpr int64_t kSegUploadMin = 1 << 15;  // host tables this long are classified on the device
   static constexpr int kSegNTM = 128, kSegVTM = 17, kSegM = kSegNTM * kSegVTM;  // CTA class
   using SegF = SegFused<K>;
   // off: nseg + 1 offsets, in host memory (dev_off false) or device memory.
@@ -918,6 +919,22 @@ struct Kernels {
     if (PAIRS) {
       wv = reinterpret_cast<uint32_t*>(w);
       w += align_up((size_t)n * 4, 256);
+    }
+    // Many segments with a host table: a host pass over them costs ~3 ns
+    // each, so upload the table (page-locked staging) and classify it on the
+    // device like a device-resident table (one synchronisation).
+    if (!dev_off && (int64_t)nseg >= kSegUploadMin) {
+      int64_t* doff = reinterpret_cast<int64_t*>(w);
+      w += align_up(8 * (nseg + 1), 256);
+      int64_t* h = nullptr;
+      MSORT_TRY(staging_acquire(8 * (nseg + 1), reinterpret_cast<void**>(&h)));
+      std::memcpy(h, off, 8 * (nseg + 1));
+      const cudaError_t e =
+          cudaMemcpyAsync(doff, h, 8 * (nseg + 1), cudaMemcpyHostToDevice, s);
+      MSORT_TRY(staging_release(s));
+      if (e != cudaSuccess) return cuda_fail(e, "segment table upload");
+      off = doff;
+      dev_off = true;
     }
     // ---- classification.  Segments of <= 32 elements are found by the tiny
     // kernel itself from the offsets table; the longer ones are listed: the

@@ -199,3 +199,15 @@ def test_segmented_concurrent_host_threads(ms, orc):
     assert not errs, errs
     for k, off, kd, _ in jobs:
         assert np.array_equal(to_host(kd, np.int32), orc.sort_segmented(k, off))
+
+
+@pytest.mark.parametrize("pairs", [False, True])
+def test_long_host_table(ms, orc, pairs):
+    """A host table of >= 2^15 segments is uploaded and classified on the device
+    (Kernels::sort_segmented); mixed lengths so every bin is used."""
+    rng = np.random.default_rng(41)
+    lens = rng.integers(0, 40, 100000)
+    lens[rng.integers(0, lens.size, 30)] = rng.integers(300, 30000, 30)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    k = _keys(int(off[-1]), 42, "dup", np.int32)
+    _run(ms, orc, k, off, pairs, dev_off=False)
