@@ -116,7 +116,10 @@ __device__ __forceinline__ void warp_sort_segment(K* __restrict__ keys,
 // 32-element bitonic network runs on all S registers (S independent shuffle
 // chains: S loads in flight and S-way ILP for these latency-bound segments).
 // Longer or trivial segments are left to the other kernels.
-constexpr int kSegPerWarp = 4;
+#ifndef MSORT_SEG_PER_WARP
+#define MSORT_SEG_PER_WARP 4
+#endif
+constexpr int kSegPerWarp = MSORT_SEG_PER_WARP;
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(128)
     kseg_tiny_sort(K* __restrict__ keys, uint32_t* __restrict__ vals,
