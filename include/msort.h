@@ -371,6 +371,17 @@ int msort_debug_set_quad(int mode);
  * buffers); environment MSORT_EXCHANGE=pull selects it too.  Returns 0. */
 int msort_debug_set_exchange(int mode);
 
+/* Tuning entry point of the K6 experiment (scripts/k6_experiment.py): one
+ * 4-way pass over int32 keys, src -> dst, with caller-computed tiles:
+ * `tiles` is a device array of ntiles records of 9 int64 {out, src[4], n[4]}
+ * (output index of the tile's first key; first key of the A, B, C, D
+ * windows in src; their lengths), each tile <= 8568 keys, the windows being
+ * the exact 4-way co-rank bounds of the tile (merge() of P:107 per level,
+ * ties A < B < C < D).  Asynchronous on `stream`; returns the cudaError_t of
+ * the launch (0 on success).  Not part of the product path. */
+int msort_debug_k6_pass(const void *src, void *dst, const void *tiles, int64_t ntiles,
+                        void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -44,7 +44,7 @@ EXPORTED = (
     "msort_tile_size", "msort_debug_set_quad", "msort_sort_host", "msort_debug_set_exchange",
     "msort_segmented_workspace_bytes", "msort_sort_segmented",
     "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
-    "msort_plan_tree_rounds", "msort_plan_tree_role", "msort_comm_wrap",
+    "msort_plan_tree_rounds", "msort_plan_tree_role", "msort_comm_wrap", "msort_debug_k6_pass",
 )
 
 
@@ -73,6 +73,8 @@ def _load():
     L.msort_comm_init.argtypes = [vp, i32, i32, c.POINTER(vp)]
     L.msort_comm_destroy.argtypes = [vp]
     L.msort_comm_wrap.argtypes = [vp, c.POINTER(vp)]
+    L.msort_debug_k6_pass.argtypes = [vp, vp, vp, c.c_int64, vp]
+    L.msort_debug_k6_pass.restype = i32
     L.msort_sort_distributed.argtypes = [vp, vp, sz, i32, i32, vp, vp, i64p]
     L.msort_sort_distributed_ws.argtypes = [vp, vp, sz, i32, i32, vp, vp, sz, vp, i64p]
     L.msort_sort_distributed_emulated.argtypes = [c.POINTER(vp), c.POINTER(vp),
