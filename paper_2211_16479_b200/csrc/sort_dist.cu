@@ -93,7 +93,7 @@ static msort_status wait_stream_nccl(msort_comm_s* c, cudaStream_t s, const char
                 " s (MSORT_NCCL_TIMEOUT_S); communicator aborted");
       return MSORT_ERROR_NCCL;
     }
-    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    if (spin > 256) std::this_thread::sleep_for(std::chrono::microseconds(5));  // keep the wait tight
   }
 }
 
