@@ -415,6 +415,31 @@ def main():
                  "frac": round(ach / 770.0, 4), "bytes_sent": sent, "bytes_received": recv,
                  "avg_exchange_ms": round(xms / xl, 4),
                  "peak_source": "measured peer copy per direction (B200_PROFILING.md; 900 nominal)"}
+        # the same exchange against a uniform NCCL all-to-all of
+        # the same byte count (torch's all_to_all_single, equal splits), timed
+        # here outside the measured region; the slowest rank is reported
+        try:
+            buf = torch.empty(n, dtype=torch.int32, device=dev)
+            out_a2a = torch.empty_like(buf)
+            for _ in range(2):
+                dist.all_to_all_single(out_a2a, buf)
+            torch.cuda.synchronize()
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record()
+            for _ in range(5):
+                dist.all_to_all_single(out_a2a, buf)
+            eb.record()
+            torch.cuda.synchronize()
+            a2a_ms = ea.elapsed_time(eb) / 5
+            t = torch.tensor([a2a_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            a2a_ms = float(t.item())
+            a2a_gbs = n * wk * (world - 1) / world / (a2a_ms / 1e3) / 1e9
+            xroof["uniform_alltoall_gbs"] = round(a2a_gbs, 1)
+            xroof["frac_of_uniform_alltoall"] = round(ach / a2a_gbs, 4)
+            del buf, out_a2a
+        except Exception as e:  # noqa: BLE001 -- context only, never fail the line
+            xroof["uniform_alltoall_error"] = str(e)[:200]
 
     # end to end through the public API with HOST buffers: every step uploads
     # its input from pinned host memory, sorts, and copies the sorted keys back
