@@ -28,6 +28,7 @@ on a bounded sample of the same workload on this host's cores (rank 0 only).
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -60,6 +61,26 @@ def parse():
     ap.add_argument("--exchange", choices=["alltoall", "pull"], default="alltoall",
                     help="N > 1: NCCL all-to-all + k-way merge, or the fused pull exchange")
     return ap.parse_args()
+
+
+def expected_digest(world: int, rank: int, n: int):
+    """The oracle's SHA-256 of rank `rank`'s expected C5 output slice at
+    `world` ranks (tests/golden/c5_digests.json), or None."""
+    if n != N_PER_GPU:
+        return None
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "c5_digests.json")) as f:
+            d = json.load(f)["digests"].get(str(world))
+        return d[rank]["sha256"] if d else None
+    except Exception:
+        return None
+
+
+def host_digest(a) -> str:
+    import numpy as np
+
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.view(np.uint8)).hexdigest()
 
 
 def load_peaks():
@@ -131,25 +152,40 @@ class ClockSampler:
                                     if r[4].replace(".", "").isdigit()), default=None)}
 
 
-def cpu_baseline(n_sample: int, samples: int):
-    """The oracle, as it stands, on bounded samples of the workload (rank 0)."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(n_sample: int, samples: int, seed: int = SEED0 + 100):
+    """the oracle, as it stands (single-threaded textbook
+    top-down merge sort), timed on the host (rank 0).  The default sample is
+    one full C5 shard: rank 0's 2^28 keys (seed 4)."""
     import msort_inputs as mi
     import oracle
 
     oracle.build()
     t = 0.0
     for s in range(samples):
-        k = mi.keys(n_sample, SEED0 + 100 + s, "u31")
+        k = mi.keys(n_sample, seed + s, "u31")
         t0 = time.perf_counter()
         oracle.sort_inplace(k)
         t += time.perf_counter() - t0
     return {"value": n_sample * samples / t, "unit": "keys/s", "cores": 1, "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"{samples} x 2^{n_sample.bit_length() - 1} int32 keys uniform [0,2^31) "
-                      f"(same generator as the workload), single-threaded top-down merge sort "
-                      f"(oracle/msort_oracle.c), {t:.1f} s of CPU"}
+                      f"(seed {seed}{'' if samples == 1 else '+i'}; seed 4 = the rank-0 C5 shard), "
+                      f"single-threaded top-down merge sort (oracle/msort_oracle.c), "
+                      f"{t:.1f} s of CPU"}
 
 
-def cpu_paper_mp(n_sample: int):
+def cpu_paper_mp(n_sample: int, seed: int = SEED0 + 200):
     """SURVEY.md §8(d) O-c: the paper's multiprocessing merge sort (chunks of
     ceil(n/c) sorted in parallel, then pairwise merges) re-created
     on host threads by the oracle library, all host cores, one 2^k sample."""
@@ -157,12 +193,13 @@ def cpu_paper_mp(n_sample: int):
     import oracle
 
     cores = len(os.sched_getaffinity(0))
-    k = mi.keys(n_sample, SEED0 + 200, "u31")
+    k = mi.keys(n_sample, seed, "u31")
     t0 = time.perf_counter()
     oracle.paper_mp_inplace(k, None, cores)
     t = time.perf_counter() - t0
     return {"value": n_sample / t, "unit": "keys/s", "cores": cores, "kind": "oracle_paper_mp",
-            "sample": f"2^{n_sample.bit_length() - 1} int32 keys uniform [0,2^31), the paper's "
+            "cpu_model": cpu_model(),
+            "sample": f"2^{n_sample.bit_length() - 1} int32 keys uniform [0,2^31) (seed {seed}), the paper's "
                       f"multiprocessing merge sort on {cores} host threads "
                       f"(oracle/msort_oracle.c msort_oracle_paper_mp), {t:.1f} s"}
 
@@ -350,19 +387,32 @@ def main():
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
 
-    # verify the last step's output (sorted, same multiset sum, ranks ordered)
-    ok = bool((kout[1:] >= kout[:-1]).all()) if n > 1 else True
-    ok &= int(kout.sum(dtype=torch.int64)) == int(kin.sum(dtype=torch.int64)) if world == 1 else True
+    # verify the last step's output BIT FOR BIT: SHA-256 of this rank's slice
+    # against the oracle's digest (tests/golden/c5_digests.json, written by
+    # tests/golden/make_c5_digests.py from oracle/ only) for p = 1, 2, 4, 8 at
+    # the C5 size; other sizes / world sizes fall back to order + multiset sum
+    # + rank edges.  Every rank's verdict is combined (MIN over ranks).
+    exp = expected_digest(world, rank, n)
+    if exp is not None:
+        got = host_digest(kout.cpu().numpy())
+        ok = got == exp
+        vmethod = "sha256 of every rank's output vs the oracle's digest (tests/golden/c5_digests.json)"
+    else:
+        ok = bool((kout[1:] >= kout[:-1]).all()) if n > 1 else True
+        vmethod = "order + multiset sum (+ rank edges); no oracle digest for this size / world"
+        if world == 1:
+            ok &= int(kout.sum(dtype=torch.int64)) == int(kin.sum(dtype=torch.int64))
     if world > 1:
-        edge = torch.tensor([int(kout[0]), int(kout[-1])], dtype=torch.int64, device=dev)
-        edges = [torch.zeros_like(edge) for _ in range(world)]
-        dist.all_gather(edges, edge)
-        e = torch.stack(edges).cpu().numpy()
-        ok &= bool(all(e[r][1] <= e[r + 1][0] for r in range(world - 1)))
-        s_in = torch.tensor([int(kin.sum(dtype=torch.int64)), int(kout.sum(dtype=torch.int64))],
-                            dtype=torch.int64, device=dev)
-        dist.all_reduce(s_in)
-        ok &= int(s_in[0]) == int(s_in[1])
+        if exp is None:
+            edge = torch.tensor([int(kout[0]), int(kout[-1])], dtype=torch.int64, device=dev)
+            edges = [torch.zeros_like(edge) for _ in range(world)]
+            dist.all_gather(edges, edge)
+            e = torch.stack(edges).cpu().numpy()
+            ok &= bool(all(e[r][1] <= e[r + 1][0] for r in range(world - 1)))
+            s_in = torch.tensor([int(kin.sum(dtype=torch.int64)), int(kout.sum(dtype=torch.int64))],
+                                dtype=torch.int64, device=dev)
+            dist.all_reduce(s_in)
+            ok &= int(s_in[0]) == int(s_in[1])
         okt = torch.tensor([1 if ok else 0], device=dev)
         dist.all_reduce(okt, op=dist.ReduceOp.MIN)
         ok = bool(okt.item())
@@ -418,9 +468,19 @@ def main():
         # the same exchange against a uniform NCCL all-to-all of
         # the same byte count (torch's all_to_all_single, equal splits), timed
         # here outside the measured region; the slowest rank is reported
+        # every rank must agree before entering the collectives: a local
+        # allocation failure must not leave the other ranks waiting
+        buf = out_a2a = None
         try:
             buf = torch.empty(n, dtype=torch.int32, device=dev)
             out_a2a = torch.empty_like(buf)
+            okf = 1
+        except Exception as e:  # noqa: BLE001 -- context only, never fail the line
+            xroof["uniform_alltoall_error"] = str(e)[:200]
+            okf = 0
+        okt = torch.tensor([okf], device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if int(okt.item()) == 1:
             for _ in range(2):
                 dist.all_to_all_single(out_a2a, buf)
             torch.cuda.synchronize()
@@ -437,9 +497,7 @@ def main():
             a2a_gbs = n * wk * (world - 1) / world / (a2a_ms / 1e3) / 1e9
             xroof["uniform_alltoall_gbs"] = round(a2a_gbs, 1)
             xroof["frac_of_uniform_alltoall"] = round(ach / a2a_gbs, 4)
-            del buf, out_a2a
-        except Exception as e:  # noqa: BLE001 -- context only, never fail the line
-            xroof["uniform_alltoall_error"] = str(e)[:200]
+        del buf, out_a2a
 
     # end to end through the public API with HOST buffers: every step uploads
     # its input from pinned host memory, sorts, and copies the sorted keys back
@@ -476,9 +534,10 @@ def main():
                 fe[i].record(strs[i])
             torch.cuda.synchronize()
             te = max(f0.elapsed_time(fe[i]) for i in range(NS))
+            exp0 = expected_digest(1, 0, n)
             for i in range(NS):
                 o = h_out[i].numpy()
-                ok &= bool(np.all(o[1:] >= o[:-1]))
+                ok &= (host_digest(o) == exp0) if exp0 else bool(np.all(o[1:] >= o[:-1]))
             path = ("msort_sort_host (pinned host -> device -> sort -> pinned host), "
                     f"steps rotate over {NS} streams")
         else:
@@ -500,7 +559,8 @@ def main():
             f1.record(stream)
             barrier()
             te = f0.elapsed_time(f1)
-            ok &= bool(np.all(h_out.numpy()[1:] >= h_out.numpy()[:-1]))
+            o = h_out.numpy()
+            ok &= (host_digest(o) == exp) if exp else bool(np.all(o[1:] >= o[:-1]))
             path = "pinned host -> cudaMemcpyAsync -> msort_sort_distributed_out_ws -> pinned host"
         if world > 1:
             t = torch.tensor([te], dtype=torch.float64, device=dev)
@@ -522,8 +582,8 @@ def main():
 
     cpu = cpu_mp = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(1 << 24, 3)
-        cpu_mp = cpu_paper_mp(1 << 26)
+        cpu = cpu_baseline(n, 1, SEED0)       # O-1 on the full rank-0 shard
+        cpu_mp = cpu_paper_mp(n, SEED0)       # O-c on the same shard, all host cores
 
     if rank == 0:
         value = world * n * args.steps / (ms_total / 1e3)
@@ -554,6 +614,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks,
             "verified": ok,
+            "verification": vmethod,
         }
         print(json.dumps(line), flush=True)
     if comm is not None:

@@ -76,10 +76,10 @@ typedef struct msort_comm_s *msort_comm_t;
 
 /* Stable ascending sort of keys[0..n) in place.  Workspace of
  * msort_workspace_bytes(n, key_dtype, MSORT_NONE, 1) bytes is taken with
- * cudaMallocAsync/cudaFreeAsync on `stream`, from the device's default memory
- * pool; the library raises that pool's release threshold once (its freed
- * blocks stay reserved for the next call; cudaMemPoolTrimTo returns them).
- * The same holds for every call that allocates scratch itself. */
+ * cudaMallocFromPoolAsync/cudaFreeAsync on `stream` from the library's own
+ * memory pool for the current device (created on first use; its freed blocks
+ * stay reserved for the next call).  The device's default pool is never
+ * modified.  The same holds for every call that allocates scratch itself. */
 msort_status msort_sort(void *keys, size_t n, msort_dtype key_dtype, msort_stream_t stream);
 
 /* Stable ascending sort of (keys, vals) pairs by key; vals travel with their
@@ -343,19 +343,14 @@ int64_t msort_launch_count(void);
 /* Tile size (elements) used for key dtype with/without payload. */
 int msort_tile_size(msort_dtype key_dtype, msort_dtype val_dtype);
 
-/* Tuning/testing knob for keys-only sorts: how merge levels are grouped into
- * HBM passes.  mode 0 (default): one 2-way level per pass (the fused K3
- * dataflow only); 1: two levels per pass (4-way merge tree, K3Q) while every
- * CTA gets >= 2 segments, the remaining levels 2-way; 2: 4-way passes whenever
- * >= 2 levels remain (small inputs too -- for tests); 4: every pair of levels
- * as a K3X pass (4-way super-tiles between X-/Y-side boundary states found
- * just in time by a searcher warp, no nested searches); 5: every pair of levels
- * as a K6 pass (4-byte keys: tiles between X-side states computed by a
- * partition kernel, cut at Y-side states when oversized, merged in two rounds
- * by the tile sort's merge engine; 8-byte keys fall back to mode 0).  The result is the same
- * in every mode (the stable sort is unique); process-wide, not thread-safe
- * against concurrent sorts.  Overrides the MSORT_QUAD environment variable.
- * Returns 0. */
+/* Testing knob for keys-only sorts: how merge levels are grouped into HBM
+ * passes.  mode 0 (default): every 2-way level in the fused K3 dataflow;
+ * mode 5: every pair of levels as one K6 4-way pass (4-byte keys; tiles from
+ * a partition kernel, merged in two rounds by the tile sort's merge engine;
+ * 8-byte keys keep mode 0).  Other values select mode 0.  The result is the
+ * same in every mode (the stable sort is unique).  Process-wide (an atomic:
+ * a concurrent sort sees either mode); overrides the MSORT_QUAD environment
+ * variable.  Returns 0. */
 int msort_debug_set_quad(int mode);
 
 /* Exchange mode of the distributed sort (D3+D4).  mode 0 (default): one NCCL
@@ -370,17 +365,6 @@ int msort_debug_set_quad(int mode);
  * through msort_sort_distributed_emulated (the same kernels, peers = local
  * buffers); environment MSORT_EXCHANGE=pull selects it too.  Returns 0. */
 int msort_debug_set_exchange(int mode);
-
-/* Tuning entry point of the K6 experiment (scripts/k6_experiment.py): one
- * 4-way pass over int32 keys, src -> dst, with caller-computed tiles:
- * `tiles` is a device array of ntiles records of 9 int64 {out, src[4], n[4]}
- * (output index of the tile's first key; first key of the A, B, C, D
- * windows in src; their lengths), each tile <= 8568 keys, the windows being
- * the exact 4-way co-rank bounds of the tile (merge() of P:107 per level,
- * ties A < B < C < D).  Asynchronous on `stream`; returns the cudaError_t of
- * the launch (0 on success).  Not part of the product path. */
-int msort_debug_k6_pass(const void *src, void *dst, const void *tiles, int64_t ntiles,
-                        void *stream);
 
 #ifdef __cplusplus
 }

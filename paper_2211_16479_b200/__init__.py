@@ -44,7 +44,7 @@ EXPORTED = (
     "msort_tile_size", "msort_debug_set_quad", "msort_sort_host", "msort_debug_set_exchange",
     "msort_segmented_workspace_bytes", "msort_sort_segmented",
     "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
-    "msort_plan_tree_rounds", "msort_plan_tree_role", "msort_comm_wrap", "msort_debug_k6_pass",
+    "msort_plan_tree_rounds", "msort_plan_tree_role", "msort_comm_wrap",
 )
 
 
@@ -73,8 +73,6 @@ def _load():
     L.msort_comm_init.argtypes = [vp, i32, i32, c.POINTER(vp)]
     L.msort_comm_destroy.argtypes = [vp]
     L.msort_comm_wrap.argtypes = [vp, c.POINTER(vp)]
-    L.msort_debug_k6_pass.argtypes = [vp, vp, vp, c.c_int64, vp]
-    L.msort_debug_k6_pass.restype = i32
     L.msort_sort_distributed.argtypes = [vp, vp, sz, i32, i32, vp, vp, i64p]
     L.msort_sort_distributed_ws.argtypes = [vp, vp, sz, i32, i32, vp, vp, sz, vp, i64p]
     L.msort_sort_distributed_emulated.argtypes = [c.POINTER(vp), c.POINTER(vp),
@@ -342,6 +340,9 @@ def sort_pairs(k: torch.Tensor, v: torch.Tensor):
     return msort_sort_pairs(k.clone(), v.clone())
 
 
+# (group, device index) -> Comm.  Keyed by the group OBJECT (hashed by
+# identity and kept alive by the key), so a destroyed group whose id() is
+# reused can never pick up a stale communicator.
 _COMMS = {}
 
 
@@ -352,7 +353,8 @@ def sort_distributed(x: torch.Tensor, group=None, vals: torch.Tensor | None = No
     group is created on first use (id broadcast over the group) and cached."""
     import torch.distributed as dist
 
-    key = (id(group), x.device.index)
+    g = group if group is not None else dist.group.WORLD
+    key = (g, x.device.index)
     comm = _COMMS.get(key)
     if comm is None:
         comm = _COMMS[key] = Comm(group)
@@ -368,6 +370,7 @@ class Comm:
     def __init__(self, group=None):
         import torch.distributed as dist
 
+        self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         idb = ctypes.create_string_buffer(128)
@@ -400,6 +403,7 @@ class Comm:
         torch.cuda.synchronize(dev)
         ptr = pg._get_backend(dev)._comm_ptr()
         self = cls.__new__(cls)
+        self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         h = ctypes.c_void_p()
@@ -415,6 +419,8 @@ def msort_sort_distributed(keys: torch.Tensor, comm: Comm, vals: torch.Tensor | 
     _check_tensor(keys, "keys")
     if vals is not None:
         _check_tensor(vals, "vals")
+        if vals.numel() != keys.numel() or vals.device != keys.device:
+            raise ValueError("keys/vals size or device mismatch")
     n = keys.numel()
     kd, vd = _dt(keys), _vdt(vals)
     if ws is None:
@@ -435,6 +441,17 @@ def msort_sort_distributed_out(in_keys: torch.Tensor, keys_out: torch.Tensor, co
     """Out-of-place collective sort: in_keys (unchanged) -> this rank's slice."""
     _check_tensor(in_keys, "in_keys")
     _check_tensor(keys_out, "keys_out")
+    if keys_out.numel() != in_keys.numel() or keys_out.dtype != in_keys.dtype or \
+            keys_out.device != in_keys.device:
+        raise ValueError("in/out keys mismatch (size, dtype or device)")
+    if (in_vals is None) != (vals_out is None):
+        raise ValueError("give both in_vals and vals_out, or neither")
+    if in_vals is not None:
+        _check_tensor(in_vals, "in_vals")
+        _check_tensor(vals_out, "vals_out")
+        if in_vals.numel() != in_keys.numel() or vals_out.numel() != in_keys.numel() or \
+                in_vals.dtype != vals_out.dtype:
+            raise ValueError("in_vals / vals_out must match the keys' size and each other's dtype")
     n = in_keys.numel()
     kd, vd = _dt(in_keys), _vdt(in_vals)
     if ws is None:
@@ -489,7 +506,7 @@ def msort_sort_distributed_tree(in_keys: torch.Tensor, comm: Comm, in_vals=None,
     n = in_keys.numel()
     kd, vd = _dt(in_keys), _vdt(in_vals)
     t = torch.tensor([n], dtype=torch.int64, device=in_keys.device)
-    dist.all_reduce(t)  # every rank: the global size
+    dist.all_reduce(t, group=getattr(comm, "group", None))  # the global size, over comm's group
     total = int(t.item())
     if comm.rank == 0 and root_keys is None:
         root_keys = torch.empty(total, dtype=in_keys.dtype, device=in_keys.device)
@@ -615,7 +632,7 @@ def set_exchange_mode(mode: int) -> None:
 
 def set_quad_mode(mode: int) -> None:
     """Merge-level grouping for keys-only sorts (include/msort.h
-    msort_debug_set_quad): 0 two-way levels only, 1 auto, 2 force 4-way."""
+    msort_debug_set_quad): 0 two-way levels only (default), 5 K6 4-way passes."""
     lib.msort_debug_set_quad(int(mode))
 
 

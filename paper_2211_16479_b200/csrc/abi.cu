@@ -79,21 +79,44 @@ LaunchScope::~LaunchScope() {
   }
 }
 
+// The library's own stream-ordered pool, one per device (created on first
+// use).  Its release threshold is raised so freed blocks stay reserved for
+// the next call; the device's default pool -- which torch and the host
+// application may use -- is never touched.
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pool[64] = {};
+static cudaError_t library_pool(int dev, cudaMemPool_t* out) {
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pool[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    cudaError_t e = cudaMemPoolCreate(&pool, &props);
+    if (e != cudaSuccess) return e;
+    uint64_t keep = ~0ull;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (e != cudaSuccess) {
+      cudaMemPoolDestroy(pool);
+      return e;
+    }
+    g_pool[dev] = pool;
+  }
+  *out = g_pool[dev];
+  return cudaSuccess;
+}
+
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
-  static bool done[64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (dev < 64 && !done[dev]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    (void)cudaGetLastError();
-    done[dev] = true;
-  }
-  return cudaMallocAsync(p, bytes, s);
+  cudaMemPool_t pool;
+  e = library_pool(dev, &pool);
+  if (e != cudaSuccess) return e;
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
 // ------------------------------------------------------------- helpers

@@ -40,24 +40,12 @@ struct LaunchScope {
   int slot;
 };
 
-// ------------------------------------------------------- tile geometry
-// Tile sort (K1): NT threads x VT items; merge passes (K3) use the same tile
-// so every pair boundary (a multiple of 2T) is a tile boundary.
-constexpr int kNT = 256;
-template <class K, bool PAIRS>
-struct Geometry {
-  static constexpr int NT = kNT;
-  static constexpr int VT = sizeof(K) == 4 ? 16 : 16;
-  static constexpr int T = NT * VT;
-};
-
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // The library's own scratch allocations (the calls without a caller
-// workspace): stream-ordered from the current device's default memory pool,
-// whose release threshold is raised once so freed blocks are reused by the
-// next call instead of being unmapped and mapped again (cudaMemPoolTrimTo on
-// that pool hands them back).
+// workspace): stream-ordered from the library's own memory pool for the
+// current device (abi.cu), whose freed blocks are reused by the next call
+// instead of being unmapped and mapped again; the default pool is untouched.
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
 
 size_t dtype_size(msort_dtype d);

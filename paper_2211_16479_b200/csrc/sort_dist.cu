@@ -44,6 +44,9 @@ struct msort_comm_s {
   // the host inside cudaMemcpyAsync, out of reach of the failure detection
   unsigned char* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // small device scratch of the communicator's own collectives (sizes and
+  // agreement flags of the rank-tree gather): 8 * (2 * world + 64) bytes
+  uint64_t* dscratch = nullptr;
 };
 
 namespace msort {
@@ -60,6 +63,24 @@ static msort_status nccl_fail(ncclResult_t r, const char* what) {
     ncclResult_t _r = (expr);                                 \
     if (_r != ncclSuccess) return ::msort::nccl_fail(_r, #expr); \
   } while (0)
+
+// ncclGroupStart/End bracket that is closed on every path: an early error
+// return between the two must not leave this thread's NCCL group open.
+struct NcclGroup {
+  bool open = false;
+  ncclResult_t start() {
+    ncclResult_t r = ncclGroupStart();
+    open = r == ncclSuccess;
+    return r;
+  }
+  ncclResult_t end() {
+    open = false;
+    return ncclGroupEnd();
+  }
+  ~NcclGroup() {
+    if (open) ncclGroupEnd();
+  }
+};
 
 // Host wait for the distributed call's stream with failure detection
 // (SURVEY.md §5): instead of blocking in cudaStreamSynchronize -- which never
@@ -307,24 +328,31 @@ struct NcclColl {
     const size_t wk = dtype_size(kd);
     RankIO& r0 = io[0];
     auto sp = [&](int r, int j) { return S[(size_t)r * p + j]; };
-    int64_t roff = 0;
     LaunchScope ls(KC_EXCHANGE, s);
-    MSORT_NCCL_TRY(ncclGroupStart());
-    for (int j = 0; j < p; ++j) {
-      // receive run j
-      int64_t rc = sp(me + 1, j) - sp(me, j);
-      int64_t sc = sp(j + 1, me) - sp(j, me);  // what I send to rank j
-      if (j == me) {
-        if (rc > 0) {
-          MSORT_CUDA_TRY(cudaMemcpyAsync((char*)r0.ws.rk + roff * wk,
-                                         (char*)r0.keys + sp(me, me) * wk, rc * wk,
+    // the self segment: a local device copy, enqueued outside the NCCL group
+    {
+      int64_t roff = 0;
+      for (int j = 0; j < me; ++j) roff += sp(me + 1, j) - sp(me, j);
+      const int64_t rc = sp(me + 1, me) - sp(me, me);
+      if (rc > 0) {
+        MSORT_CUDA_TRY(cudaMemcpyAsync((char*)r0.ws.rk + roff * wk,
+                                       (char*)r0.keys + sp(me, me) * wk, rc * wk,
+                                       cudaMemcpyDeviceToDevice, s));
+        if (vd != MSORT_NONE)
+          MSORT_CUDA_TRY(cudaMemcpyAsync((char*)r0.ws.rv + roff * 4,
+                                         (char*)r0.vals + sp(me, me) * 4, rc * 4,
                                          cudaMemcpyDeviceToDevice, s));
-          if (vd != MSORT_NONE)
-            MSORT_CUDA_TRY(cudaMemcpyAsync((char*)r0.ws.rv + roff * 4,
-                                           (char*)r0.vals + sp(me, me) * 4, rc * 4,
-                                           cudaMemcpyDeviceToDevice, s));
-        }
-      } else {
+      }
+    }
+    // every other segment: one grouped send/recv per peer; zero-length
+    // segments are skipped on both sides (both hold the same split matrix)
+    int64_t roff = 0;
+    NcclGroup grp;
+    MSORT_NCCL_TRY(grp.start());
+    for (int j = 0; j < p; ++j) {
+      const int64_t rc = sp(me + 1, j) - sp(me, j);  // run j, received from rank j
+      const int64_t sc = sp(j + 1, me) - sp(j, me);  // what I send to rank j
+      if (j != me) {
         if (sc > 0) {
           MSORT_NCCL_TRY(ncclSend((char*)r0.keys + sp(j, me) * wk, (size_t)sc, nccl_type(kd), j,
                                   c->comm, s));
@@ -342,7 +370,7 @@ struct NcclColl {
       }
       roff += rc;
     }
-    MSORT_NCCL_TRY(ncclGroupEnd());
+    MSORT_NCCL_TRY(grp.end());
     return MSORT_SUCCESS;
   }
   int rank_of(int local) const { return c->rank + local; }
@@ -737,7 +765,8 @@ struct TreeNccl {
     TreeBufs& b = tb[0];
     const size_t wk = dtype_size(kd);
     LaunchScope ls(KC_EXCHANGE, s);
-    MSORT_NCCL_TRY(ncclGroupStart());
+    NcclGroup grp;
+    MSORT_NCCL_TRY(grp.start());
     if (me == child) {
       MSORT_NCCL_TRY(ncclSend(b.ak, (size_t)cnt, nccl_type(kd), parent, c->comm, s));
       if (vd != MSORT_NONE)
@@ -749,10 +778,31 @@ struct TreeNccl {
         MSORT_NCCL_TRY(ncclRecv((char*)b.av + b.cnt * 4, (size_t)cnt, ncclUint32, child, c->comm,
                                 s));
     }
-    MSORT_NCCL_TRY(ncclGroupEnd());
+    MSORT_NCCL_TRY(grp.end());
     return MSORT_SUCCESS;
   }
   int local(int rank) const { return rank == c->rank ? 0 : -1; }
+  // Collective agreement before any point-to-point transfer: every rank
+  // learns whether all ranks are ready (one all-reduce MIN of a flag and a
+  // host wait), so a rank that fails never leaves its peers blocked in a
+  // send or receive that it will not post.
+  msort_status agree(bool ok, const char* what) {
+    uint64_t* d = c->dscratch + 2 * (size_t)c->world;
+    uint64_t* h = reinterpret_cast<uint64_t*>(c->pinned + c->pinned_bytes - 64);
+    h[0] = ok ? 1 : 0;
+    MSORT_CUDA_TRY(cudaMemcpyAsync(d, h, 8, cudaMemcpyHostToDevice, s));
+    {
+      LaunchScope ls(KC_NCCL, s);
+      MSORT_NCCL_TRY(ncclAllReduce(d, d, 1, ncclUint64, ncclMin, c->comm, s));
+    }
+    MSORT_CUDA_TRY(cudaMemcpyAsync(h + 1, d, 8, cudaMemcpyDeviceToHost, s));
+    MSORT_TRY(wait_stream_nccl(c, s, what));
+    if (h[1] == 0 && ok) {
+      set_error(std::string(what) + ": another rank failed");
+      return MSORT_ERROR_OUT_OF_MEMORY;
+    }
+    return MSORT_SUCCESS;
+  }
 };
 struct TreeEmul {
   cudaStream_t s;
@@ -768,6 +818,7 @@ struct TreeEmul {
     return MSORT_SUCCESS;
   }
   int local(int rank) const { return rank; }
+  msort_status agree(bool, const char*) { return MSORT_SUCCESS; }
 };
 
 // ranks: the global ranks this process drives (one for NCCL, all for the
@@ -802,6 +853,8 @@ static msort_status tree_run(Coll& C, const std::vector<int>& ranks,
       for (void* q : *a) cudaFreeAsync(q, s);
     }
   } freer{&allocs, s};
+  std::vector<void*> sws(ranks.size(), nullptr);
+  bool ok = true;
   for (size_t l = 0; l < ranks.size(); ++l) {
     const int r = ranks[l];
     const size_t cap = (size_t)sub[r];
@@ -809,14 +862,22 @@ static msort_status tree_run(Coll& C, const std::vector<int>& ranks,
     b.ak = alloc(cap * wk), b.bk = alloc(cap * wk);
     b.av = pairs ? alloc(cap * 4) : nullptr, b.bv = pairs ? alloc(cap * 4) : nullptr;
     b.part = alloc(4096);
-    void* sws = alloc(single_ws_bytes((size_t)nall[r], kd, vd));
-    if (!b.ak || !b.bk || (pairs && (!b.av || !b.bv)) || !b.part || !sws) {
-      set_error("tree sort: out of device memory");
-      return MSORT_ERROR_OUT_OF_MEMORY;
-    }
+    sws[l] = alloc(single_ws_bytes((size_t)nall[r], kd, vd));
+    ok = ok && b.ak && b.bk && (!pairs || (b.av && b.bv)) && b.part && sws[l];
+  }
+  // every rank agrees before the first transfer (a rank that could not
+  // allocate must not leave the others waiting in a send / receive)
+  MSORT_TRY(C.agree(ok, "tree sort: buffers"));
+  if (!ok) {
+    set_error("tree sort: out of device memory");
+    return MSORT_ERROR_OUT_OF_MEMORY;
+  }
+  for (size_t l = 0; l < ranks.size(); ++l) {
+    const int r = ranks[l];
+    TreeBufs& b = tb[l];
     // D1: the local sort (the paper's subsort), into [own | ...]
     MSORT_TRY(sort_single_dispatch(in_k[l], pairs ? in_v[l] : nullptr, b.ak, b.av,
-                                   (size_t)nall[r], kd, vd, sws,
+                                   (size_t)nall[r], kd, vd, sws[l],
                                    single_ws_bytes((size_t)nall[r], kd, vd), s));
     b.cnt = nall[r];
   }
@@ -862,30 +923,28 @@ msort_status tree_nccl(const void* in_keys, const void* in_vals, size_t n, msort
     return MSORT_ERROR_NCCL;
   }
   const int p = comm->world;
-  // every rank's size (one allgather, one host sync)
-  uint64_t* d = nullptr;
-  MSORT_CUDA_TRY(scratch_alloc((void**)&d, 8 * (size_t)(p + 1), s));
-  std::vector<uint64_t> hn((size_t)p);
-  memcpy(comm->pinned, &n, 8);  // page-locked: no blocking copies (failure detection)
-  cudaError_t e = cudaMemcpyAsync(d + p, comm->pinned, 8, cudaMemcpyHostToDevice, s);
-  ncclResult_t nr = e == cudaSuccess ? ncclAllGather(d + p, d, 1, ncclUint64, comm->comm, s)
-                                     : ncclSuccess;
-  if (e == cudaSuccess && nr == ncclSuccess)
-    e = cudaMemcpyAsync(comm->pinned + 64, d, 8 * (size_t)p, cudaMemcpyDeviceToHost, s);
-  if (nr != ncclSuccess || e != cudaSuccess) {
-    cudaFreeAsync(d, s);
-    if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather (tree sizes)");
-    return cuda_fail(e, "tree sizes");
+  // every rank's (size, root capacity): one all-gather, one host sync; the
+  // capacity check is then the same decision on every rank
+  uint64_t* d = comm->dscratch;  // [p x (n, cap)] gathered, [2] sent
+  uint64_t* h = reinterpret_cast<uint64_t*>(comm->pinned);
+  h[0] = (uint64_t)n;
+  h[1] = comm->rank == 0 ? (uint64_t)root_cap : 0;
+  cudaError_t e = cudaMemcpyAsync(d + 2 * p, h, 16, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "tree sizes");
+  {
+    LaunchScope ls(KC_NCCL, s);
+    MSORT_NCCL_TRY(ncclAllGather(d + 2 * p, d, 2, ncclUint64, comm->comm, s));
   }
+  MSORT_CUDA_TRY(cudaMemcpyAsync(comm->pinned + 64, d, 16 * (size_t)p, cudaMemcpyDeviceToHost, s));
   MSORT_TRY(wait_stream_nccl(comm, s, "tree sizes"));
-  memcpy(hn.data(), comm->pinned + 64, 8 * (size_t)p);
-  cudaFreeAsync(d, s);
-  std::vector<int64_t> nall(hn.begin(), hn.end());
+  const uint64_t* g = reinterpret_cast<const uint64_t*>(comm->pinned + 64);
+  std::vector<int64_t> nall((size_t)p);
   int64_t total = 0;
-  for (int64_t v : nall) total += v;
+  for (int r = 0; r < p; ++r) nall[r] = (int64_t)g[2 * r], total += nall[r];
+  const uint64_t cap0 = g[1];
   if (total_out) *total_out = total;
-  if (comm->rank == 0 && (size_t)total > root_cap) {
-    set_error("tree sort: root output holds " + std::to_string(root_cap) + " elements, need " +
+  if ((uint64_t)total > cap0) {  // decided identically on every rank
+    set_error("tree sort: root output holds " + std::to_string(cap0) + " elements, need " +
               std::to_string(total));
     return MSORT_ERROR_INVALID_VALUE;
   }
@@ -923,18 +982,35 @@ msort_status comm_unique_id(void* out) {
   return MSORT_SUCCESS;
 }
 
+// The communicator's page-locked staging and small device scratch.
+static msort_status comm_buffers(msort_comm_s* cs) {
+  const size_t w = (size_t)cs->world;
+  cs->pinned_bytes = std::max<size_t>({8 * (w + 1) * w, kIpcBytes * w, 16 * w + 64}) + 4096;
+  if (cudaMallocHost(reinterpret_cast<void**>(&cs->pinned), cs->pinned_bytes) != cudaSuccess) {
+    cs->pinned = nullptr;
+    set_error("cudaMallocHost (communicator staging)");
+    return MSORT_ERROR_OUT_OF_MEMORY;
+  }
+  if (cudaMalloc(reinterpret_cast<void**>(&cs->dscratch), 8 * (2 * w + 64)) != cudaSuccess) {
+    cudaFreeHost(cs->pinned);
+    cs->pinned = nullptr, cs->dscratch = nullptr;
+    set_error("cudaMalloc (communicator scratch)");
+    return MSORT_ERROR_OUT_OF_MEMORY;
+  }
+  return MSORT_SUCCESS;
+}
+
 msort_status comm_init(const void* idp, int rank, int world, msort_comm_s** out) {
   ncclUniqueId id;
   memcpy(&id, idp, sizeof(id));
   ncclComm_t c;
   MSORT_NCCL_TRY(ncclCommInitRank(&c, world, id, rank));
   auto* cs = new msort_comm_s{c, rank, world, {}};
-  cs->pinned_bytes = std::max<size_t>(8 * (size_t)(world + 1) * world, kIpcBytes * world) + 4096;
-  if (cudaMallocHost(reinterpret_cast<void**>(&cs->pinned), cs->pinned_bytes) != cudaSuccess) {
+  msort_status st = comm_buffers(cs);
+  if (st != MSORT_SUCCESS) {
     ncclCommDestroy(c);
     delete cs;
-    set_error("cudaMallocHost (communicator staging)");
-    return MSORT_ERROR_OUT_OF_MEMORY;
+    return st;
   }
   *out = cs;
   return MSORT_SUCCESS;
@@ -949,11 +1025,10 @@ msort_status comm_wrap(void* nccl_comm, msort_comm_s** out) {
   MSORT_NCCL_TRY(ncclCommCount(c, &world));
   auto* cs = new msort_comm_s{c, rank, world, {}};
   cs->owned = false;
-  cs->pinned_bytes = std::max<size_t>(8 * (size_t)(world + 1) * world, kIpcBytes * world) + 4096;
-  if (cudaMallocHost(reinterpret_cast<void**>(&cs->pinned), cs->pinned_bytes) != cudaSuccess) {
+  msort_status st = comm_buffers(cs);
+  if (st != MSORT_SUCCESS) {
     delete cs;
-    set_error("cudaMallocHost (communicator staging)");
-    return MSORT_ERROR_OUT_OF_MEMORY;
+    return st;
   }
   *out = cs;
   return MSORT_SUCCESS;
@@ -964,6 +1039,7 @@ msort_status comm_destroy(msort_comm_s* c) {
   for (auto& kv : c->ipc_open) cudaIpcCloseMemHandle(kv.second);
   ncclResult_t r = (c->aborted || !c->owned) ? ncclSuccess : ncclCommDestroy(c->comm);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->dscratch) cudaFree(c->dscratch);
   delete c;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
   return MSORT_SUCCESS;

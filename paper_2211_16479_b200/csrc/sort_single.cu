@@ -17,15 +17,15 @@
 //
 // "P:n" = /root/reference/PAPER.md line n.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "k3_merge.cuh"
-#include "k3q_merge.cuh"
-#include "k3x_merge.cuh"
 #include "msort_device.cuh"
 #include "networks.cuh"
 #include "msort_internal.h"
@@ -371,16 +371,6 @@ __global__ void __launch_bounds__(NT)
 // ----------------------------------------------------------------- K3
 // k3_merge.cuh: the persistent merge pass with fused co-rank search (K2).
 
-#ifdef MSORT_K3X_TRACE
-extern "C" int msort_debug_k3x_trace(unsigned long long* host, int n, int reset) {
-  int r = (int)cudaMemcpyFromSymbol(host, g_k3x_trace, sizeof(unsigned long long) * n);
-  if (reset) {
-    static unsigned long long z[1024 * 8];
-    cudaMemcpyToSymbol(g_k3x_trace, z, sizeof(z));
-  }
-  return r;
-}
-#endif
 #ifdef MSORT_K3_TRACE
 extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, g_k3_trace, sizeof(unsigned long long) * n);
@@ -405,83 +395,120 @@ extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
 #define MSORT_K3_CHDIV 2  // full chunks per CTA per level below which chunks shrink
 #endif
 #ifndef MSORT_QUAD
-#define MSORT_QUAD 0  // keys only: 1 = two merge levels per HBM pass (k3q_merge.cuh), see DESIGN.md
+#define MSORT_QUAD 0  // keys only, 4-byte keys: 5 = two merge levels per HBM pass (K6)
 #endif
-#ifndef MSORT_QUAD_SEG
-#define MSORT_QUAD_SEG 65536  // target keys per 4-way segment
-#endif
-#ifndef MSORT_X_NC
-#define MSORT_X_NC 384  // K3X mergers (super-tile capacity NC x 17)
-#endif
-#ifndef MSORT_X_S
-#define MSORT_X_S 2  // K3X stages
-#endif
-#ifndef MSORT_QUAD_NT
-#define MSORT_QUAD_NT 128
-#endif
-#ifndef MSORT_QUAD_VT
-#define MSORT_QUAD_VT 15  // odd: conflict-free blocked stores
-#endif
-
-// 4-way pass mode: 0 off, 1 auto (while every CTA gets >= 2 segments),
-// 2 always (tests); env MSORT_QUAD overrides the default, msort_debug_set_quad
-// overrides both.
-static int g_quad_mode = -1;
+// Merge-level grouping for keys-only sorts: 0 = every level in the fused
+// 2-way dataflow (default), 5 = K6 4-way passes (opt-in experiment).  The
+// environment variable MSORT_QUAD sets it once; msort_debug_set_quad (tests)
+// overrides it.  Atomic: concurrent sorts read a consistent value.
+static std::atomic<int> g_quad_mode{-1};
 static int quad_mode() {
-  if (g_quad_mode < 0) {
+  int m = g_quad_mode.load(std::memory_order_relaxed);
+  if (m < 0) {
     const char* e = getenv("MSORT_QUAD");
-    g_quad_mode = e ? atoi(e) : MSORT_QUAD;
+    int v = e ? atoi(e) : MSORT_QUAD;
+    if (v != 5) v = 0;
+    g_quad_mode.compare_exchange_strong(m, v);
+    m = g_quad_mode.load(std::memory_order_relaxed);
   }
-  return g_quad_mode;
+  return m;
 }
 
 // Scheduler state in the workspace: 64 chunk counters (one per launch of a
 // sort) then the per-level, per-pair completion counters of the fused merge.
 constexpr int kMaxLaunches = 64;
 
-// Page-locked staging buffer for host tables uploaded by a call (segment
-// descriptors).  staging_acquire waits until the previous upload from it has
-// completed (an event recorded by staging_release), growing it if needed;
-// the mutex is held from acquire to release.
+// Page-locked staging buffers for host tables uploaded by a call (segment
+// descriptors): a small ring per device, each buffer with its own event.  A
+// call takes a buffer whose previous upload has completed (growing it if
+// needed), so it only waits when every buffer of its device is still in
+// flight; the lease records the buffer's event on the caller's stream.
+struct StageBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ev = nullptr;
+  bool held = false;
+};
+constexpr int kStageRing = 4;
 static std::mutex g_stage_mu;
-static void* g_stage = nullptr;
-static size_t g_stage_cap = 0;
-static cudaEvent_t g_stage_ev = nullptr;
-static msort_status staging_acquire(size_t bytes, void** out) {
-  g_stage_mu.lock();
-  if (g_stage_ev) {
-    cudaError_t e = cudaEventSynchronize(g_stage_ev);
-    if (e != cudaSuccess) {
-      g_stage_mu.unlock();
-      return cuda_fail(e, "staging event");
-    }
-  } else {
-    cudaError_t e = cudaEventCreateWithFlags(&g_stage_ev, cudaEventDisableTiming);
-    if (e != cudaSuccess) {
-      g_stage_mu.unlock();
-      return cuda_fail(e, "cudaEventCreate");
+static StageBuf g_stage[64][kStageRing];
+
+struct StageLease {
+  int dev = -1, slot = -1;
+  void* ptr = nullptr;
+  ~StageLease() {  // an early return before release(): nothing was enqueued
+    if (slot >= 0) {
+      std::lock_guard<std::mutex> lk(g_stage_mu);
+      g_stage[dev][slot].held = false;
     }
   }
-  if (bytes > g_stage_cap) {
-    if (g_stage) cudaFreeHost(g_stage);
-    g_stage = nullptr;
-    g_stage_cap = 0;
-    const size_t cap = std::max<size_t>(bytes + bytes / 2, 1 << 16);
-    cudaError_t e = cudaHostAlloc(&g_stage, cap, cudaHostAllocDefault);
-    if (e != cudaSuccess) {
-      g_stage_mu.unlock();
-      return cuda_fail(e, "cudaHostAlloc (staging)");
+  msort_status release(cudaStream_t s) {
+    cudaError_t e;
+    {
+      std::lock_guard<std::mutex> lk(g_stage_mu);
+      e = cudaEventRecord(g_stage[dev][slot].ev, s);
+      g_stage[dev][slot].held = false;
     }
-    g_stage_cap = cap;
+    slot = -1;
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord (staging)");
+    return MSORT_SUCCESS;
   }
-  *out = g_stage;
-  return MSORT_SUCCESS;
-}
-static msort_status staging_release(cudaStream_t s) {
-  cudaError_t e = cudaEventRecord(g_stage_ev, s);
-  g_stage_mu.unlock();
-  if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord (staging)");
-  return MSORT_SUCCESS;
+};
+
+static msort_status staging_acquire(size_t bytes, StageLease& L) {
+  int dev = 0;
+  MSORT_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= 64) {
+    set_error("device index >= 64");
+    return MSORT_ERROR_NOT_SUPPORTED;
+  }
+  for (int attempt = 0;; ++attempt) {
+    int pick = -1;
+    {
+      std::lock_guard<std::mutex> lk(g_stage_mu);
+      // a free buffer whose last upload is complete (or never used)
+      for (int i = 0; i < kStageRing && pick < 0; ++i) {
+        StageBuf& b = g_stage[dev][i];
+        if (b.held) continue;
+        if (!b.ev) {
+          cudaError_t e = cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming);
+          if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate (staging)");
+          pick = i;
+        } else if (cudaEventQuery(b.ev) == cudaSuccess) {
+          pick = i;
+        }
+      }
+      (void)cudaGetLastError();  // cudaErrorNotReady from the queries
+      if (pick < 0 && attempt > 0) {
+        for (int i = 0; i < kStageRing && pick < 0; ++i)
+          if (!g_stage[dev][i].held) pick = i;  // waited for below
+      }
+      if (pick >= 0) {
+        StageBuf& b = g_stage[dev][pick];
+        b.held = true;
+        L.dev = dev, L.slot = pick;
+      }
+    }
+    if (pick < 0) {
+      if (attempt > 1000000) {
+        set_error("staging: every buffer held");
+        return MSORT_ERROR_NOT_SUPPORTED;
+      }
+      std::this_thread::yield();
+      continue;
+    }
+    StageBuf& b = g_stage[dev][pick];
+    MSORT_CUDA_TRY(cudaEventSynchronize(b.ev));  // immediate unless every buffer was busy
+    if (bytes > b.cap) {
+      if (b.p) cudaFreeHost(b.p);
+      b.p = nullptr, b.cap = 0;
+      const size_t cap = std::max<size_t>(bytes + bytes / 2, 1 << 16);
+      MSORT_CUDA_TRY(cudaHostAlloc(&b.p, cap, cudaHostAllocDefault));
+      b.cap = cap;
+    }
+    L.ptr = b.p;
+    return MSORT_SUCCESS;
+  }
 }
 
 template <class K, bool PAIRS>
@@ -527,22 +554,6 @@ struct Kernels {
   using Explicit = SinglePass<K, ExplicitPairs>;
   using Peer = SinglePass<K, PeerPairs>;
 
-  // 4-way pass (keys only)
-  static constexpr int NTQ = MSORT_QUAD_NT, VTQ = MSORT_QUAD_VT;
-  using LQ = QuadLayout<K, NTQ, VTQ>;
-  static int& gridq(int dev) {
-    static int g[64] = {};
-    return g[dev & 63];
-  }
-
-  // K3X (quad mode 4): two levels per pass, boundaries found just in time
-  static constexpr int NCX = MSORT_X_NC, SX = MSORT_X_S;
-  using LX = K3XLayout<K, NCX, 17, SX>;
-  static int& gridx(int dev) {
-    static int g[64] = {};
-    return g[dev & 63];
-  }
-
   // K6 (4-byte keys only, quad mode 5): 128 threads x 68 keys, tiles of
   // <= XS keys of X plus <= YS keys of Y (XS + YS = Tm = 126 x 68)
   static constexpr int kK6NT2 = MSORT_K6_NT2, kK6VT = 68;
@@ -573,27 +584,22 @@ struct Kernels {
     return (int)std::max<int64_t>(1, std::min<int64_t>(kChunk, per));
   }
 
-  // Segments of the 4-way pass over runs of L: groups of 4L, S_full segments
-  // per full group (S_last for the last), nseg in all.
-  static void quad_geometry(int64_t n, int64_t L, int64_t& ng, int& sf, int& sl, int64_t& nseg) {
-    ng = (n + 4 * L - 1) / (4 * L);
-    auto segs = [](int64_t len) {
-      int64_t k = (len + MSORT_QUAD_SEG - 1) / MSORT_QUAD_SEG;
-      return (int)std::max<int64_t>(1, std::min<int64_t>(k, kQuadMaxSeg));
-    };
-    sf = segs(4 * L);
-    sl = segs(n - (ng - 1) * 4 * L);
-    nseg = (ng - 1) * sf + sl;
-  }
-
+  // Kernel attributes are set lazily, per kernel instance and device, the
+  // first time a call needs that kernel (a first call only pays for what it
+  // launches).
   template <class Src>
-  static msort_status set_smem() {
+  static msort_status k3_ready(int dev) {
+    static std::atomic<bool> done[64];
+    if (done[dev & 63].load(std::memory_order_acquire)) return MSORT_SUCCESS;
     auto k = k3_merge_pass<K, PAIRS, NC, VT3, S, MINB, Src>;
     MSORT_CUDA_TRY(
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3_smem));
+    done[dev & 63].store(true, std::memory_order_release);
     return MSORT_SUCCESS;
   }
 
+  // K1 and the persistent merge kernel's grid (every CTA of the fused
+  // levels must be resident: grid = SMs x occupancy).
   static msort_status init() {
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
@@ -606,13 +612,7 @@ struct Kernels {
       MSORT_CUDA_TRY(cudaFuncSetAttribute(k1_tile_sort_keys<K, NT1, VT>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)k1_smem));
-    MSORT_TRY(set_smem<Fused>());
-    MSORT_TRY(set_smem<Explicit>());
-    MSORT_TRY(set_smem<Peer>());
-    MSORT_TRY(set_smem<SegF>());
-#ifdef MSORT_K3_PERPASS
-    MSORT_TRY((set_smem<SinglePass<K, UniformPairs>>()));
-#endif
+    MSORT_TRY(k3_ready<Fused>(dev));
     int sms = 0, occ = 0;
     MSORT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     MSORT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -621,32 +621,22 @@ struct Kernels {
       set_error("merge pass kernel does not fit on an SM");
       return MSORT_ERROR_NOT_SUPPORTED;
     }
-    // every CTA of the persistent merge kernel must be resident (the fused
-    // levels wait on each other's progress): grid = SMs x occupancy
     grid3(dev) = sms * occ;
+    return MSORT_SUCCESS;
+  }
+
+  // K6 (opt-in): its attribute and grid, on first use
+  static msort_status k6_init(int dev) {
     if constexpr (!PAIRS && sizeof(K) == 4) {
+      if (k6_grid(dev)) return MSORT_SUCCESS;
       auto k6 = k6_quad_pass<K, kK6NT2, kK6VT>;
       MSORT_CUDA_TRY(cudaFuncSetAttribute(k6, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)(K6S::KEYS * sizeof(K))));
-      int o6 = 0;
+      int o6 = 0, sms = 0;
+      MSORT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       MSORT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o6, k6, K6S::NT1,
                                                                    K6S::KEYS * sizeof(K)));
       k6_grid(dev) = sms * std::max(o6, 1);
-    }
-    if constexpr (!PAIRS) {
-      auto kq = k3q_pass<K, NTQ, VTQ>;
-      MSORT_CUDA_TRY(
-          cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LQ::bytes));
-      int oq = 0;
-      MSORT_CUDA_TRY(
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oq, kq, NTQ + 64, LQ::bytes));
-      gridq(dev) = sms * std::max(oq, 1);
-      auto kx = k3x_pass<K, NCX, 17, SX>;
-      MSORT_CUDA_TRY(
-          cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LX::bytes));
-      int ox = 0;
-      MSORT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, kx, NCX + 96, LX::bytes));
-      gridx(dev) = sms * std::max(ox, 1);
     }
     return MSORT_SUCCESS;
   }
@@ -656,6 +646,7 @@ struct Kernels {
                                 cudaStream_t s, KernelClass kc) {
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
+    MSORT_TRY(k3_ready<Src>(dev));
     const int64_t grid = std::min<int64_t>(grid3(dev), (nchunks + src.grab - 1) / src.grab);
     {
       LaunchScope ls(kc, s);
@@ -692,21 +683,14 @@ struct Kernels {
     while ((int64_t(1) << passes) < ntiles) ++passes;
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
-    // 4-way passes (two levels each) while there are enough segments to keep
-    // every CTA busy; the remaining levels run as the fused 2-way dataflow.
+    // K6 (opt-in, 4-byte keys only): every pair of levels as one 4-way pass;
+    // otherwise (the default) every level runs in the fused 2-way dataflow.
     int nq = 0;
     int64_t Lq = T;
     if constexpr (!PAIRS) {
-      const int mode = k6_mode() ? 5 : quad_mode();
-      if (mode == 4 || mode == 5)
-        nq = passes / 2, Lq = (int64_t)T << (2 * nq);  // K3X / K6: every pair of levels
-      while (mode && mode < 4 && passes - 2 * nq >= 2) {
-        int64_t ng, nseg;
-        int sf, sl;
-        quad_geometry((int64_t)n, Lq, ng, sf, sl, nseg);
-        if (mode == 1 && nseg < 2 * (int64_t)gridq(dev)) break;
-        ++nq;
-        Lq *= 4;
+      if (k6_mode()) {
+        MSORT_TRY(k6_init(dev));
+        nq = passes / 2, Lq = (int64_t)T << (2 * nq);
       }
     }
     const int left = passes - 2 * nq;  // 2-way levels
@@ -724,8 +708,7 @@ struct Kernels {
     }
     auto* ctr = reinterpret_cast<unsigned long long*>(w);
     auto* done = reinterpret_cast<unsigned*>(ctr + kMaxLaunches);
-    auto* qstates = reinterpret_cast<QuadState*>(
-        w + align_up(((size_t)n / T + 2 + 2 * 64) * sizeof(int64_t), 256));
+    char* const k6ws = w + align_up(((size_t)n / T + 2 + 2 * 64) * sizeof(int64_t), 256);
     (void)ws_bytes;
 
     K* bk[2] = {keys, wk};
@@ -759,7 +742,7 @@ struct Kernels {
       if (k6_mode() && nq > 0) {
         // K6 (k6_quad.cuh): partition (unit states, tiles, cut pieces), then
         // the 4-way pass over the unit tiles and over the pieces
-        char* kw = reinterpret_cast<char*>(qstates);
+        char* kw = k6ws;
         int64_t* states = reinterpret_cast<int64_t*>(kw);
         const int64_t NUmax = k6_units_max((int64_t)n);
         K6Tile* tiles = reinterpret_cast<K6Tile*>(kw + align_up(32 * NUmax, 256));
@@ -810,53 +793,6 @@ struct Kernels {
         if (left == 0) return MSORT_SUCCESS;
       }
       }
-      if (quad_mode() == 4 && !k6_mode()) {
-        for (int q = 0; q < nq; ++q, L *= 4) {
-          const int64_t ng = ((int64_t)n + 4 * L - 1) / (4 * L);
-          const int64_t upg = (2 * L + LX::XS - 1) / LX::XS + 1;
-          {
-            LaunchScope ls(KC_MERGE, s);
-            k3x_pass<K, NCX, 17, SX>
-                <<<(unsigned)std::min<int64_t>(gridx(dev), (ng * upg + 3) / 4), NCX + 96, LX::bytes,
-                   s>>>(bk[cur], bk[cur ^ 1], (int64_t)n, L, ng, upg, ctr + 32 + q);
-          }
-          MSORT_CUDA_TRY(cudaGetLastError());
-#ifdef MSORT_K3_CHECK
-          {
-            cudaError_t e = cudaStreamSynchronize(s);
-            if (e != cudaSuccess) return cuda_fail(e, "k3x (debug sync)");
-          }
-#endif
-          cur ^= 1;
-        }
-        if (left == 0) return MSORT_SUCCESS;
-      }
-      for (int q = 0; q < nq && quad_mode() != 4 && !k6_mode(); ++q, L *= 4) {
-        int64_t ng, nseg;
-        int sf, sl;
-        quad_geometry((int64_t)n, L, ng, sf, sl, nseg);
-        {
-          LaunchScope ls(KC_PARTITION, s);
-          k2q_partition<K><<<(unsigned)ng, 256, 0, s>>>(bk[cur], (int64_t)n, L, sf, sl, ng,
-                                                         qstates);
-        }
-        MSORT_CUDA_TRY(cudaGetLastError());
-        {
-          LaunchScope ls(KC_MERGE, s);
-          k3q_pass<K, NTQ, VTQ><<<(unsigned)std::min<int64_t>(gridq(dev), nseg), NTQ + 64,
-                                   LQ::bytes, s>>>(bk[cur], bk[cur ^ 1], (int64_t)n, L, sf, nseg,
-                                                   qstates, ctr + 32 + q);
-        }
-        MSORT_CUDA_TRY(cudaGetLastError());
-#ifdef MSORT_K3_CHECK
-        {
-          cudaError_t e = cudaStreamSynchronize(s);
-          if (e != cudaSuccess) return cuda_fail(e, "k3q (debug sync)");
-        }
-#endif
-        cur ^= 1;
-      }
-      if (left == 0) return MSORT_SUCCESS;
     }
 #ifdef MSORT_K3_PERPASS
     // tuning variant: one launch per merge level
@@ -926,12 +862,13 @@ struct Kernels {
     if (!dev_off && (int64_t)nseg >= kSegUploadMin) {
       int64_t* doff = reinterpret_cast<int64_t*>(w);
       w += align_up(8 * (nseg + 1), 256);
-      int64_t* h = nullptr;
-      MSORT_TRY(staging_acquire(8 * (nseg + 1), reinterpret_cast<void**>(&h)));
+      StageLease lease;
+      MSORT_TRY(staging_acquire(8 * (nseg + 1), lease));
+      int64_t* h = static_cast<int64_t*>(lease.ptr);
       std::memcpy(h, off, 8 * (nseg + 1));
       const cudaError_t e =
           cudaMemcpyAsync(doff, h, 8 * (nseg + 1), cudaMemcpyHostToDevice, s);
-      MSORT_TRY(staging_release(s));
+      MSORT_TRY(lease.release(s));
       if (e != cudaSuccess) return cuda_fail(e, "segment table upload");
       off = doff;
       dev_off = true;
@@ -1032,14 +969,9 @@ struct Kernels {
     const int64_t words = w_desc + w_k1 + w_tab;
     int64_t* dstage = reinterpret_cast<int64_t*>(w);
     w += align_up((size_t)words * 8, 256);
-    int64_t* h = nullptr;
-    MSORT_TRY(staging_acquire((size_t)words * 8, reinterpret_cast<void**>(&h)));
-    struct Unlock {  // early returns before staging_release
-      bool held = true;
-      ~Unlock() {
-        if (held) g_stage_mu.unlock();
-      }
-    } unlock;
+    StageLease lease;  // early returns before release() hand it back unused
+    MSORT_TRY(staging_acquire((size_t)words * 8, lease));
+    int64_t* h = static_cast<int64_t*>(lease.ptr);
     if (w_off) std::memcpy(h, off, (size_t)w_off * 8);
     if (!dev_off) {
       int64_t at = w_off;
@@ -1079,8 +1011,7 @@ struct Kernels {
     }
     if (words)
       MSORT_CUDA_TRY(cudaMemcpyAsync(dstage, h, (size_t)words * 8, cudaMemcpyHostToDevice, s));
-    unlock.held = false;
-    MSORT_TRY(staging_release(s));
+    MSORT_TRY(lease.release(s));
     // ---- launches
     if (ntiny) {
       LaunchScope ls(KC_TILE_SORT, s);
@@ -1354,26 +1285,7 @@ int tile_size_for(msort_dtype kd, msort_dtype vd) {
 
 }  // namespace msort
 
-// Experiment (K6, k6_quad.cuh): one 4-way pass over int32 keys with
-// caller-computed tiles (K6Tile[ntiles], device memory).  Not declared in
-// include/msort.h: a tuning entry point for scripts/k6_experiment.py.
-extern "C" int msort_debug_k6_pass(const void* src, void* dst, const void* tiles, int64_t ntiles,
-                                   void* stream) {
-  using namespace msort;
-  constexpr int NT2 = 126, VT = 68;
-  using SH = K6Shape<NT2, VT>;
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(k6_quad_pass<int32_t, NT2, VT>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SH::KEYS * 4));
-    init = true;
-  }
-  k6_quad_pass<int32_t, NT2, VT><<<(unsigned)ntiles, SH::NT1, SH::KEYS * 4, (cudaStream_t)stream>>>(
-      (const int32_t*)src, (int32_t*)dst, (const K6Tile*)tiles, nullptr);
-  return (int)cudaGetLastError();
-}
-
 extern "C" int msort_debug_set_quad(int mode) {
-  msort::g_quad_mode = mode;
+  msort::g_quad_mode.store(mode == 5 ? 5 : 0);
   return 0;
 }

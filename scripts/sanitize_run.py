@@ -29,7 +29,7 @@ k = mi.keys_torch(250007, 4, "u31", device="cuda")
 v = torch.arange(k.numel(), dtype=torch.int32, device="cuda")
 ms.msort_sort_pairs(k, v)
 check_sorted(k)
-ms.set_quad_mode(2)
+ms.set_quad_mode(5)
 k = mi.keys_torch(300001, 5, "u31", device="cuda")
 ms.msort_sort(k)
 check_sorted(k)

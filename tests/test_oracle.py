@@ -272,6 +272,58 @@ def test_golden_file_matches_survey():
             assert got["check"] == 0
 
 
+# SURVEY.md §8(c) addendum (independent numpy computation: np.sort per shard,
+# value bisection, cross-checked by np.partition on the concatenation): the
+# key at global position K_r = r * 2^28 of the C5 concatenation at p ranks,
+# and every shard's min / max.
+SURVEY_C5_VSTAR = {2: [1073704941], 4: [536879718, 1073750287, 1610621812],
+                   8: [268433051, 536898611, 805317802, 1073767078, 1342188887, 1610616419,
+                       1879055353]}
+SURVEY_C5_MINMAX = [(14, 2147483646), (4, 2147483647), (18, 2147483633), (0, 2147483629),
+                    (23, 2147483647), (1, 2147483635), (8, 2147483632), (5, 2147483640)]
+
+
+def test_c5_digests_match_survey():
+    """tests/golden/c5_digests.json (make_c5_digests.py: oracle only) against
+    the survey's independent numbers: rank r's slice at p ranks starts with
+    v*_r (its first key IS the key at K_r), the p = 1 slice spans shard 0's
+    min..max, the p-rank slices span the min..max of the first p shards, and
+    consecutive slices are ordered.  The slices' sums add up to the shards'
+    sums (the generator, independent of the oracle)."""
+    with open(os.path.join(GOLDEN, "c5_digests.json")) as f:
+        g = json.load(f)
+    assert g["n_per_rank"] == 1 << 28
+    d = g["digests"]
+    assert d["1"][0]["first"] == SURVEY_C5_MINMAX[0][0]
+    assert d["1"][0]["last"] == SURVEY_C5_MINMAX[0][1]
+    for p, vstar in SURVEY_C5_VSTAR.items():
+        rows = d[str(p)]
+        assert len(rows) == p
+        assert [r["first"] for r in rows[1:]] == vstar, p
+        assert rows[0]["first"] == min(m for m, _ in SURVEY_C5_MINMAX[:p])
+        assert rows[-1]["last"] == max(m for _, m in SURVEY_C5_MINMAX[:p])
+        assert all(rows[r]["last"] <= rows[r + 1]["first"] for r in range(p - 1))
+        assert all(len(r["sha256"]) == 64 for r in rows)
+
+
+def test_c5_digest_sums_match_generator():
+    """The p = 1 and p = 2 digest rows sum to the generated shards' sums (the
+    seeded generator alone, no sort): the slices are a permutation's worth of
+    keys.  (p = 4, 8 would take a minute of numpy; their first keys are pinned
+    above.)"""
+    with open(os.path.join(GOLDEN, "c5_digests.json")) as f:
+        d = json.load(f)["digests"]
+    n = 1 << 28
+    sums = []
+    for r in range(2):
+        t = 0
+        for s in range(0, n, 1 << 24):
+            t += int((mi.splitmix64(1 << 24, 4 + r, s) >> np.uint64(33)).sum())
+        sums.append(t)
+    for p in (1, 2):
+        assert sum(x["sum"] for x in d[str(p)]) == sum(sums[:p]), p
+
+
 def test_oracle_live_c1_matches_survey(orc):
     k, _ = mi.config_input("C1")
     s = orc.sort(k)
