@@ -166,6 +166,30 @@ msort_status msort_sort_host(const void *host_keys, const void *host_vals, void 
                              msort_dtype val_dtype, void *dev_keys, void *dev_vals, void *ws,
                              size_t ws_bytes, msort_stream_t stream);
 
+/* Stable merge of p sorted runs -- the merge() step of P:107 ("merge the
+ * two sorted halves", P:77-84 step 4; the parent's merge(local, tmp) of
+ * P:516) generalised to p runs, i.e. D4 of the distributed sort as its own
+ * call.  Run j is in_keys[run_offsets[j], run_offsets[j+1]) (and in_vals
+ * alike), each sorted ascending; the output keys_out[0, n) (vals_out) holds
+ * all n = run_offsets[p] elements in stable order: ties go to the lower run,
+ * then the lower index.  Out of place (input and output must not overlap).
+ *   run_offsets  HOST array of p + 1 int64, run_offsets[0] = 0,
+ *                non-decreasing (empty runs allowed); 1 <= p <= 128.
+ *   ws           device workspace of msort_merge_runs_workspace_bytes bytes.
+ * Keys only with 3 <= p <= 8: ONE pass over HBM (K5: sample-based tiles,
+ * log2(p) merge rounds in shared memory per tile; the environment variable
+ * MSORT_K5 = 0 / n <= 16 changes that range); otherwise ceil(log2 p) rounds
+ * of the pairwise merge pass.  Asynchronous on `stream`.  Runs that
+ * are not sorted give an unspecified permutation (not checked).
+ * Errors: INVALID_VALUE for bad offsets, overlapping buffers, a short
+ * workspace; as msort_sort_ws otherwise. */
+msort_status msort_merge_runs_workspace_bytes(size_t n, int p, msort_dtype key_dtype,
+                                              msort_dtype val_dtype, size_t *bytes);
+msort_status msort_merge_runs(const void *in_keys, const void *in_vals,
+                              const int64_t *run_offsets, int p, void *keys_out, void *vals_out,
+                              msort_dtype key_dtype, msort_dtype val_dtype, void *ws,
+                              size_t ws_bytes, msort_stream_t stream);
+
 /* --------------------------------------------------------------- multi GPU */
 
 /* Fill `id_out` (host, 128 bytes) with a fresh NCCL unique id.  Rank 0 calls
@@ -355,15 +379,16 @@ int msort_debug_set_quad(int mode);
 
 /* Exchange mode of the distributed sort (D3+D4).  mode 0 (default): one NCCL
  * all-to-all (grouped ncclSend/ncclRecv) into a receive buffer, then the local
- * k-way merge.  mode 1 ("pull", the fused exchange): D1 leaves each sorted
- * shard in the workspace's exchange buffer, every rank publishes that buffer
- * through CUDA IPC, and the first k-way merge round reads its p segments in
- * place from their owners (peer memory over NVLink/NVSwitch) -- the segments
- * cross NVLink once, straight into the merge, with no receive-buffer pass
- * through HBM; a barrier then frees the exchange buffers.  Requires the
- * workspace to come from cudaMalloc (IPC-exportable).  Validated on one GPU
- * through msort_sort_distributed_emulated (the same kernels, peers = local
- * buffers); environment MSORT_EXCHANGE=pull selects it too.  Returns 0. */
+ * k-way merge (one K5 pass for keys with 3..8 ranks, K3 rounds otherwise).
+ * mode 1 ("pull", the fused exchange): D1 leaves each sorted shard in a
+ * buffer the communicator owns (cudaMalloc, IPC-exportable), every rank
+ * publishes it through CUDA IPC, and the merge reads the p segments in place
+ * from their owners (peer memory over NVLink/NVSwitch): for keys with 3..8
+ * ranks D3 and D4 are ONE K5 kernel (no receive buffer, every segment crosses
+ * NVLink once, straight into the merge); otherwise the first K3 round reads
+ * the peers.  A barrier then frees the exchange buffers.  Validated on one
+ * GPU through msort_sort_distributed_emulated (the same kernels, peers =
+ * local buffers); environment MSORT_EXCHANGE=pull selects it too.  Returns 0. */
 int msort_debug_set_exchange(int mode);
 
 #ifdef __cplusplus

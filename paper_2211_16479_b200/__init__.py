@@ -45,6 +45,7 @@ EXPORTED = (
     "msort_segmented_workspace_bytes", "msort_sort_segmented",
     "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
     "msort_plan_tree_rounds", "msort_plan_tree_role", "msort_comm_wrap",
+    "msort_merge_runs", "msort_merge_runs_workspace_bytes",
 )
 
 
@@ -103,6 +104,8 @@ def _load():
     L.msort_plan_tree_rounds.restype = i32
     L.msort_plan_tree_role.argtypes = [i32, i32, i32, c.POINTER(i32)]
     L.msort_plan_tree_role.restype = i32
+    L.msort_merge_runs_workspace_bytes.argtypes = [sz, i32, i32, i32, c.POINTER(c.c_size_t)]
+    L.msort_merge_runs.argtypes = [vp, vp, i64p, i32, vp, vp, i32, i32, vp, sz, vp]
     L.msort_tile_size.argtypes = [i32, i32]
     L.msort_tile_size.restype = i32
     for f in ("msort_sort", "msort_sort_pairs", "msort_workspace_bytes", "msort_sort_ws",
@@ -113,7 +116,7 @@ def _load():
               "msort_plan_narrow", "msort_plan_fill", "msort_profile_read",
               "msort_segmented_workspace_bytes", "msort_sort_segmented",
               "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
-              "msort_comm_wrap"):
+              "msort_comm_wrap", "msort_merge_runs", "msort_merge_runs_workspace_bytes"):
         getattr(L, f).restype = i32
     return L
 
@@ -323,6 +326,51 @@ def msort_sort_segmented(keys: torch.Tensor, seg_offsets, vals: torch.Tensor | N
                                         kd, vd, _ptr(ws), ws.numel(),
                                         ctypes.c_void_p(_stream(stream))), "msort_sort_segmented")
     return keys, vals
+
+
+def msort_merge_runs(in_keys: torch.Tensor, run_offsets, keys_out: torch.Tensor | None = None,
+                     in_vals: torch.Tensor | None = None, vals_out: torch.Tensor | None = None,
+                     ws: torch.Tensor | None = None, stream=None):
+    """Stable merge of p sorted runs in_keys[off[j]:off[j+1]] (include/msort.h
+    msort_merge_runs; ties to the lower run).  run_offsets: p + 1 host
+    offsets (list / numpy / CPU tensor).  Returns (keys_out, vals_out)."""
+    _check_tensor(in_keys, "in_keys")
+    if isinstance(run_offsets, torch.Tensor):
+        run_offsets = run_offsets.detach().cpu().numpy()
+    off = np.ascontiguousarray(np.asarray(run_offsets, dtype=np.int64))
+    if off.ndim != 1 or off.size < 2:
+        raise ValueError("run_offsets must hold p + 1 >= 2 offsets")
+    p = off.size - 1
+    n = in_keys.numel()
+    if int(off[-1]) != n:
+        raise ValueError("run_offsets[-1] must equal in_keys.numel()")
+    if keys_out is None:
+        keys_out = torch.empty_like(in_keys)
+    _check_tensor(keys_out, "keys_out")
+    if keys_out.numel() != n or keys_out.dtype != in_keys.dtype or keys_out.device != in_keys.device:
+        raise ValueError("keys_out must match in_keys (size, dtype, device)")
+    if in_vals is not None:
+        _check_tensor(in_vals, "in_vals")
+        if in_vals.numel() != n or in_vals.device != in_keys.device:
+            raise ValueError("in_vals must match in_keys (size, device)")
+        if vals_out is None:
+            vals_out = torch.empty_like(in_vals)
+        _check_tensor(vals_out, "vals_out")
+        if vals_out.numel() != n or vals_out.dtype != in_vals.dtype:
+            raise ValueError("vals_out must match in_vals")
+    kd, vd = _dt(in_keys), _vdt(in_vals)
+    if ws is None:
+        nb = ctypes.c_size_t()
+        _check(lib.msort_merge_runs_workspace_bytes(n, p, kd, vd, ctypes.byref(nb)),
+               "msort_merge_runs_workspace_bytes")
+        ws = torch.empty(max(nb.value, 256), dtype=torch.uint8, device=in_keys.device)
+        _keep_for(ws, stream)
+    with _on(in_keys.device):
+        _check(lib.msort_merge_runs(_ptr(in_keys), _ptr(in_vals),
+                                    off.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), p,
+                                    _ptr(keys_out), _ptr(vals_out), kd, vd, _ptr(ws), ws.numel(),
+                                    ctypes.c_void_p(_stream(stream))), "msort_merge_runs")
+    return keys_out, vals_out
 
 
 def sort(x: torch.Tensor) -> torch.Tensor:

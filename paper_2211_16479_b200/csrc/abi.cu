@@ -425,6 +425,55 @@ msort_status msort_sort_host(const void* host_keys, const void* host_vals, void*
   return MSORT_SUCCESS;
 }
 
+msort_status msort_merge_runs_workspace_bytes(size_t n, int p, msort_dtype key_dtype,
+                                              msort_dtype val_dtype, size_t* bytes) {
+  if (!bytes || !dtype_size(key_dtype) || p < 1 ||
+      (val_dtype != MSORT_NONE && val_dtype != MSORT_UINT32 && val_dtype != MSORT_INT32)) {
+    set_error("bad argument to msort_merge_runs_workspace_bytes");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  *bytes = merge_runs_ws_bytes(n, p, key_dtype, val_dtype);
+  return MSORT_SUCCESS;
+}
+
+msort_status msort_merge_runs(const void* in_keys, const void* in_vals,
+                              const int64_t* run_offsets, int p, void* keys_out, void* vals_out,
+                              msort_dtype key_dtype, msort_dtype val_dtype, void* ws,
+                              size_t ws_bytes, msort_stream_t stream) {
+  if (!run_offsets || p < 1 || p > 128) {
+    set_error("msort_merge_runs: run_offsets NULL or p outside [1, 128]");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  if (run_offsets[0] != 0) {
+    set_error("msort_merge_runs: run_offsets[0] must be 0");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  for (int j = 0; j < p; ++j)
+    if (run_offsets[j + 1] < run_offsets[j]) {
+      set_error("msort_merge_runs: run_offsets decrease at run " + std::to_string(j));
+      return MSORT_ERROR_INVALID_VALUE;
+    }
+  const size_t n = (size_t)run_offsets[p];
+  MSORT_TRY(validate_out(in_keys, in_vals, keys_out, vals_out, n, key_dtype, val_dtype));
+  const size_t wk = dtype_size(key_dtype);
+  if (n > 0 && (overlaps(in_keys, n * wk, keys_out, n * wk) ||
+                (val_dtype != MSORT_NONE && overlaps(in_vals, n * 4, vals_out, n * 4)))) {
+    set_error("msort_merge_runs: input and output overlap (the merge is out of place)");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  if (n == 0) return MSORT_SUCCESS;
+  MSORT_TRY(check_device());
+  MSORT_TRY(validate_ws(keys_out, vals_out, n, key_dtype, val_dtype, ws, ws_bytes,
+                        merge_runs_ws_bytes(n, p, key_dtype, val_dtype)));
+  if (overlaps(ws, ws_bytes, in_keys, n * wk) ||
+      (val_dtype != MSORT_NONE && overlaps(ws, ws_bytes, in_vals, n * 4))) {
+    set_error("workspace overlaps the input");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  return merge_runs_dispatch(in_keys, in_vals, run_offsets, p, keys_out, vals_out, key_dtype,
+                             val_dtype, ws, ws_bytes, (cudaStream_t)stream);
+}
+
 msort_status msort_comm_unique_id(void* id_out) {
   if (!id_out) {
     set_error("id_out is NULL");

@@ -1,0 +1,412 @@
+// k5_kway.cuh -- K5, the one-pass stable p-way merge.
+//
+// The distributed sort ends with p sorted runs on each rank (one segment from
+// every rank, in source-rank order); D4 merges them into the rank's output.
+// The paper does the corresponding final merges pairwise up its rank tree
+// (merge(local, tmp)); here all p runs are merged in ONE pass over HBM:
+// every key is read once and written once (2 n wk bytes), instead of once per
+// level of a pairwise merge tree (ceil(log2 p) passes).  Ties go to the lower
+// run (source rank), so the result is the stable order of the rank-major
+// concatenation (R10/R11).  Keys only (any keys-only output is
+// unique; equal keys are indistinguishable).  Included by sort_single.cu
+// after merge_keys_dual / put_outputs.
+//
+// Tiles.  Run j is sampled every S keys (its keys at 0, S, 2S, ...); the
+// samples of all runs, merged stably (ties to the lower run, then the lower
+// index; k5_sample_level, payload = sample id), are in the stable order of
+// the output.  Every g-th merged sample starts a tile; tile t's start STATE
+// is the number of keys of each run that precede its sample x = (key v,
+// run k, index i) in the stable order:
+//     c_j = #{R_j <= v} (j < k),   c_k = i,   c_j = #{R_j < v} (j > k),
+// found by a binary search per run inside the S keys between the run's
+// samples around x (k5_bounds).  Between two consecutive
+// tile starts lie g merged samples, and run j contributes fewer than
+// (q_j + 1) S keys when q_j of them are its own, so a tile holds at most
+//     S (g + p) - p  keys  <=  C (the tile capacity)
+// by the choice of S -- no tile is ever cut, whatever the key distribution.
+//
+// Merge (k5_merge, one CTA per tile, K6's engine generalised): the tile's p
+// windows arrive by TMA bulk copies (cp.async.bulk, SASS UBLKCP) between
+// MIN/MAX sentinels; ceil(log2 p) rounds of pairwise merges in shared memory
+// (round r merges adjacent groups of 2^r runs, lower group first on ties:
+// each thread VT outputs as two merge chains, merge_keys_dual); the last
+// round writes at the destination's 16-byte phase and the tile leaves by one
+// bulk store.  The runs may live in other GPUs' memory (the pull exchange:
+// peer pointers mapped through CUDA IPC), so the exchange and the merge are
+// one kernel and the segments cross NVLink once, straight into the merge.
+#pragma once
+
+namespace msort {
+
+constexpr int kK5MaxRuns = 16;
+#ifndef MSORT_K5_G
+#define MSORT_K5_G 8  // merged samples per K5 tile, per run
+#endif
+#ifndef MSORT_K5_MINB
+#define MSORT_K5_MINB 6  // K5 CTAs per SM the register budget allows (4-byte keys)
+#endif  // runs merged in one pass (more: K3 rounds first)
+
+// Runs of one K5 merge: run j = n[j] keys at k[j] (device pointers, possibly
+// into a peer GPU's memory).
+struct K5Runs {
+  int p;
+  const void* k[kK5MaxRuns];
+  int64_t n[kK5MaxRuns];
+  int64_t soff[kK5MaxRuns + 1];  // first sample of run j in the sample arrays
+  int64_t S;                      // sample stride
+  int64_t g;                      // merged samples per tile
+  int64_t ntiles;                 // T (tile t = [state t, state t+1))
+};
+
+// Shape of the merge CTA: NT threads x VT keys per thread and round;
+// capacity C = (NT - P2 / 2) * VT keys for P2 (p rounded up to a power of
+// two) runs, so that a round's ceil(len / VT) threads per pair fit in NT.
+template <int NT, int VT>
+struct K5Shape {
+  static constexpr int cap(int P2) { return (NT - P2 / 2) * VT; }
+  // keys of shared memory: capacity + per-run slack (<= 3 phase + 2
+  // sentinels + 3 rounding) + guard
+  static constexpr int keys(int P2) { return cap(P2) + 8 * P2 + 16; }
+};
+
+// ---------------------------------------------------------------- partition
+// Run j's samples are its keys at 0, S, 2S, ...; sample x = (run k, index
+// m) is stored at skey[soff[k] + m] with id x.  The sample runs are merged
+// stably (ties to the lower run, then the lower index) in ceil(log2 p) small
+// levels; every g-th merged sample starts a tile.
+
+// first index in [lo, hi) with a[i] > v (UPPER) or a[i] >= v
+template <class K, bool UPPER>
+__device__ __forceinline__ int64_t k5_bound(const K* __restrict__ a, int64_t lo, int64_t hi, K v) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const K x = a[mid];
+    if (UPPER ? !(v < x) : (x < v)) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int k5_run_of(const K5Runs& R, int64_t x) {
+  int k = 0;
+  while (k + 1 < R.p && R.soff[k + 1] <= x) ++k;
+  return k;
+}
+
+// skey[x] = the sample's key, sid[x] = x (its id: run and index follow from
+// soff).
+template <class K>
+__global__ void __launch_bounds__(256)
+    k5_samples(const __grid_constant__ K5Runs R, K* __restrict__ skey,
+               uint32_t* __restrict__ sid) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= R.soff[R.p]) return;
+  const int k = k5_run_of(R, x);
+  skey[x] = static_cast<const K*>(R.k[k])[(x - R.soff[k]) * R.S];
+  sid[x] = (uint32_t)x;
+}
+
+// One level of the sample merge: runs q = [ro[q], ro[q+1]) of (ik, iv); pair
+// m = (runs 2m, 2m+1) merged stably (ties to run 2m) into (ok, ov) at the
+// same place (a lone last run is copied).  One CTA per output chunk of <= Q
+// samples of one pair: the chunk's two co-ranks by 32-ary warp searches in
+// global memory (L2-resident arrays), both windows staged in shared memory,
+// each thread merges VT outputs there (merge path + serial merge).
+constexpr int kK5LvlNT = 256, kK5LvlVT = 8, kK5LvlQ = kK5LvlNT * kK5LvlVT;
+struct K5Level {
+  int q;                            // runs at this level
+  int64_t ro[kK5MaxRuns + 1];       // their offsets
+  int64_t c0[kK5MaxRuns / 2 + 2];   // first chunk of each pair (prefix)
+};
+
+template <class K>
+__device__ __forceinline__ int64_t k5_corank_warp(const K* __restrict__ A, int64_t na,
+                                                  const K* __restrict__ B, int64_t nb, int64_t d,
+                                                  int lane) {
+  int64_t lo = d - nb > 0 ? d - nb : 0, hi = d < na ? d : na;
+  while (hi > lo) {  // i(d) = min{i : i = min(d, na) or A[i] > B[d-1-i]}
+    const int64_t span = hi - lo;
+    const int64_t step = (span + 31) >> 5;
+    const int64_t off = step * (lane + 1);
+    const int64_t q = lo + (off < span ? off : span) - 1;
+    const bool pred = A[q] > B[d - 1 - q];
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (m == 0) {
+      lo = hi;
+    } else {
+      const int f = __ffs(m) - 1;
+      const int64_t pf = __shfl_sync(0xffffffffu, q, f);
+      const int64_t pp = __shfl_sync(0xffffffffu, q, f > 0 ? f - 1 : 0);
+      hi = pf;
+      if (f > 0) lo = pp + 1;
+    }
+  }
+  return lo;
+}
+
+template <class K>
+__global__ void __launch_bounds__(kK5LvlNT)
+    k5_sample_level(const __grid_constant__ K5Level L, const K* __restrict__ ik,
+                    const uint32_t* __restrict__ iv, K* __restrict__ ok,
+                    uint32_t* __restrict__ ov) {
+  constexpr int Q = kK5LvlQ, VT = kK5LvlVT;
+  __shared__ K sk[Q + 2];
+  __shared__ uint32_t sv[Q + 2];
+  __shared__ int64_t s_co[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int npair = (L.q + 1) / 2;
+  int m = 0;
+  while (m + 1 < npair && L.c0[m + 1] <= (int64_t)blockIdx.x) ++m;
+  const int64_t a0 = L.ro[2 * m], a1 = L.ro[min(2 * m + 1, L.q)];
+  const int64_t b1 = L.ro[min(2 * m + 2, L.q)];
+  const int64_t na = a1 - a0, nb = b1 - a1;
+  const int64_t d0 = ((int64_t)blockIdx.x - L.c0[m]) * Q;
+  const int64_t d1 = min(d0 + Q, na + nb);
+  const K* A = ik + a0;
+  const K* B = ik + a1;
+  if (warp < 2) {
+    const int64_t d = warp == 0 ? d0 : d1;
+    const int64_t i = d == na + nb ? na : k5_corank_warp<K>(A, na, B, nb, d, lane);
+    if (lane == 0) s_co[warp] = i;
+  }
+  __syncthreads();
+  const int64_t i0 = s_co[0], i1 = s_co[1];
+  const int la = (int)(i1 - i0), lb = (int)((d1 - i1) - (d0 - i0));
+  const int64_t j0 = d0 - i0;
+  for (int e = tid; e < la + lb; e += kK5LvlNT) {
+    const int64_t src = e < la ? a0 + i0 + e : a1 + j0 + (e - la);
+    sk[e] = ik[src];
+    sv[e] = iv[src];
+  }
+  __syncthreads();
+  const int d = tid * VT, tot = la + lb;
+  if (d < tot) {
+    int lo = d - lb > 0 ? d - lb : 0, hi = d < la ? d : la;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sk[mid] > sk[la + d - 1 - mid]) hi = mid;
+      else lo = mid + 1;
+    }
+    int i = lo, j = la + (d - lo);
+    const int e = min(d + VT, tot);
+    for (int o = d; o < e; ++o) {
+      const bool takeB = j < tot && (i >= la || sk[j] < sk[i]);
+      const int src = takeB ? j : i;
+      ok[a0 + d0 + o] = sk[src];
+      ov[a0 + d0 + o] = sv[src];
+      i += takeB ? 0 : 1;
+      j += takeB ? 1 : 0;
+    }
+  }
+}
+
+// states[t * p + j] for t = 0..T: tile t's start state (t = T: the ends).
+// One thread per (t, j): the merged sample x = mid[t g] = (key v, run k,
+// index i);
+//     c_j = #{R_j <= v} (j < k),   c_k = i,   c_j = #{R_j < v} (j > k),
+// searched only between run j's samples around x: with r = rank_j(x) (the
+// number of run j's samples before x, by a search in its sample array), the
+// sample at (r - 1) S precedes x and the one at r S does not, so
+// c_j in [(r - 1) S + 1, r S]  (c_j = 0 when r = 0).
+template <class K>
+__global__ void __launch_bounds__(256)
+    k5_bounds(const __grid_constant__ K5Runs R, const K* __restrict__ skey,
+              const K* __restrict__ mkey, const uint32_t* __restrict__ mid,
+              int64_t* __restrict__ states) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = R.p;
+  if (i >= (R.ntiles + 1) * p) return;
+  const int64_t t = i / p;
+  const int j = (int)(i - t * p);
+  int64_t c;
+  if (t == 0) {
+    c = 0;
+  } else if (t == R.ntiles) {
+    c = R.n[j];
+  } else {
+    const int64_t x = mid[t * R.g];
+    const int k = k5_run_of(R, x);
+    if (j == k) {
+      c = (x - R.soff[k]) * R.S;  // x itself starts the tile
+    } else {
+      const K v = mkey[t * R.g];
+      const int64_t r =
+          (j < k ? k5_bound<K, true>(skey, R.soff[j], R.soff[j + 1], v)
+                 : k5_bound<K, false>(skey, R.soff[j], R.soff[j + 1], v)) - R.soff[j];
+      const K* run = static_cast<const K*>(R.k[j]);
+      const int64_t lo = r == 0 ? 0 : (r - 1) * R.S + 1, hi = min(r * R.S, R.n[j]);
+      c = j < k ? k5_bound<K, true>(run, lo, hi, v)   // lower runs: keys <= v first
+                : k5_bound<K, false>(run, lo, hi, v); // higher runs: keys < v first
+    }
+  }
+  states[i] = c;
+}
+
+// ---------------------------------------------------------------- merge
+// One CTA per tile; P2 = p rounded up to a power of two (runs p..P2-1 are
+// empty), R = log2(P2) rounds.  The whole round structure is laid out once
+// by thread 0 (sizes are known from the tile's states): round r has P2 >> r
+// runs; run i of round r = the merge of runs 2i, 2i+1 of round r-1; round
+// r's pair m = (run 2m = A, run 2m+1 = B) sits in shared memory as
+// [MIN | B | MAX .. MIN | A | MAX] (B below A: merge_keys_dual clamps A at
+// its MAX and B at its MIN sentinel with one bound each); its threads are
+// [tp[r][m], tp[r][m+1]), one per VT outputs.
+template <class K, int NT, int VT, int MINB, int P2>
+__global__ void __launch_bounds__(NT, MINB)
+    k5_merge(const __grid_constant__ K5Runs R, const int64_t* __restrict__ states,
+             K* __restrict__ dst) {
+  constexpr int RR = __builtin_ctz(P2);  // rounds
+  constexpr uint32_t Z = sizeof(K);
+  extern __shared__ __align__(16) unsigned char smem[];
+  K* sk = reinterpret_cast<K*>(smem);
+  const char* sb = reinterpret_cast<const char*>(smem);
+  __shared__ uint64_t bar;
+  __shared__ int s_len[RR + 1][P2];     // run sizes per round (round RR: the tile)
+  __shared__ int s_off[RR + 1][P2];     // run offsets (keys) per round; RR: the output phase
+  __shared__ int s_tp[RR][P2 / 2 + 1];  // first thread of each pair per round
+  __shared__ int cr[NT + 1];            // co-ranks of the threads' first diagonals
+  __shared__ int64_t s_src[P2];
+  __shared__ int64_t s_out;
+  const int tid = threadIdx.x;
+  const int p = R.p;
+  const int64_t t = blockIdx.x;
+
+  if (tid == 0) {
+    mbar_init(&bar, 32);
+    fence_mbar_init();
+  }
+  if (tid < P2) {
+    int64_t a = 0, b = 0;
+    if (tid < p) a = states[t * p + tid], b = states[(t + 1) * p + tid];
+    s_src[tid] = a;
+    s_len[0][tid] = (int)(b - a);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // round 0: windows at their global 16-byte phase (TMA), MIN slot before
+    int o = 0;
+    for (int m = 0; m < P2 / 2; ++m) {
+#pragma unroll
+      for (int h = 1; h >= 0; --h) {
+        const int j = 2 * m + h;
+        const int ph = j < p ? stage_offset(static_cast<const K*>(R.k[j]) + s_src[j]) : 0;
+        const int at = ((o + 4) & ~3) + ph;
+        s_off[0][j] = at;
+        o = at + s_len[0][j] + 1;
+      }
+    }
+    int64_t out = 0;
+    for (int j = 0; j < p; ++j) out += s_src[j];
+    s_out = out;
+    // rounds 1..RR-1: 16-byte aligned runs (a full thread's outputs leave as
+    // vectors); round RR (the output) at the destination's 16-byte phase
+#pragma unroll
+    for (int r = 1; r <= RR; ++r) {
+      int o2 = 0;
+      const int nr = P2 >> r;
+      for (int q = 0; q < (nr + 1) / 2; ++q) {
+#pragma unroll
+        for (int h = 1; h >= 0; --h) {
+          const int j = 2 * q + h;
+          if (j >= nr) continue;
+          s_len[r][j] = s_len[r - 1][2 * j] + s_len[r - 1][2 * j + 1];
+          const int at = (o2 + 4) & ~3;
+          s_off[r][j] = at;
+          o2 = at + s_len[r][j] + 1;
+        }
+      }
+    }
+    s_off[RR][0] = stage_offset(dst + out);
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
+      int tp = 0;
+      const int np = P2 >> (r + 1);
+      // the last round's diagonals are shifted by the output phase ph
+      // (thread k: [k VT - ph, (k+1) VT - ph)), so every full thread's
+      // outputs start 16-byte aligned in the phase-matched output buffer
+      const int sh = r + 1 == RR ? s_off[RR][0] : 0;
+      for (int m = 0; m < np; ++m) {
+        s_tp[r][m] = tp;
+        tp += (s_len[r + 1][m] + sh + VT - 1) / VT;
+      }
+      s_tp[r][np] = tp;
+    }
+    uint32_t tx = 0;
+    for (int j = 0; j < p; ++j)
+      tx += window_bulk_bytes(static_cast<const K*>(R.k[j]) + s_src[j], s_len[0][j]);
+    mbar_expect_tx(&bar, tx);
+  }
+  __syncthreads();
+  if (tid < P2) {
+    sk[s_off[0][tid] - 1] = KeyTraits<K>::min_key();
+    sk[s_off[0][tid] + s_len[0][tid]] = KeyTraits<K>::max_key();
+  }
+  if (tid < 32) {
+    for (int j = 0; j < p; ++j) {
+      const K* g = static_cast<const K*>(R.k[j]) + s_src[j];
+      stage_window(sk + s_off[0][j], g, s_len[0][j], &bar, tid == 0, tid, 32);
+    }
+    mbar_arrive(&bar);
+  }
+  mbar_wait(&bar, 0);
+  __syncthreads();  // sentinels written by other threads
+
+  K key[VT];
+  const int tot = s_len[RR][0];
+#pragma unroll 1
+  for (int r = 0; r < RR; ++r) {
+    const int npair = P2 >> (r + 1);
+    int m = 0;
+#pragma unroll
+    for (int q = 1; q < P2 / 2; ++q)
+      if (q < npair && s_tp[r][q] <= tid) m = q;
+    const bool act = tid < s_tp[r][npair];
+    const int la = s_len[r][2 * m], lb = s_len[r][2 * m + 1], len = la + lb;
+    const uint32_t oa = (uint32_t)s_off[r][2 * m] * Z, ob = (uint32_t)s_off[r][2 * m + 1] * Z;
+    const int sh = r + 1 == RR ? s_off[RR][0] : 0;  // output phase (last round)
+    int d = 0, c = 0, i0 = 0;
+    if (act) {
+      d = max(0, (tid - s_tp[r][m]) * VT - sh);
+      c = min((tid - s_tp[r][m] + 1) * VT - sh, len) - d;
+      i0 = merge_path_off<K>(sb, oa, la, ob, lb, d);
+      cr[tid] = i0;
+    }
+    __syncthreads();
+    if (act) {
+      const int i1 = d + c == len ? la : cr[tid + 1];
+      merge_keys_dual<K, VT>(sb, oa + (uint32_t)i0 * Z, oa + (uint32_t)la * Z,
+                             ob + (uint32_t)(d - i0) * Z, oa + (uint32_t)i1 * Z,
+                             ob + (uint32_t)(d + c - i1) * Z, ob - Z, key);
+    }
+    __syncthreads();  // every thread has read its inputs: the buffer is free
+    if (r + 1 < RR) {
+      if (act) put_outputs<K, VT>(sk + s_off[r + 1][m] + d, key, c);
+      if (tid < npair) {
+        sk[s_off[r + 1][tid] - 1] = KeyTraits<K>::min_key();
+        sk[s_off[r + 1][tid] + s_len[r + 1][tid]] = KeyTraits<K>::max_key();
+      }
+      __syncthreads();
+    } else {
+      if (act) put_outputs<K, VT>(sk + sh + d, key, c);  // full threads: (sh + d) % 4 == 0
+    }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (tid < 32) {
+    const int ph = s_off[RR][0];
+    K* go = dst + s_out;
+    int h, mid;
+    window_split(go, tot, h, mid);
+    if (tid == 0 && mid) {
+      bulk_s2g(go + h, sk + ph + h, (uint32_t)(mid * sizeof(K)));
+      bulk_commit();
+    }
+    for (int i = tid; i < tot - mid; i += 32) {
+      const int j = i < h ? i : i + mid;
+      go[j] = sk[ph + j];
+    }
+    if (tid == 0 && mid) bulk_wait_read<0>();  // shared memory must outlive the copy's reads
+  }
+}
+
+}  // namespace msort

@@ -91,6 +91,23 @@ struct PullRuns {
 msort_status pull_round_dispatch(const PullRuns& pr, void* out_k, void* out_v, int64_t* off_out,
                                  msort_dtype kd, msort_dtype vd, void* part_ws, cudaStream_t s);
 
+// D4 in one pass (K5, k5_kway.cuh): stable merge of pr.runs sorted runs of
+// keys (run j = pr.n[j] keys at pr.k[j], possibly peer memory; ties to the
+// lower run) into dst.  Keys only.  scratch: device memory of at least
+// kway5_scratch_bytes(pr, kd) bytes (a small fraction of the keys), which is
+// SIZE_MAX when K5 does not take that run count (3..8 by default, see
+// Kernels::k5_max_runs) -- the caller then merges by K3 rounds.
+constexpr int kK5Runs = 16;
+msort_status kway5_dispatch(const PullRuns& pr, void* dst, msort_dtype kd, void* scratch,
+                            size_t scratch_bytes, cudaStream_t s);
+size_t kway5_scratch_bytes(const PullRuns& pr, msort_dtype kd);
+
+// msort_merge_runs: workspace bytes and the call (sort_single.cu).
+size_t merge_runs_ws_bytes(size_t n, int p, msort_dtype kd, msort_dtype vd);
+msort_status merge_runs_dispatch(const void* ik, const void* iv, const int64_t* off, int p,
+                                 void* ok, void* ov, msort_dtype kd, msort_dtype vd, void* ws,
+                                 size_t ws_bytes, cudaStream_t s);
+
 // Exchange mode of the distributed sort: 0 = NCCL all-to-all into a receive
 // buffer then a local k-way merge; 1 = pull (the first merge round reads the
 // peers' sorted segments in place).  (sort_dist.cu, msort_debug_set_exchange)

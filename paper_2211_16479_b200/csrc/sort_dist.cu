@@ -47,6 +47,12 @@ struct msort_comm_s {
   // small device scratch of the communicator's own collectives (sizes and
   // agreement flags of the rank-tree gather): 8 * (2 * world + 64) bytes
   uint64_t* dscratch = nullptr;
+  // pull exchange: the sorted shard that the peers read in place lives in a
+  // buffer the communicator owns, from cudaMalloc (IPC-exportable whatever
+  // allocator the caller's workspace came from); grown on demand and reused
+  // (its IPC handle, opened once by each peer, stays valid between calls)
+  void* xbuf = nullptr;
+  size_t xbuf_bytes = 0;
 };
 
 namespace msort {
@@ -632,6 +638,7 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
     int rounds = 0;
     while ((1 << rounds) < p) ++rounds;
     std::vector<std::vector<int64_t>> offs(nloc);
+    std::vector<char> one_pass(nloc, 0);
     for (int l = 0; l < nloc; ++l) {
       const int me = C.rank_of(l);
       offs[l].assign((size_t)p + 1, 0);
@@ -643,6 +650,14 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
         pr.k[j] = (const char*)bk[j] + a * wk;
         pr.v[j] = pairs ? bv[j] + a : nullptr;
         pr.n[j] = b - a;
+      }
+      // keys only, 3..16 runs: the whole D4 is ONE K5 pass reading every
+      // segment from its owner (D3 + D4 in one kernel, no receive buffer)
+      if (!pairs && p >= 3 && p <= kK5Runs &&
+          kway5_scratch_bytes(pr, kd) <= io[l].ws.sort_ws_bytes) {
+        MSORT_TRY(kway5_dispatch(pr, io[l].keys, kd, io[l].ws.sort_ws, io[l].ws.sort_ws_bytes, s));
+        one_pass[l] = 1;
+        continue;
       }
       char* sw = io[l].ws.sort_ws;
       void* tk = sw;
@@ -656,7 +671,7 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
     MSORT_TRY(C.barrier(io));
     if (rounds > 1) {
       for (int l = 0; l < nloc; ++l) {
-        if (io[l].n == 0) continue;
+        if (io[l].n == 0 || one_pass[l]) continue;
         char* sw = io[l].ws.sort_ws;
         void* tk = sw;
         void* tv = pairs ? sw + align_up(io[l].n * wk, 256) : nullptr;
@@ -669,14 +684,27 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
   }
   // D3: exchange
   MSORT_TRY(C.exchange(io, S, kd, vd));
-  // D4: k-way merge of the received runs (source-rank order) into keys
+  // D4: k-way merge of the received runs (source-rank order) into keys --
+  // one K5 pass for keys only with 3..16 runs, else rounds of K3
   for (int l = 0; l < nloc; ++l) {
     int me = C.rank_of(l);
     std::vector<int64_t> off(p + 1);
     off[0] = 0;
     for (int j = 0; j < p; ++j) off[j + 1] = off[j] + S[(size_t)(me + 1) * p + j] - S[(size_t)me * p + j];
     if (io[l].n == 0) continue;
-    char* sw = io[l].ws.sort_ws;  // sort workspace doubles as the ping-pong buffer
+    char* sw = io[l].ws.sort_ws;  // sort workspace doubles as the ping-pong buffer / K5 scratch
+    if (vd == MSORT_NONE && p >= 3 && p <= kK5Runs) {
+      PullRuns pr{};
+      pr.runs = p;
+      for (int j = 0; j < p; ++j) {
+        pr.k[j] = (const char*)io[l].ws.rk + off[j] * wk;
+        pr.n[j] = off[j + 1] - off[j];
+      }
+      if (kway5_scratch_bytes(pr, kd) <= io[l].ws.sort_ws_bytes) {
+        MSORT_TRY(kway5_dispatch(pr, io[l].keys, kd, sw, io[l].ws.sort_ws_bytes, s));
+        continue;
+      }
+    }
     void* tk = sw;
     void* tv = vd != MSORT_NONE ? sw + align_up(io[l].n * wk, 256) : nullptr;
     void* part = sw + align_up(io[l].n * wk, 256) + (vd != MSORT_NONE ? align_up(io[l].n * 4, 256) : 0);
@@ -701,8 +729,24 @@ msort_status dist_nccl(const void* in_keys, const void* in_vals, void* keys, voi
   const bool pull = exchange_mode() == 1 && comm->world > 1;
   RankIO io{in_keys, pv ? in_vals : nullptr, keys, pv ? vals : nullptr, n,
             carve(ws, n, kd, vd, comm->world), nullptr, nullptr};
-  io.sk = pull ? io.ws.rk : io.keys;
-  io.sv = pull ? io.ws.rv : io.vals;
+  io.sk = io.keys;
+  io.sv = io.vals;
+  if (pull) {
+    // the sorted shard goes to the communicator's IPC-exportable buffer
+    const size_t kb = align_up(n * dtype_size(kd), 256);
+    const size_t need = std::max<size_t>(kb + (pv ? align_up(n * 4, 256) : 0), 256);
+    if (need > comm->xbuf_bytes) {
+      // the previous call ended with a barrier after every peer's reads, so
+      // the old buffer is free; wait for this stream's earlier work too
+      MSORT_CUDA_TRY(cudaStreamSynchronize(s));
+      if (comm->xbuf) cudaFree(comm->xbuf);
+      comm->xbuf = nullptr, comm->xbuf_bytes = 0;
+      MSORT_CUDA_TRY(cudaMalloc(&comm->xbuf, need + need / 8));
+      comm->xbuf_bytes = need + need / 8;
+    }
+    io.sk = comm->xbuf;
+    io.sv = pv ? static_cast<char*>(comm->xbuf) + kb : nullptr;
+  }
   NcclColl C{comm, s};
   return dist_run(C, &io, 1, kd, vd, s, split_out, pull);
 }
@@ -1040,6 +1084,7 @@ msort_status comm_destroy(msort_comm_s* c) {
   ncclResult_t r = (c->aborted || !c->owned) ? ncclSuccess : ncclCommDestroy(c->comm);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->dscratch) cudaFree(c->dscratch);
+  if (c->xbuf) cudaFree(c->xbuf);
   delete c;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
   return MSORT_SUCCESS;

@@ -220,6 +220,7 @@ __device__ __forceinline__ void store_vec(K* dst, const K (&key)[VT]) {
 
 }  // namespace msort
 #include "k6_quad.cuh"
+#include "k5_kway.cuh"
 namespace msort {
 
 // Compare-exchange of the keys-only register network (min and max; any
@@ -1108,12 +1109,161 @@ struct Kernels {
     return launch_k3(src, (tiles + src.ch - 1) / src.ch, ctr, s, KC_KWAY);
   }
 
+  // ---- K5: one-pass p-way merge (keys only; k5_kway.cuh) -------------
+  static constexpr int K5NT = sizeof(K) == 4 ? 128 : 256;
+  static constexpr int K5VT = sizeof(K) == 4 ? 68 : 34;
+  static constexpr int K5MINB = sizeof(K) == 4 ? MSORT_K5_MINB : 2;
+  using K5S = K5Shape<K5NT, K5VT>;
+  // shared memory for any p (the capacity, and with it the buffer, is
+  // largest for two runs)
+  static constexpr size_t k5_smem = (size_t)K5S::keys(2) * sizeof(K);
+  static int P2of(int p) {
+    int P2 = 1;
+    while (P2 < p) P2 <<= 1;
+    return P2;
+  }
+  // Tile geometry for p runs of the given sizes: fills R.S, R.g, R.soff,
+  // R.ntiles; returns the scratch bytes the partition needs.
+  static size_t k5_plan(K5Runs& R) {
+    const int p = R.p;
+    const int64_t C = K5S::cap(P2of(p));
+    R.g = MSORT_K5_G * (int64_t)p;  // merged samples per tile (utilisation g / (g + p))
+    R.S = std::max<int64_t>(1, (C + p) / (R.g + p));  // tile <= S (g + p) - p <= C
+    R.soff[0] = 0;
+    for (int j = 0; j < p; ++j) R.soff[j + 1] = R.soff[j] + (R.n[j] + R.S - 1) / R.S;
+    const int64_t M = R.soff[p];
+    R.ntiles = std::max<int64_t>(1, (M + R.g - 1) / R.g);
+    return 3 * align_up((size_t)M * sizeof(K), 256) + 3 * align_up((size_t)M * 4, 256) +
+           align_up((size_t)(R.ntiles + 1) * p * 8, 256);
+  }
+  // Merge the runs of R (R.p in [2, kK5MaxRuns], R.k/R.n set) into dst in one
+  // pass.  scratch: >= the bytes k5_plan returns, device memory not
+  // overlapping the runs or dst.
+  // Largest run count merged by K5 automatically: 8 (measured on 2^28 keys:
+  // one K5 pass beats the ceil(log2 p) K3 rounds for p = 3..8 -- e.g. 1.12
+  // vs 1.22 ms at p = 8 -- but not at 16: 1.74 vs 1.62 ms).  The environment
+  // variable MSORT_K5 overrides it for A/B runs and tests: 0 = never, n =
+  // up to n runs (<= 16).
+  static int k5_max_runs() {
+    const char* e = getenv("MSORT_K5");
+    if (!e || !*e) return 8;
+    return std::min(atoi(e), kK5MaxRuns);
+  }
+  static msort_status kway5(K5Runs R, K* dst, char* scratch, size_t scratch_bytes,
+                            cudaStream_t s) {
+    const int p = R.p;
+    if (p < 2 || p > kK5MaxRuns) {
+      set_error("k5: run count out of range");
+      return MSORT_ERROR_NOT_SUPPORTED;
+    }
+    const size_t need = k5_plan(R);
+    if (need > scratch_bytes) {
+      set_error("k5: scratch too small");
+      return MSORT_ERROR_INVALID_VALUE;
+    }
+    const int64_t M = R.soff[p];
+    if (M == 0) return MSORT_SUCCESS;  // every run empty
+    if (M >= ((int64_t)1 << 32)) {
+      set_error("k5: too many samples");
+      return MSORT_ERROR_NOT_SUPPORTED;
+    }
+    int dev = 0;
+    MSORT_CUDA_TRY(cudaGetDevice(&dev));
+    MSORT_TRY(k5_init(dev));
+    char* w = scratch;
+    auto take = [&](size_t b) {
+      char* q = w;
+      w += align_up(b, 256);
+      return q;
+    };
+    K* skey = reinterpret_cast<K*>(take((size_t)M * sizeof(K)));
+    K* tkey = reinterpret_cast<K*>(take((size_t)M * sizeof(K)));
+    K* mkey = reinterpret_cast<K*>(take((size_t)M * sizeof(K)));
+    uint32_t* sid = reinterpret_cast<uint32_t*>(take((size_t)M * 4));
+    uint32_t* tid = reinterpret_cast<uint32_t*>(take((size_t)M * 4));
+    uint32_t* mid = reinterpret_cast<uint32_t*>(take((size_t)M * 4));
+    int64_t* states = reinterpret_cast<int64_t*>(take((size_t)(R.ntiles + 1) * p * 8));
+    {
+      LaunchScope ls(KC_PARTITION, s);
+      k5_samples<K><<<(unsigned)((M + 255) / 256), 256, 0, s>>>(R, skey, sid);
+      // ceil(log2 p) levels of pairwise merges of the sample runs (ties to
+      // the lower run), ping-ponging so the last lands in (mkey, mid); the
+      // unmerged samples (skey) stay for the rank searches of k5_bounds
+      K5Level L{};
+      L.q = p;
+      for (int j = 0; j <= p; ++j) L.ro[j] = R.soff[j];
+      int levels = 0;
+      while ((1 << levels) < p) ++levels;
+      const K* ck = skey;
+      const uint32_t* cv = sid;
+      for (int lv = 0; lv < levels; ++lv) {
+        const bool to_m = (levels - 1 - lv) % 2 == 0;  // the last level writes (mkey, mid)
+        K* nk = to_m ? mkey : tkey;
+        uint32_t* nv = to_m ? mid : tid;
+        const int npair = (L.q + 1) / 2;
+        int64_t ch = 0;
+        for (int m = 0; m < npair; ++m) {
+          L.c0[m] = ch;
+          const int64_t len = L.ro[std::min(2 * m + 2, L.q)] - L.ro[2 * m];
+          ch += (len + kK5LvlQ - 1) / kK5LvlQ;
+        }
+        L.c0[npair] = ch;
+        if (ch > 0)
+          k5_sample_level<K><<<(unsigned)ch, kK5LvlNT, 0, s>>>(L, ck, cv, nk, nv);
+        K5Level N{};
+        N.q = npair;
+        for (int m = 0; m <= N.q; ++m) N.ro[m] = L.ro[std::min(2 * m, L.q)];
+        L = N;
+        ck = nk, cv = nv;
+      }
+      const int64_t nb = (R.ntiles + 1) * p;
+      k5_bounds<K><<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(R, skey, ck, cv, states);
+    }
+    MSORT_CUDA_TRY(cudaGetLastError());
+    {
+      LaunchScope ls(KC_KWAY, s);
+      const int P2 = P2of(p);
+      const unsigned T = (unsigned)R.ntiles;
+      if (P2 <= 2) k5_merge<K, K5NT, K5VT, K5MINB, 2><<<T, K5NT, k5_smem, s>>>(R, states, dst);
+      else if (P2 == 4) k5_merge<K, K5NT, K5VT, K5MINB, 4><<<T, K5NT, k5_smem, s>>>(R, states, dst);
+      else if (P2 == 8) k5_merge<K, K5NT, K5VT, K5MINB, 8><<<T, K5NT, k5_smem, s>>>(R, states, dst);
+      else k5_merge<K, K5NT, K5VT, K5MINB, 16><<<T, K5NT, k5_smem, s>>>(R, states, dst);
+    }
+    MSORT_CUDA_TRY(cudaGetLastError());
+#ifdef MSORT_K3_CHECK
+    {
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return cuda_fail(e, "k5 (debug sync)");
+    }
+#endif
+    return MSORT_SUCCESS;
+  }
+  static msort_status k5_init(int dev) {
+    static std::atomic<bool> done[64];
+    if (done[dev & 63].load(std::memory_order_acquire)) return MSORT_SUCCESS;
+    MSORT_CUDA_TRY(cudaFuncSetAttribute(k5_merge<K, K5NT, K5VT, K5MINB, 2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)k5_smem));
+    MSORT_CUDA_TRY(cudaFuncSetAttribute(k5_merge<K, K5NT, K5VT, K5MINB, 4>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)k5_smem));
+    MSORT_CUDA_TRY(cudaFuncSetAttribute(k5_merge<K, K5NT, K5VT, K5MINB, 8>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)k5_smem));
+    MSORT_CUDA_TRY(cudaFuncSetAttribute(k5_merge<K, K5NT, K5VT, K5MINB, 16>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)k5_smem));
+    done[dev & 63].store(true, std::memory_order_release);
+    return MSORT_SUCCESS;
+  }
+
   // Merge `runs` consecutive runs src[off[r], off[r+1]) into dst with rounds of
   // pairwise merges (ties to the lower run: merge() left-first at every
   // round keeps the lower run on the left).
   static msort_status kway(K* src_k, uint32_t* src_v, K* tmp_k, uint32_t* tmp_v, K* dst_k,
                            uint32_t* dst_v, const int64_t* off_in, int runs,
-                           unsigned long long* ctr, cudaStream_t s) {
+                           unsigned long long* ctr, cudaStream_t s,
+                           KernelClass kc = KC_KWAY) {
     MSORT_TRY(init());
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
@@ -1165,7 +1315,7 @@ struct Kernels {
       if (tiles > 0) {
         src.ch = chunk_tiles(tiles, dev);
         src.grab = src.ch < kChunk ? 1 : kGrab;
-        MSORT_TRY(launch_k3(src, (tiles + src.ch - 1) / src.ch, ctr + round, s, KC_KWAY));
+        MSORT_TRY(launch_k3(src, (tiles + src.ch - 1) / src.ch, ctr + round, s, kc));
       }
       int nr = pm.npairs;
       for (int m = 0; m <= nr; ++m) off[m] = off[std::min(2 * m, runs)];
@@ -1268,6 +1418,110 @@ msort_status pull_round_dispatch(const PullRuns& pr, void* out_k, void* out_v, i
     case MSORT_UINT32: return pull_k<uint32_t>(pr, out_k, out_v, off_out, ctr, s);
     case MSORT_INT64: return pull_k<int64_t>(pr, out_k, out_v, off_out, ctr, s);
     case MSORT_UINT64: return pull_k<uint64_t>(pr, out_k, out_v, off_out, ctr, s);
+    default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
+  }
+}
+
+template <class K>
+static msort_status kway5_k(const PullRuns& pr, void* dst, void* scratch, size_t bytes,
+                            cudaStream_t s) {
+  K5Runs R{};
+  R.p = pr.runs;
+  for (int j = 0; j < pr.runs; ++j) R.k[j] = pr.k[j], R.n[j] = pr.n[j];
+  return Kernels<K, false>::kway5(R, (K*)dst, (char*)scratch, bytes, s);
+}
+
+msort_status kway5_dispatch(const PullRuns& pr, void* dst, msort_dtype kd, void* scratch,
+                            size_t scratch_bytes, cudaStream_t s) {
+  if (pr.runs < 2 || pr.runs > kK5MaxRuns) {
+    set_error("k5: run count out of range");
+    return MSORT_ERROR_NOT_SUPPORTED;
+  }
+  switch (kd) {
+    case MSORT_INT32: return kway5_k<int32_t>(pr, dst, scratch, scratch_bytes, s);
+    case MSORT_UINT32: return kway5_k<uint32_t>(pr, dst, scratch, scratch_bytes, s);
+    case MSORT_INT64: return kway5_k<int64_t>(pr, dst, scratch, scratch_bytes, s);
+    case MSORT_UINT64: return kway5_k<uint64_t>(pr, dst, scratch, scratch_bytes, s);
+    default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
+  }
+}
+
+template <class K>
+static size_t kway5_bytes_k(const PullRuns& pr) {
+  K5Runs R{};
+  R.p = pr.runs;
+  for (int j = 0; j < pr.runs; ++j) R.n[j] = pr.n[j];
+  return Kernels<K, false>::k5_plan(R);
+}
+
+size_t kway5_scratch_bytes(const PullRuns& pr, msort_dtype kd) {
+  // SIZE_MAX: K5 not applicable (run count) or disabled (MSORT_K5=0)
+  if (pr.runs < 2 || pr.runs > Kernels<int32_t, false>::k5_max_runs()) return SIZE_MAX;
+  return dtype_size(kd) == 4 ? kway5_bytes_k<int32_t>(pr) : kway5_bytes_k<int64_t>(pr);
+}
+
+// msort_merge_runs (include/msort.h): stable merge of p sorted runs of
+// in_keys (run j = [off[j], off[j+1])), ties to the lower run, into keys_out.
+// Keys only with 3..16 runs: one K5 pass; otherwise rounds of K3.
+template <class K>
+static size_t merge_runs_ws_k(size_t n, int p, bool pairs) {
+  // K3 rounds: one ping-pong buffer (+ payloads) and the scheduler counters
+  size_t b = align_up(n * sizeof(K), 256) + (pairs ? align_up(n * 4, 256) : 0) +
+             align_up(kMaxLaunches * 8, 256);
+  if (!pairs && p >= 3 && p <= kK5MaxRuns) {  // (any run count K5 may be asked for)
+    // K5: the partition's sample arrays for the worst split of n over p runs
+    K5Runs R{};
+    R.p = p;
+    for (int j = 0; j < p; ++j) R.n[j] = (int64_t)(n / p) + 1;
+    size_t k5 = Kernels<K, false>::k5_plan(R);
+    b = std::max(b, k5 + 4096);
+  }
+  return b;
+}
+
+size_t merge_runs_ws_bytes(size_t n, int p, msort_dtype kd, msort_dtype vd) {
+  const bool pairs = vd != MSORT_NONE;
+  return dtype_size(kd) == 4 ? merge_runs_ws_k<int32_t>(n, p, pairs)
+                             : merge_runs_ws_k<int64_t>(n, p, pairs);
+}
+
+template <class K>
+static msort_status merge_runs_k(const void* ik, const void* iv, const int64_t* off, int p,
+                                 void* ok, void* ov, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int64_t n = off[p] - off[0];
+  if (!iv && p >= 3 && p <= Kernels<K, false>::k5_max_runs()) {
+    K5Runs R{};
+    R.p = p;
+    for (int j = 0; j < p; ++j)
+      R.k[j] = (const K*)ik + (off[j] - off[0]), R.n[j] = off[j + 1] - off[j];
+    K5Runs Q = R;
+    if (Kernels<K, false>::k5_plan(Q) <= ws_bytes)
+      return Kernels<K, false>::kway5(R, (K*)ok, (char*)ws, ws_bytes, s);
+  }
+  char* w = (char*)ws;
+  K* tk = (K*)w;
+  w += align_up((size_t)n * sizeof(K), 256);
+  uint32_t* tv = nullptr;
+  if (iv) {
+    tv = (uint32_t*)w;
+    w += align_up((size_t)n * 4, 256);
+  }
+  auto* ctr = reinterpret_cast<unsigned long long*>(w);
+  if (iv)
+    return Kernels<K, true>::kway((K*)ik, (uint32_t*)iv, tk, tv, (K*)ok, (uint32_t*)ov, off, p,
+                                  ctr, s);
+  return Kernels<K, false>::kway((K*)ik, nullptr, tk, nullptr, (K*)ok, nullptr, off, p, ctr, s);
+}
+
+msort_status merge_runs_dispatch(const void* ik, const void* iv, const int64_t* off, int p,
+                                 void* ok, void* ov, msort_dtype kd, msort_dtype vd, void* ws,
+                                 size_t ws_bytes, cudaStream_t s) {
+  if (vd == MSORT_NONE) iv = nullptr, ov = nullptr;
+  switch (kd) {
+    case MSORT_INT32: return merge_runs_k<int32_t>(ik, iv, off, p, ok, ov, ws, ws_bytes, s);
+    case MSORT_UINT32: return merge_runs_k<uint32_t>(ik, iv, off, p, ok, ov, ws, ws_bytes, s);
+    case MSORT_INT64: return merge_runs_k<int64_t>(ik, iv, off, p, ok, ov, ws, ws_bytes, s);
+    case MSORT_UINT64: return merge_runs_k<uint64_t>(ik, iv, off, p, ok, ov, ws, ws_bytes, s);
     default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
   }
 }
