@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU (default 2^28)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config lines (C1-C4, BASELINE.json configs 1-4)")
     ap.add_argument("--no-batched", action="store_true",
                     help="skip the batched (segmented) sort lines (SURVEY §8(f) f3)")
     ap.add_argument("--e2e-streams", type=int, default=3, help="streams the e2e steps rotate over")
@@ -310,6 +312,126 @@ def batched_bench(ms, mi, dev, reps=10):
                         "offsets on the device; msort_sort_segmented", "results": out}
 
 
+def config_digest(name):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "config_digests.json")) as f:
+            return json.load(f)["configs"].get(name)
+    except Exception:
+        return None
+
+
+def configs_bench(ms, mi, dev, peak, reps=20):
+    """BASELINE.json's single-GPU configs beside the headline:
+    C1 (2^16 int32), C2 (2^24 int32), C3 (2^26 int64 in [0,1000) + uint32
+    index payload), C4 (2^27 uint32 + uint32 index payload).  Per config:
+    median device ms of `reps` out-of-place sorts from the pristine input
+    (CUDA events around each call; an untimed L2 flush before each for C1/C2,
+    whose data fit in L2; C3/C4 are larger than L2), keys/s, the merge
+    kernel's roofline (levels x 2 n (wk + wv) bytes per launch over its live
+    event time, against the measured HBM peak) and the step's (every executed
+    pass at HBM rate), and the output checked BIT FOR BIT against the
+    oracle's SHA-256 digests (tests/golden/config_digests.json).  C1 also
+    reports the device time of a CUDA-graph replay of the call."""
+    import numpy as np
+    import torch
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = {}
+    for name in ("C1", "C2", "C3", "C4"):
+        c = mi.CONFIGS[name]
+        n, pairs = c["n"], c["pairs"]
+        k = mi.keys_torch(n, c["seed"], c["dist"], device=dev)
+        if c["dist"] == "u32":
+            k = k.view(torch.uint32)
+        kin = k
+        vin = torch.arange(n, dtype=torch.int32, device=dev).view(torch.uint32) if pairs else None
+        kout = torch.empty_like(kin)
+        vout = torch.empty_like(vin) if pairs else None
+        wk = kin.element_size()
+        wv = 4 if pairs else 0
+        ws = ms.workspace(n, torch.int64 if wk == 8 else torch.int32, pairs, device=dev)
+
+        def call():
+            ms.msort_sort_out(kin, kout, in_vals=vin, vals_out=vout, ws=ws)
+
+        for _ in range(3):
+            call()
+        torch.cuda.synchronize()
+        ts = []
+        ms.profile_reset()
+        ms.profile_enable(True)
+        for _ in range(reps):
+            if n * (wk + wv) < (64 << 20):
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            call()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms.profile_enable(False)
+        prof = ms.profile_read()
+        ts.sort()
+        med = ts[len(ts) // 2]
+        kd = {4: ms.MSORT_INT32, 8: ms.MSORT_INT64}[wk]
+        T = ms.tile_size(kd, ms.MSORT_UINT32 if pairs else ms.MSORT_NONE)
+        levels = ((n + T - 1) // T - 1).bit_length()
+        per_pass = 2 * n * (wk + wv)
+        mp_l, mp_ms = prof["merge_pass"]
+        roof = None
+        if mp_l:
+            ach = levels * per_pass / (mp_ms / mp_l / 1e3) / 1e9
+            roof = {"kernel": "k3_merge_pass", "bound": "hbm", "achieved": round(ach, 1),
+                    "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                    "avg_launch_ms": round(mp_ms / mp_l, 4), "merge_levels": levels}
+        t_roof = (levels + 1) * per_pass / (peak * 1e9) * 1e3
+        exp = config_digest(name)
+        ok = None
+        if exp:
+            a = kout.view(torch.int64 if wk == 8 else torch.int32).cpu().numpy()
+            ok = host_digest(a) == exp["keys_sha256"]
+            if pairs:
+                ok &= host_digest(vout.view(torch.int32).cpu().numpy()) == exp["vals_sha256"]
+        d = {"n": n, "key": str(kin.dtype).replace("torch.", ""), "payload": "uint32 index" if pairs
+             else None, "ms": round(med, 4), "min_ms": round(ts[0], 4),
+             "keys_per_s": n / (med / 1e3), "tile": T, "merge_levels": levels,
+             "phases_ms": {k2: round(v[1] / reps, 4) for k2, v in prof.items() if v[0]},
+             "roofline": roof,
+             "step_roofline": {"passes": levels + 1, "t_roof_ms": round(t_roof, 4),
+                               "frac": round(t_roof / med, 4),
+                               "floor_frac": round(per_pass / (peak * 1e9) * 1e3 / med, 4)},
+             "l2_flush": n * (wk + wv) < (64 << 20), "verified": ok}
+        if name == "C1":
+            s = torch.cuda.Stream(device=dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                ms.msort_sort_out(kin, kout, ws=ws, stream=s)
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=s):
+                    ms.msort_sort_out(kin, kout, ws=ws, stream=s)
+            for _ in range(5):
+                g.replay()
+            torch.cuda.synchronize()
+            gt = []
+            for _ in range(reps):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.replay()
+                e1.record()
+                e1.synchronize()
+                gt.append(e0.elapsed_time(e1))
+            gt.sort()
+            d["graph_replay_ms"] = round(gt[len(gt) // 2], 4)
+            d["graph_replay_verified"] = host_digest(kout.cpu().numpy()) == exp["keys_sha256"] \
+                if exp else None
+        out[name] = d
+        del k, kin, vin, kout, vout, ws
+        torch.cuda.empty_cache()
+    return {"workload": "BASELINE.json configs 1-4 (msort_inputs.CONFIGS), one GPU, "
+                        "out of place from the pristine input", "results": out}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -442,8 +564,14 @@ def main():
     # whole-step roofline: bytes of every executed pass at HBM rate (+ NVLink)
     step_bytes = (passes + 1) * alg_bytes
     t_roof = step_bytes / (peak * 1e9)
+    d4_passes = 0
     if world > 1:
-        t_roof += n * wk * (world - 1) / world / 770e9 + alg_bytes * 3 / (peak * 1e9)
+        # D4 as executed: one K5 pass for keys with 3..8 ranks (in pull mode
+        # it also carries the exchange), one K3 round at p = 2, else
+        # ceil(log2 p) K3 rounds; plus the exchange over NVLink
+        d4_passes = 1 if world <= 8 else (world - 1).bit_length()
+        step_bytes += d4_passes * alg_bytes
+        t_roof += n * wk * (world - 1) / world / 770e9 + d4_passes * alg_bytes / (peak * 1e9)
 
     clocks = sampler.summary(t0, t1)
 
@@ -579,6 +707,9 @@ def main():
     batched = None
     if rank == 0 and world == 1 and not args.no_batched:
         batched = batched_bench(ms, mi, dev)
+    per_config = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        per_config = configs_bench(ms, mi, dev, peak)
 
     cpu = cpu_mp = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -604,6 +735,7 @@ def main():
             "roofline": roof,
             "exchange_roofline": xroof,
             "step_roofline": {"bytes_per_gpu": step_bytes, "t_roof_ms": t_roof * 1e3,
+                              "hbm_passes": passes + 1 + d4_passes,
                               "frac": round(t_roof * 1e3 / ms_step, 4),
                               "floor_frac": round(2 * n * wk / (peak * 1e9) * 1e3 / ms_step, 4)},
             "phases": phases,
@@ -611,6 +743,7 @@ def main():
             "cpu_paper_mp": cpu_mp,
             "e2e": e2e,
             "batched_sort": batched,
+            "configs": per_config,
             "gpu_launches": launches,
             "clocks": clocks,
             "verified": ok,

@@ -324,6 +324,22 @@ def test_c5_digest_sums_match_generator():
         assert sum(x["sum"] for x in d[str(p)]) == sum(sums[:p]), p
 
 
+def test_config_digests_match_survey():
+    """tests/golden/config_digests.json (make_config_digests.py: oracle only):
+    first / last sorted key (and payload) of C1-C4 equal the survey's
+    independent numpy values (SURVEY.md §8(c) golden values)."""
+    with open(os.path.join(GOLDEN, "config_digests.json")) as f:
+        g = json.load(f)["configs"]
+    for name, exp in SURVEY.items():
+        d = g[name]
+        assert d["n"] == mi.CONFIGS[name]["n"], name
+        assert d["first"] == exp["sorted_at"][0] and d["last"] == exp["sorted_at"][-1], name
+        if "payload_at" in exp:
+            assert d["vals_first"] == exp["payload_at"][0], name
+            assert d["vals_last"] == exp["payload_at"][-1], name
+        assert len(d["keys_sha256"]) == 64
+
+
 def test_oracle_live_c1_matches_survey(orc):
     k, _ = mi.config_input("C1")
     s = orc.sort(k)
