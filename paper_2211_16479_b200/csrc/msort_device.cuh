@@ -530,6 +530,51 @@ __device__ __forceinline__ void keys_network(K (&x)[N]) {
   InsertAll<P, N, K>::run(x);
 }
 
+// Warp-shuffle bitonic sorting network, keys only (the north_star's
+// "warp-shuffle sorting networks"): the warp's 32 * VW keys, VW per lane,
+// end sorted in BLOCKED order (lane l holds ranks [l VW, (l + 1) VW)).
+// Batcher's bitonic network over i = lane * VW + k: for each block size, the
+// half-cleaner strides j; element i and its partner i ^ j are put in
+// ascending order when (i & size) == 0, descending otherwise.  Strides below
+// VW pair registers of one lane (compare-exchange in registers); larger
+// strides pair the same register of lanes lane ^ (j / VW), exchanged by
+// __shfl_xor_sync -- no shared memory, no bank conflicts.  Keys only: equal
+// keys are indistinguishable, so the (unstable) network gives the sort.
+template <int VW, class K>
+__device__ __forceinline__ void warp_bitonic_keys(K (&key)[VW], int lane) {
+  static_assert((VW & (VW - 1)) == 0, "VW: power of two");
+  constexpr int N = 32 * VW;
+#pragma unroll
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      if (j < VW) {
+#pragma unroll
+        for (int k = 0; k < VW; ++k) {
+          const int p = k ^ j;
+          if (p > k) {
+            const bool up = ((lane * VW + k) & size) == 0;
+            const K lo = key[k] < key[p] ? key[k] : key[p];
+            const K hi = key[k] < key[p] ? key[p] : key[k];
+            key[k] = up ? lo : hi;
+            key[p] = up ? hi : lo;
+          }
+        }
+      } else {
+        const int lm = j / VW;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int k = 0; k < VW; ++k) {
+          const K o = __shfl_xor_sync(0xffffffffu, key[k], lm);
+          const bool up = ((lane * VW + k) & size) == 0;
+          const bool keep_small = up == lower;  // lower lane of an ascending pair: the min
+          key[k] = keep_small ? (o < key[k] ? o : key[k]) : (o < key[k] ? key[k] : o);
+        }
+      }
+    }
+  }
+}
+
 // Odd-even transposition sort: swaps only adjacent elements and only when
 // strictly greater, so it is stable -- used when a payload index travels.
 template <int N, class K>

@@ -221,6 +221,7 @@ __device__ __forceinline__ void store_vec(K* dst, const K (&key)[VT]) {
 }  // namespace msort
 #include "k6_quad.cuh"
 #include "k5_kway.cuh"
+#include "k0_small.cuh"
 namespace msort {
 
 // Compare-exchange of the keys-only register network (min and max; any
@@ -372,6 +373,11 @@ __global__ void __launch_bounds__(NT)
 // ----------------------------------------------------------------- K3
 // k3_merge.cuh: the persistent merge pass with fused co-rank search (K2).
 
+#ifdef MSORT_K0_TRACE
+extern "C" int msort_debug_k0_trace(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_k0_trace, sizeof(unsigned long long) * 8 * 16);
+}
+#endif
 #ifdef MSORT_K3_TRACE
 extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, g_k3_trace, sizeof(unsigned long long) * n);
@@ -679,6 +685,10 @@ struct Kernels {
       }
       return MSORT_SUCCESS;
     }
+    if constexpr (!PAIRS) {
+      // small keys-only sorts: the whole sort in one cluster launch (K0)
+      if ((int64_t)n <= kK0MaxN && k0_enabled()) return small_sort(in_k, keys, (int64_t)n, s);
+    }
     const int64_t ntiles = (int64_t)((n + T - 1) / T);
     int passes = 0;
     while ((int64_t(1) << passes) < ntiles) ++passes;
@@ -827,6 +837,52 @@ struct Kernels {
     f.ch = chunk_tiles(f.ntiles, dev);
     f.grab = f.ch < kChunk ? 1 : kGrab;  // small sorts: one chunk per CTA at a time
     return launch_k3(f, (int64_t)left * ((f.ntiles + f.ch - 1) / f.ch), ctr, s, KC_MERGE);
+  }
+
+  // ---- K0: n <= kK0MaxN keys in one launch (k0_small.cuh) -------------
+  // MSORT_K0 (environment): 0 disables K0, 2 selects its A/B variant
+  // without the warp-shuffle network
+  static int k0_mode() {
+    const char* e = getenv("MSORT_K0");
+    return e && *e ? atoi(e) : 1;
+  }
+  static bool k0_enabled() { return k0_mode() != 0; }
+  template <bool SHFL>
+  static msort_status k0_attr(int dev, size_t smem) {
+    static std::atomic<bool> done[64];
+    if (!done[dev & 63].load(std::memory_order_acquire)) {
+      MSORT_CUDA_TRY(cudaFuncSetAttribute(k0_small_sort<K, SHFL>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      done[dev & 63].store(true, std::memory_order_release);
+    }
+    return MSORT_SUCCESS;
+  }
+  static msort_status small_sort(const K* in, K* out, int64_t n, cudaStream_t s) {
+    int dev = 0;
+    MSORT_CUDA_TRY(cudaGetDevice(&dev));
+    constexpr size_t smem = 3 * (size_t)k0_padded<K>() * sizeof(K);
+    const bool shfl = k0_mode() != 2;
+    MSORT_TRY(shfl ? k0_attr<true>(dev, smem) : k0_attr<false>(dev, smem));
+    int CL = 1;
+    while ((int64_t)CL * kK0Chunk < n) CL *= 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)CL, 1, 1);
+    cfg.blockDim = dim3(kK0NT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = CL > 1 ? 1 : 0;
+    {
+      LaunchScope ls(KC_TILE_SORT, s);
+      if (shfl) MSORT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k0_small_sort<K, true>, in, out, n, CL));
+      else MSORT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k0_small_sort<K, false>, in, out, n, CL));
+    }
+    return MSORT_SUCCESS;
   }
 
   // Batched sort of independent segments [off[i], off[i+1]) of keys/vals, in

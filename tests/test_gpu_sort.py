@@ -246,3 +246,47 @@ def test_random_sizes_stress(ms, orc):
         k = _keys(n, 5000 + t, dist, dtype)
         v = mi.index_payload(n) if pairs else None
         check_parity(ms, orc, k, v)
+
+
+# ---- K0: keys-only sorts of n <= 69632 in one cluster launch
+K0_SIZES = [2, 3, 31, 100, 1000, 4097, 8191, 8192, 8193, 12000, 16384, 16385, 30001, 32768,
+            32769, 50000, 65535, 65536, 65537, 69632]
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.uint32, np.int64, np.uint64])
+def test_small_cluster_sort_sizes(ms, orc, dtype):
+    """Every cluster size (1, 2, 4, 8 CTAs), ragged chunks, the K0 / general
+    path boundary (65536 / 65537), against the oracle."""
+    for i, n in enumerate(K0_SIZES):
+        for dist in ("rand", "dup"):
+            check_parity(ms, orc, _keys(n, 900 + i, dist, dtype), None)
+
+
+@pytest.mark.parametrize("dist", ["eq", "asc", "desc", "ext"])
+def test_small_cluster_sort_structured(ms, orc, dist):
+    for dtype in (np.int32, np.uint64):
+        for n in (8704, 20000, 65536):
+            check_parity(ms, orc, _keys(n, 7, dist, dtype), None)
+
+
+def test_small_cluster_sort_c1_out_of_place_and_graph(ms, orc):
+    """C1 (2^16 int32, seed 0) out of place, then captured in a CUDA graph and
+    replayed on new data: bit-exact every time."""
+    k, _ = mi.config_input("C1")
+    kin = to_dev(k)
+    kout = torch.empty_like(kin)
+    ws = ms.workspace(k.size, torch.int32, False, device="cuda")
+    ms.msort_sort_out(kin, kout, ws=ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(kout, np.int32), orc.sort(k))
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            ms.msort_sort_out(kin, kout, ws=ws, stream=s)
+    for seed in (11, 12):
+        k2 = mi.keys(k.size, seed, "i32")
+        kin.copy_(to_dev(k2))
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(kout, np.int32), orc.sort(k2))
