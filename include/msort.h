@@ -391,6 +391,15 @@ int msort_debug_set_quad(int mode);
  * local buffers); environment MSORT_EXCHANGE=pull selects it too.  Returns 0. */
 int msort_debug_set_exchange(int mode);
 
+/* Experiment hook (scripts/k1_ab.py; not part of the product path): the tile
+ * sort (K1) alone on int32 keys -- every T-key tile of in[0, n) sorted into
+ * out (device pointers) by the product kernel (variant 0: 128 threads x 68
+ * keys, a per-thread merge-exchange network + merge-path rounds, T = 8704) or
+ * its A/B variant (1: 128 x 64, the warp-shuffle bitonic network for the
+ * first 2048-key runs, then the same block rounds, T = 8192).  Asynchronous
+ * on `stream`; returns T, or -1 on a launch error. */
+int msort_debug_tile_sort(const void *in, void *out, int64_t n, int variant, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

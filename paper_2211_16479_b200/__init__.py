@@ -45,7 +45,7 @@ EXPORTED = (
     "msort_segmented_workspace_bytes", "msort_sort_segmented",
     "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
     "msort_plan_tree_rounds", "msort_plan_tree_role", "msort_comm_wrap",
-    "msort_merge_runs", "msort_merge_runs_workspace_bytes",
+    "msort_merge_runs", "msort_merge_runs_workspace_bytes", "msort_debug_tile_sort",
 )
 
 
@@ -106,6 +106,8 @@ def _load():
     L.msort_plan_tree_role.restype = i32
     L.msort_merge_runs_workspace_bytes.argtypes = [sz, i32, i32, i32, c.POINTER(c.c_size_t)]
     L.msort_merge_runs.argtypes = [vp, vp, i64p, i32, vp, vp, i32, i32, vp, sz, vp]
+    L.msort_debug_tile_sort.argtypes = [vp, vp, c.c_int64, i32, vp]
+    L.msort_debug_tile_sort.restype = i32
     L.msort_tile_size.argtypes = [i32, i32]
     L.msort_tile_size.restype = i32
     for f in ("msort_sort", "msort_sort_pairs", "msort_workspace_bytes", "msort_sort_ws",

@@ -540,39 +540,48 @@ __device__ __forceinline__ void keys_network(K (&x)[N]) {
 // strides pair the same register of lanes lane ^ (j / VW), exchanged by
 // __shfl_xor_sync -- no shared memory, no bank conflicts.  Keys only: equal
 // keys are indistinguishable, so the (unstable) network gives the sort.
+// One stage (block size SIZE, stride J) of the network; the stages are
+// instantiated one by one (template recursion) so that every register index
+// is a compile-time constant at any VW.
+template <int VW, int SIZE, int J>
+struct WarpBitonicStage {
+  template <class K>
+  static __device__ __forceinline__ void run(K (&key)[VW], int lane) {
+    if constexpr (J < VW) {
+#pragma unroll
+      for (int k = 0; k < VW; ++k) {
+        if ((k & J) == 0) {
+          const int p = k | J;
+          const bool up = ((lane * VW + k) & SIZE) == 0;
+          const K lo = key[k] < key[p] ? key[k] : key[p];
+          const K hi = key[k] < key[p] ? key[p] : key[k];
+          key[k] = up ? lo : hi;
+          key[p] = up ? hi : lo;
+        }
+      }
+    } else {
+      constexpr int lm = J / VW;
+      const bool lower = (lane & lm) == 0;
+#pragma unroll
+      for (int k = 0; k < VW; ++k) {
+        const K o = __shfl_xor_sync(0xffffffffu, key[k], lm);
+        const bool up = ((lane * VW + k) & SIZE) == 0;
+        const bool keep_small = up == lower;  // lower lane of an ascending pair: the min
+        key[k] = keep_small ? (o < key[k] ? o : key[k]) : (o < key[k] ? key[k] : o);
+      }
+    }
+    if constexpr (J > 1) {
+      WarpBitonicStage<VW, SIZE, J / 2>::run(key, lane);
+    } else if constexpr (SIZE < 32 * VW) {
+      WarpBitonicStage<VW, SIZE * 2, SIZE>::run(key, lane);
+    }
+  }
+};
+
 template <int VW, class K>
 __device__ __forceinline__ void warp_bitonic_keys(K (&key)[VW], int lane) {
   static_assert((VW & (VW - 1)) == 0, "VW: power of two");
-  constexpr int N = 32 * VW;
-#pragma unroll
-  for (int size = 2; size <= N; size <<= 1) {
-#pragma unroll
-    for (int j = size >> 1; j > 0; j >>= 1) {
-      if (j < VW) {
-#pragma unroll
-        for (int k = 0; k < VW; ++k) {
-          const int p = k ^ j;
-          if (p > k) {
-            const bool up = ((lane * VW + k) & size) == 0;
-            const K lo = key[k] < key[p] ? key[k] : key[p];
-            const K hi = key[k] < key[p] ? key[p] : key[k];
-            key[k] = up ? lo : hi;
-            key[p] = up ? hi : lo;
-          }
-        }
-      } else {
-        const int lm = j / VW;
-        const bool lower = (lane & lm) == 0;
-#pragma unroll
-        for (int k = 0; k < VW; ++k) {
-          const K o = __shfl_xor_sync(0xffffffffu, key[k], lm);
-          const bool up = ((lane * VW + k) & size) == 0;
-          const bool keep_small = up == lower;  // lower lane of an ascending pair: the min
-          key[k] = keep_small ? (o < key[k] ? o : key[k]) : (o < key[k] ? key[k] : o);
-        }
-      }
-    }
-  }
+  WarpBitonicStage<VW, 2, 1>::run(key, lane);
 }
 
 // Odd-even transposition sort: swaps only adjacent elements and only when

@@ -292,7 +292,12 @@ struct K1KeysShape {
   static_assert((NT & (NT - 1)) == 0 && NT >= 32, "NT: power of two >= 32");
 };
 
-template <class K, int NT, int VT>
+// SHFL (the A/B variant of SURVEY §8(a) S1 / north_star (1), VT a power of
+// two): each warp sorts its 32 x VT keys with the warp-shuffle bitonic
+// network (warp_bitonic_keys, no shared memory) instead of the per-thread
+// network + the five in-warp merge rounds; the block rounds then start from
+// runs of 32 VT.
+template <class K, int NT, int VT, bool SHFL = false>
 __global__ void __launch_bounds__(NT)
     k1_tile_sort_keys(const K* __restrict__ in_k, K* __restrict__ out_k, int64_t n,
                       const int64_t* __restrict__ seg) {
@@ -318,10 +323,16 @@ __global__ void __launch_bounds__(NT)
     const int i = k * NT + tid;
     key[k] = i < cnt ? in_k[base + i] : KeyTraits<K>::max_key();
   }
-  k1_network<VT>(key);
+  int r0 = 0;
+  if constexpr (SHFL) {
+    warp_bitonic_keys<VT>(key, tid & 31);  // the warp's 32 VT keys, blocked
+    r0 = 5;
+  } else {
+    k1_network<VT>(key);
+  }
 
 #pragma unroll 1
-  for (int r = 0; r < SH::ROUNDS; ++r) {
+  for (int r = r0; r < SH::ROUNDS; ++r) {
     const int w = VT << r;
     const bool in_warp = (2 << r) <= 32;
     // region origin of this round's pairs (vectors)
@@ -372,6 +383,46 @@ __global__ void __launch_bounds__(NT)
 
 // ----------------------------------------------------------------- K3
 // k3_merge.cuh: the persistent merge pass with fused co-rank search (K2).
+
+// A/B hook of the tile sort alone (scripts/k1_ab.py): sorts every tile of
+// in[0, n) (int32) into out with the product K1 (variant 0: 128 x 68, T =
+// 8704) or the warp-shuffle variant (1: 128 x 64, T = 8192).  Returns the
+// tile size, or -1 on a launch error.  Not part of the product path.
+extern "C" int msort_debug_tile_sort(const void* in, void* out, int64_t n, int variant,
+                                     void* stream) {
+  using namespace msort;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (variant == 0) {
+    using SH = K1KeysShape<int32_t, 128, 68>;
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k1_tile_sort_keys<int32_t, 128, 68, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::smem);
+      init = true;
+    }
+    const int64_t nt = (n + SH::T - 1) / SH::T;
+    {
+      LaunchScope ls(KC_TILE_SORT, s);
+      k1_tile_sort_keys<int32_t, 128, 68, false><<<(unsigned)nt, 128, SH::smem, s>>>(
+          (const int32_t*)in, (int32_t*)out, n, nullptr);
+    }
+    return cudaGetLastError() == cudaSuccess ? SH::T : -1;
+  }
+  using SH = K1KeysShape<int32_t, 128, 64>;
+  static bool init1 = false;
+  if (!init1) {
+    cudaFuncSetAttribute(k1_tile_sort_keys<int32_t, 128, 64, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::smem);
+    init1 = true;
+  }
+  const int64_t nt = (n + SH::T - 1) / SH::T;
+  {
+    LaunchScope ls(KC_TILE_SORT, s);
+    k1_tile_sort_keys<int32_t, 128, 64, true><<<(unsigned)nt, 128, SH::smem, s>>>(
+        (const int32_t*)in, (int32_t*)out, n, nullptr);
+  }
+  return cudaGetLastError() == cudaSuccess ? SH::T : -1;
+}
 
 #ifdef MSORT_K0_TRACE
 extern "C" int msort_debug_k0_trace(unsigned long long* host) {
