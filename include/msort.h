@@ -215,6 +215,20 @@ msort_status msort_comm_wrap(void *nccl_comm, msort_comm_t *out);
  * or msort_comm_wrap (frees only the wrapper). */
 msort_status msort_comm_destroy(msort_comm_t comm);
 
+/* Reserve the pull exchange (msort_debug_set_exchange(1)) for calls with up to
+ * n_max local elements of these dtypes: the communicator allocates its
+ * exchange buffer (cudaMalloc), publishes it through CUDA IPC and opens every
+ * peer's, once.  Collective (every rank calls it; synchronises `stream`).
+ * Afterwards a pull-mode msort_sort_distributed* call on keys with 3..8 ranks
+ * runs WITHOUT any host synchronisation: the splitters (D2) stay on the
+ * device, one K5 launch planned on the device from the split matrix reads
+ * every rank's segment in place over NVLink (D3 + D4), and only a
+ * split_matrix_out request makes the call wait.  A call with n_local above
+ * the reservation returns MSORT_ERROR_INVALID_VALUE (before any collective:
+ * every rank must respect its reservation, as for matching NCCL counts). */
+msort_status msort_comm_reserve(msort_comm_t comm, size_t n_max, msort_dtype key_dtype,
+                                msort_dtype val_dtype, msort_stream_t stream);
+
 /* Distributed stable sort (re-designed: local sort, exact
  * splitters by co-rank, one variable all-to-all over NVLink, local k-way
  * merge).  Collective: every rank calls it with the same dtypes; n_local may
@@ -224,7 +238,9 @@ msort_status msort_comm_destroy(msort_comm_t comm);
  * vals: NULL (val_dtype MSORT_NONE) or 4-byte payloads.
  * split_matrix_out: NULL or host (world+1)*world int64: entry (r, j) = number
  * of rank j's elements among the first K_r outputs.
- * Synchronises `stream` once (the exchange sizes are needed on the host).
+ * Synchronises `stream` once (the exchange sizes are needed on the host) --
+ * except in the reserved pull mode (msort_comm_reserve), which does not
+ * synchronise unless split_matrix_out is requested.
  * Failure detection: that wait polls the stream and ncclCommGetAsyncError
  * instead of blocking; an NCCL error -- or, with the environment variable
  * MSORT_NCCL_TIMEOUT_S set, a wait longer than that many seconds (a dead or

@@ -46,6 +46,7 @@ EXPORTED = (
     "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
     "msort_plan_tree_rounds", "msort_plan_tree_role", "msort_comm_wrap",
     "msort_merge_runs", "msort_merge_runs_workspace_bytes", "msort_debug_tile_sort",
+    "msort_comm_reserve",
 )
 
 
@@ -74,6 +75,7 @@ def _load():
     L.msort_comm_init.argtypes = [vp, i32, i32, c.POINTER(vp)]
     L.msort_comm_destroy.argtypes = [vp]
     L.msort_comm_wrap.argtypes = [vp, c.POINTER(vp)]
+    L.msort_comm_reserve.argtypes = [vp, sz, i32, i32, vp]
     L.msort_sort_distributed.argtypes = [vp, vp, sz, i32, i32, vp, vp, i64p]
     L.msort_sort_distributed_ws.argtypes = [vp, vp, sz, i32, i32, vp, vp, sz, vp, i64p]
     L.msort_sort_distributed_emulated.argtypes = [c.POINTER(vp), c.POINTER(vp),
@@ -118,7 +120,8 @@ def _load():
               "msort_plan_narrow", "msort_plan_fill", "msort_profile_read",
               "msort_segmented_workspace_bytes", "msort_sort_segmented",
               "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
-              "msort_comm_wrap", "msort_merge_runs", "msort_merge_runs_workspace_bytes"):
+              "msort_comm_wrap", "msort_merge_runs", "msort_merge_runs_workspace_bytes",
+              "msort_comm_reserve"):
         getattr(L, f).restype = i32
     return L
 
@@ -434,6 +437,14 @@ class Comm:
         _check(lib.msort_comm_init(idb, self.rank, self.world, ctypes.byref(h)), "msort_comm_init")
         self.handle = h
 
+    def reserve(self, n_max: int, keys_dtype=torch.int32, with_vals: bool = False, stream=None):
+        """Collective: reserve the pull exchange for up to n_max local keys
+        (include/msort.h msort_comm_reserve); afterwards pull-mode sorts of
+        keys with 3..8 ranks run without host synchronisation."""
+        _check(lib.msort_comm_reserve(self.handle, int(n_max), _TORCH_DT[keys_dtype],
+                                      MSORT_UINT32 if with_vals else MSORT_NONE,
+                                      ctypes.c_void_p(_stream(stream))), "msort_comm_reserve")
+
     def close(self):
         if self.handle:
             _check(lib.msort_comm_destroy(self.handle), "msort_comm_destroy")
@@ -475,14 +486,16 @@ def msort_sort_distributed(keys: torch.Tensor, comm: Comm, vals: torch.Tensor | 
     kd, vd = _dt(keys), _vdt(vals)
     if ws is None:
         ws = workspace(n, keys.dtype, vals is not None, world=comm.world, device=keys.device)
-    split = np.zeros((comm.world + 1) * comm.world, dtype=np.int64)
+    # the split matrix only when asked for: fetching it is a host synchronisation
+    split = np.zeros((comm.world + 1) * comm.world, dtype=np.int64) if return_split else None
+    sp = split.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)) if return_split else None
     with _on(keys.device):
         _check(lib.msort_sort_distributed_ws(
             _ptr(keys), _ptr(vals), n, kd, vd, comm.handle, _ptr(ws), ws.numel(),
-            ctypes.c_void_p(_stream(stream)),
-            split.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "msort_sort_distributed_ws")
-    split = split.reshape(comm.world + 1, comm.world)
-    return (keys, vals, split) if return_split else (keys, vals)
+            ctypes.c_void_p(_stream(stream)), sp), "msort_sort_distributed_ws")
+    if return_split:
+        return keys, vals, split.reshape(comm.world + 1, comm.world)
+    return keys, vals
 
 
 def msort_sort_distributed_out(in_keys: torch.Tensor, keys_out: torch.Tensor, comm: Comm,
@@ -507,15 +520,16 @@ def msort_sort_distributed_out(in_keys: torch.Tensor, keys_out: torch.Tensor, co
     if ws is None:
         ws = workspace(n, in_keys.dtype, in_vals is not None, world=comm.world,
                        device=in_keys.device)
-    split = np.zeros((comm.world + 1) * comm.world, dtype=np.int64)
+    split = np.zeros((comm.world + 1) * comm.world, dtype=np.int64) if return_split else None
+    sp = split.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)) if return_split else None
     with _on(in_keys.device):
         _check(lib.msort_sort_distributed_out_ws(
             _ptr(in_keys), _ptr(in_vals), _ptr(keys_out), _ptr(vals_out), n, kd, vd, comm.handle,
-            _ptr(ws), ws.numel(), ctypes.c_void_p(_stream(stream)),
-            split.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+            _ptr(ws), ws.numel(), ctypes.c_void_p(_stream(stream)), sp),
             "msort_sort_distributed_out_ws")
-    split = split.reshape(comm.world + 1, comm.world)
-    return (keys_out, vals_out, split) if return_split else (keys_out, vals_out)
+    if return_split:
+        return keys_out, vals_out, split.reshape(comm.world + 1, comm.world)
+    return keys_out, vals_out
 
 
 def msort_sort_distributed_emulated(keys: list, vals: list | None = None, stream=None):

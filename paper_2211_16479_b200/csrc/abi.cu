@@ -27,6 +27,8 @@ msort_status comm_unique_id(void* out);
 msort_status comm_init(const void* idp, int rank, int world, msort_comm_s** out);
 msort_status comm_destroy(msort_comm_s* c);
 msort_status comm_wrap(void* nccl_comm, msort_comm_s** out);
+msort_status comm_reserve(msort_comm_s* c, size_t n_max, msort_dtype kd, msort_dtype vd,
+                          cudaStream_t s);
 int comm_world(msort_comm_s* c);
 
 // ---------------------------------------------------------------- errors
@@ -501,6 +503,17 @@ msort_status msort_comm_wrap(void* nccl_comm, msort_comm_t* out) {
 }
 
 msort_status msort_comm_destroy(msort_comm_t comm) { return comm_destroy(comm); }
+
+msort_status msort_comm_reserve(msort_comm_t comm, size_t n_max, msort_dtype key_dtype,
+                                msort_dtype val_dtype, msort_stream_t stream) {
+  if (!comm || !dtype_size(key_dtype) ||
+      (val_dtype != MSORT_NONE && val_dtype != MSORT_UINT32 && val_dtype != MSORT_INT32)) {
+    set_error("bad argument to msort_comm_reserve");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  MSORT_TRY(check_device());
+  return comm_reserve(comm, n_max, key_dtype, val_dtype, (cudaStream_t)stream);
+}
 
 msort_status msort_sort_distributed_ws(void* keys, void* vals, size_t n_local,
                                        msort_dtype key_dtype, msort_dtype val_dtype,

@@ -58,6 +58,11 @@ struct K5Runs {
   int64_t ntiles;                 // T (tile t = [state t, state t+1))
 };
 
+// The kernels take the geometry by value (host-planned) or as a pointer into
+// device memory (planned on the device by k5_plan_dev: no host round trip).
+__device__ __forceinline__ const K5Runs& k5r(const K5Runs& r) { return r; }
+__device__ __forceinline__ const K5Runs& k5r(const K5Runs* r) { return *r; }
+
 // Shape of the merge CTA: NT threads x VT keys per thread and round;
 // capacity C = (NT - P2 / 2) * VT keys for P2 (p rounded up to a power of
 // two) runs, so that a round's ceil(len / VT) threads per pair fit in NT.
@@ -95,10 +100,11 @@ __device__ __forceinline__ int k5_run_of(const K5Runs& R, int64_t x) {
 
 // skey[x] = the sample's key, sid[x] = x (its id: run and index follow from
 // soff).
-template <class K>
+template <class K, class RS>
 __global__ void __launch_bounds__(256)
-    k5_samples(const __grid_constant__ K5Runs R, K* __restrict__ skey,
+    k5_samples(const __grid_constant__ RS Rin, K* __restrict__ skey,
                uint32_t* __restrict__ sid) {
+  const K5Runs& R = k5r(Rin);
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= R.soff[R.p]) return;
   const int k = k5_run_of(R, x);
@@ -118,6 +124,8 @@ struct K5Level {
   int64_t ro[kK5MaxRuns + 1];       // their offsets
   int64_t c0[kK5MaxRuns / 2 + 2];   // first chunk of each pair (prefix)
 };
+__device__ __forceinline__ const K5Level& k5l(const K5Level& l) { return l; }
+__device__ __forceinline__ const K5Level& k5l(const K5Level* l) { return *l; }
 
 template <class K>
 __device__ __forceinline__ int64_t k5_corank_warp(const K* __restrict__ A, int64_t na,
@@ -144,17 +152,19 @@ __device__ __forceinline__ int64_t k5_corank_warp(const K* __restrict__ A, int64
   return lo;
 }
 
-template <class K>
+template <class K, class LS>
 __global__ void __launch_bounds__(kK5LvlNT)
-    k5_sample_level(const __grid_constant__ K5Level L, const K* __restrict__ ik,
+    k5_sample_level(const __grid_constant__ LS Lin, const K* __restrict__ ik,
                     const uint32_t* __restrict__ iv, K* __restrict__ ok,
                     uint32_t* __restrict__ ov) {
+  const K5Level& L = k5l(Lin);
   constexpr int Q = kK5LvlQ, VT = kK5LvlVT;
   __shared__ K sk[Q + 2];
   __shared__ uint32_t sv[Q + 2];
   __shared__ int64_t s_co[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int npair = (L.q + 1) / 2;
+  if ((int64_t)blockIdx.x >= L.c0[npair]) return;  // upper-bound grid (device-planned)
   int m = 0;
   while (m + 1 < npair && L.c0[m + 1] <= (int64_t)blockIdx.x) ++m;
   const int64_t a0 = L.ro[2 * m], a1 = L.ro[min(2 * m + 1, L.q)];
@@ -208,11 +218,12 @@ __global__ void __launch_bounds__(kK5LvlNT)
 // number of run j's samples before x, by a search in its sample array), the
 // sample at (r - 1) S precedes x and the one at r S does not, so
 // c_j in [(r - 1) S + 1, r S]  (c_j = 0 when r = 0).
-template <class K>
+template <class K, class RS>
 __global__ void __launch_bounds__(256)
-    k5_bounds(const __grid_constant__ K5Runs R, const K* __restrict__ skey,
+    k5_bounds(const __grid_constant__ RS Rin, const K* __restrict__ skey,
               const K* __restrict__ mkey, const uint32_t* __restrict__ mid,
               int64_t* __restrict__ states) {
+  const K5Runs& R = k5r(Rin);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int p = R.p;
   if (i >= (R.ntiles + 1) * p) return;
@@ -242,6 +253,58 @@ __global__ void __launch_bounds__(256)
   states[i] = c;
 }
 
+// ------------------------------------------------------- device planning
+// The geometry of one K5 merge planned on the device (one thread), so the
+// distributed pull path needs no host round trip: rank `me`'s runs are the
+// segments [S[me][j], S[me+1][j]) of every rank j's sorted shard (the split
+// matrix S, (p+1) x p int64, on the device), at bases[j] (device table of the
+// ranks' shard pointers, possibly peer memory).  Fills the K5Runs (the
+// sample stride S and fill g come from the host: they depend on p only) and
+// the sample-merge levels; the kernels are launched with upper-bound grids.
+constexpr int kK5MaxLevels = 4;
+struct K5Geo {
+  K5Runs R;
+  K5Level L[kK5MaxLevels];
+  int levels;
+};
+__global__ void k5_plan_dev(K5Geo* __restrict__ G, const int64_t* __restrict__ split, int me,
+                            int p, const void* const* __restrict__ bases, int wk, int64_t S,
+                            int64_t g) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  K5Runs& R = G->R;
+  R.p = p, R.S = S, R.g = g;
+  R.soff[0] = 0;
+  for (int j = 0; j < p; ++j) {
+    const int64_t a = split[(int64_t)me * p + j], b = split[(int64_t)(me + 1) * p + j];
+    R.k[j] = static_cast<const char*>(bases[j]) + a * wk;
+    R.n[j] = b - a;
+    R.soff[j + 1] = R.soff[j] + (R.n[j] + S - 1) / S;
+  }
+  const int64_t M = R.soff[p];
+  R.ntiles = M == 0 ? 0 : max((int64_t)1, (M + g - 1) / g);
+  K5Level L{};
+  L.q = p;
+  for (int j = 0; j <= p; ++j) L.ro[j] = R.soff[j];
+  int levels = 0;
+  while ((1 << levels) < p) ++levels;
+  G->levels = levels;
+  for (int lv = 0; lv < levels && lv < kK5MaxLevels; ++lv) {
+    const int npair = (L.q + 1) / 2;
+    int64_t ch = 0;
+    for (int m = 0; m < npair; ++m) {
+      L.c0[m] = ch;
+      const int64_t len = L.ro[min(2 * m + 2, L.q)] - L.ro[2 * m];
+      ch += (len + kK5LvlQ - 1) / kK5LvlQ;
+    }
+    L.c0[npair] = ch;
+    G->L[lv] = L;
+    K5Level N{};
+    N.q = npair;
+    for (int m = 0; m <= N.q; ++m) N.ro[m] = L.ro[min(2 * m, L.q)];
+    L = N;
+  }
+}
+
 // ---------------------------------------------------------------- merge
 // One CTA per tile; P2 = p rounded up to a power of two (runs p..P2-1 are
 // empty), R = log2(P2) rounds.  The whole round structure is laid out once
@@ -251,10 +314,12 @@ __global__ void __launch_bounds__(256)
 // [MIN | B | MAX .. MIN | A | MAX] (B below A: merge_keys_dual clamps A at
 // its MAX and B at its MIN sentinel with one bound each); its threads are
 // [tp[r][m], tp[r][m+1]), one per VT outputs.
-template <class K, int NT, int VT, int MINB, int P2>
+template <class K, int NT, int VT, int MINB, int P2, class RS>
 __global__ void __launch_bounds__(NT, MINB)
-    k5_merge(const __grid_constant__ K5Runs R, const int64_t* __restrict__ states,
+    k5_merge(const __grid_constant__ RS Rin, const int64_t* __restrict__ states,
              K* __restrict__ dst) {
+  const K5Runs& R = k5r(Rin);
+  if ((int64_t)blockIdx.x >= R.ntiles) return;  // upper-bound grid (device-planned)
   constexpr int RR = __builtin_ctz(P2);  // rounds
   constexpr uint32_t Z = sizeof(K);
   extern __shared__ __align__(16) unsigned char smem[];

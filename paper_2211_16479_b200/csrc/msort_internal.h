@@ -101,6 +101,14 @@ constexpr int kK5Runs = 16;
 msort_status kway5_dispatch(const PullRuns& pr, void* dst, msort_dtype kd, void* scratch,
                             size_t scratch_bytes, cudaStream_t s);
 size_t kway5_scratch_bytes(const PullRuns& pr, msort_dtype kd);
+// The same merge planned on the device (k5_plan_dev): rank `me` of p merges
+// its segments [S[me][j], S[me+1][j]) of every rank j's sorted shard (split
+// matrix `split` and shard table `bases` in device memory) into dst (n_out
+// keys).  No host synchronisation.  scratch >= kway5_dev_bytes(n_out, p, kd).
+size_t kway5_dev_bytes(int64_t n_out, int p, msort_dtype kd);
+msort_status kway5_dev_dispatch(const int64_t* split, int me, int p, const void* const* bases,
+                                void* dst, int64_t n_out, msort_dtype kd, void* scratch,
+                                size_t scratch_bytes, cudaStream_t s);
 
 // msort_merge_runs: workspace bytes and the call (sort_single.cu).
 size_t merge_runs_ws_bytes(size_t n, int p, msort_dtype kd, msort_dtype vd);

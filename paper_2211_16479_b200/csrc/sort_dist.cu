@@ -53,6 +53,14 @@ struct msort_comm_s {
   // (its IPC handle, opened once by each peer, stays valid between calls)
   void* xbuf = nullptr;
   size_t xbuf_bytes = 0;
+  // msort_comm_reserve: the exchange buffer holds up to reserved_n local keys
+  // (+ payloads) on every rank, its IPC mappings are open, and dbases (device
+  // table of the p ranks' shard pointers) lets the pull path plan K5 on the
+  // device -- no host synchronisation per call
+  size_t reserved_n = 0;
+  size_t reserved_wk = 0;
+  bool reserved_vals = false;
+  const void** dbases = nullptr;
 };
 
 namespace msort {
@@ -380,6 +388,14 @@ struct NcclColl {
     return MSORT_SUCCESS;
   }
   int rank_of(int local) const { return c->rank + local; }
+  // Sync-free pull (after msort_comm_reserve): the device table of the
+  // ranks' shard pointers, or nullptr when the communicator is not reserved
+  // for this call's size (the host-planned pull path runs instead).
+  const void* const* reserved_bases(RankIO* io, msort_dtype kd, bool pairs) {
+    if (!c->dbases || pairs || io[0].n > c->reserved_n || dtype_size(kd) > c->reserved_wk)
+      return nullptr;
+    return c->dbases;
+  }
   msort_status wait(const char* what) { return wait_stream_nccl(c, s, what); }
   // device -> host copy of `bytes` through the pinned staging, then the wait
   msort_status fetch(void* host, const void* dev, size_t bytes, const char* what) {
@@ -516,6 +532,20 @@ struct EmulColl {
     return MSORT_SUCCESS;
   }
   int rank_of(int local) const { return local; }
+  // The emulation always takes the device-planned pull path (so it is the one
+  // the tests exercise): the shard table is uploaded into rank 0's
+  // workspace (its IPC record area, unused in the emulation).
+  std::vector<const void*> tab;
+  const void* const* reserved_bases(RankIO* io, msort_dtype, bool pairs) {
+    if (pairs) return nullptr;
+    tab.assign(p, nullptr);
+    for (int j = 0; j < p; ++j) tab[j] = io[j].sk;
+    auto* d = reinterpret_cast<const void**>(io[0].ws.ipc_all);
+    if (cudaMemcpyAsync(d, tab.data(), sizeof(void*) * p, cudaMemcpyHostToDevice, s) !=
+        cudaSuccess)
+      return nullptr;
+    return d;
+  }
   msort_status wait(const char* what) {
     cudaError_t e = cudaStreamSynchronize(s);
     return e == cudaSuccess ? MSORT_SUCCESS : cuda_fail(e, what);
@@ -611,6 +641,29 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
   MSORT_CUDA_TRY(cudaGetLastError());
   // The one host synchronisation: the exchange sizes are needed on the host.
   const bool pull = pull_mode;
+  const size_t wk0 = dtype_size(kd);
+  if (pull && vd == MSORT_NONE && p >= 3 && p <= kK5Runs &&
+      kway5_scratch_bytes(PullRuns{p, {}, {}, {}}, kd) != SIZE_MAX) {
+    // D3 + D4 as ONE K5 launch planned on the device from the split matrix
+    // (sync-free once the shard pointers are known on the device: the
+    // emulation always, NCCL after msort_comm_reserve)
+    const void* const* bases = C.reserved_bases(io, kd, false);
+    bool fits = bases != nullptr;
+    for (int l = 0; l < nloc && fits; ++l)
+      fits = kway5_dev_bytes((int64_t)io[l].n, p, kd) <= io[l].ws.sort_ws_bytes;
+    if (fits) {
+      for (int l = 0; l < nloc; ++l)
+        MSORT_TRY(kway5_dev_dispatch(io[l].ws.split, C.rank_of(l), p, bases, io[l].keys,
+                                     (int64_t)io[l].n, kd, io[l].ws.sort_ws,
+                                     io[l].ws.sort_ws_bytes, s));
+      // every rank has read the others' segments: exchange buffers are free
+      MSORT_TRY(C.barrier(io));
+      if (split_out)  // the only host synchronisation, and only when asked for
+        MSORT_TRY(C.fetch(split_out, io[0].ws.split, S.size() * 8, "split matrix"));
+      return MSORT_SUCCESS;
+    }
+  }
+  (void)wk0;
   std::vector<unsigned char> ipc_host(pull ? kIpcBytes * (size_t)p : 0);
   if (pull) MSORT_TRY(C.ipc_publish(io, ipc_host.data()));
   MSORT_TRY(C.fetch(S.data(), io[0].ws.split, S.size() * 8, "split matrix"));
@@ -735,6 +788,12 @@ msort_status dist_nccl(const void* in_keys, const void* in_vals, void* keys, voi
     // the sorted shard goes to the communicator's IPC-exportable buffer
     const size_t kb = align_up(n * dtype_size(kd), 256);
     const size_t need = std::max<size_t>(kb + (pv ? align_up(n * 4, 256) : 0), 256);
+    if (comm->dbases && (n > comm->reserved_n || dtype_size(kd) > comm->reserved_wk ||
+                         (pv && !comm->reserved_vals))) {
+      // the peers hold mappings of the reserved buffer: it cannot move
+      set_error("pull exchange: n_local exceeds the msort_comm_reserve reservation");
+      return MSORT_ERROR_INVALID_VALUE;
+    }
     if (need > comm->xbuf_bytes) {
       // the previous call ended with a barrier after every peer's reads, so
       // the old buffer is free; wait for this stream's earlier work too
@@ -749,6 +808,56 @@ msort_status dist_nccl(const void* in_keys, const void* in_vals, void* keys, voi
   }
   NcclColl C{comm, s};
   return dist_run(C, &io, 1, kd, vd, s, split_out, pull);
+}
+
+// msort_comm_reserve: allocate the pull exchange buffer for up to n_max local
+// keys (+ 4-byte payloads), publish it through CUDA IPC, open every peer's,
+// and keep the table of the p shard pointers on the device.  Collective.
+msort_status comm_reserve(msort_comm_s* c, size_t n_max, msort_dtype kd, msort_dtype vd,
+                          cudaStream_t s) {
+  if (c->aborted) {
+    set_error("communicator was aborted after an earlier failure");
+    return MSORT_ERROR_NCCL;
+  }
+  const int p = c->world;
+  const bool pv = vd != MSORT_NONE;
+  const size_t kb = align_up(n_max * dtype_size(kd), 256);
+  const size_t need = std::max<size_t>(kb + (pv ? align_up(n_max * 4, 256) : 0), 256);
+  if (need > c->xbuf_bytes) {
+    MSORT_CUDA_TRY(cudaStreamSynchronize(s));
+    if (c->xbuf) cudaFree(c->xbuf);
+    c->xbuf = nullptr, c->xbuf_bytes = 0;
+    MSORT_CUDA_TRY(cudaMalloc(&c->xbuf, need));
+    c->xbuf_bytes = need;
+  }
+  // device scratch for the IPC record gather
+  unsigned char* rec = nullptr;
+  MSORT_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&rec), kIpcBytes * (size_t)(p + 1), s));
+  struct Free {
+    unsigned char* q;
+    cudaStream_t s;
+    ~Free() { cudaFreeAsync(q, s); }
+  } fr{rec, s};
+  RankIO io{};
+  io.sk = c->xbuf;
+  io.sv = pv ? static_cast<char*>(c->xbuf) + kb : nullptr;
+  io.ws.ipc_send = rec;
+  io.ws.ipc_all = rec + kIpcBytes;
+  NcclColl C{c, s};
+  std::vector<unsigned char> host(kIpcBytes * (size_t)p);
+  MSORT_TRY(C.ipc_publish(&io, host.data()));
+  std::vector<const void*> bk;
+  std::vector<const uint32_t*> bv;
+  MSORT_TRY(C.peer_bases(&io, host.data(), pv, bk, bv));
+  if (!c->dbases)
+    MSORT_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->dbases), sizeof(void*) * p));
+  memcpy(c->pinned, bk.data(), sizeof(void*) * p);
+  MSORT_CUDA_TRY(cudaMemcpyAsync(c->dbases, c->pinned, sizeof(void*) * p, cudaMemcpyHostToDevice, s));
+  MSORT_TRY(wait_stream_nccl(c, s, "reserve"));
+  c->reserved_n = n_max;
+  c->reserved_wk = dtype_size(kd);
+  c->reserved_vals = pv;
+  return MSORT_SUCCESS;
 }
 
 msort_status dist_emulated(void* const* keys, void* const* vals, const size_t* n, int world,
@@ -1085,6 +1194,7 @@ msort_status comm_destroy(msort_comm_s* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->dscratch) cudaFree(c->dscratch);
   if (c->xbuf) cudaFree(c->xbuf);
+  if (c->dbases) cudaFree(c->dbases);
   delete c;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
   return MSORT_SUCCESS;

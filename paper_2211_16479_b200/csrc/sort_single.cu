@@ -1277,36 +1277,17 @@ struct Kernels {
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
     MSORT_TRY(k5_init(dev));
-    char* w = scratch;
-    auto take = [&](size_t b) {
-      char* q = w;
-      w += align_up(b, 256);
-      return q;
-    };
-    K* skey = reinterpret_cast<K*>(take((size_t)M * sizeof(K)));
-    K* tkey = reinterpret_cast<K*>(take((size_t)M * sizeof(K)));
-    K* mkey = reinterpret_cast<K*>(take((size_t)M * sizeof(K)));
-    uint32_t* sid = reinterpret_cast<uint32_t*>(take((size_t)M * 4));
-    uint32_t* tid = reinterpret_cast<uint32_t*>(take((size_t)M * 4));
-    uint32_t* mid = reinterpret_cast<uint32_t*>(take((size_t)M * 4));
-    int64_t* states = reinterpret_cast<int64_t*>(take((size_t)(R.ntiles + 1) * p * 8));
+    const K5Bufs B = k5_carve(scratch, M, R.ntiles, p);
+    // the sample-merge levels, planned here
+    K5Level lv[kK5MaxLevels];
+    int64_t lch[kK5MaxLevels];
+    int levels = 0;
     {
-      LaunchScope ls(KC_PARTITION, s);
-      k5_samples<K><<<(unsigned)((M + 255) / 256), 256, 0, s>>>(R, skey, sid);
-      // ceil(log2 p) levels of pairwise merges of the sample runs (ties to
-      // the lower run), ping-ponging so the last lands in (mkey, mid); the
-      // unmerged samples (skey) stay for the rank searches of k5_bounds
       K5Level L{};
       L.q = p;
       for (int j = 0; j <= p; ++j) L.ro[j] = R.soff[j];
-      int levels = 0;
       while ((1 << levels) < p) ++levels;
-      const K* ck = skey;
-      const uint32_t* cv = sid;
-      for (int lv = 0; lv < levels; ++lv) {
-        const bool to_m = (levels - 1 - lv) % 2 == 0;  // the last level writes (mkey, mid)
-        K* nk = to_m ? mkey : tkey;
-        uint32_t* nv = to_m ? mid : tid;
+      for (int l = 0; l < levels; ++l) {
         const int npair = (L.q + 1) / 2;
         int64_t ch = 0;
         for (int m = 0; m < npair; ++m) {
@@ -1315,26 +1296,74 @@ struct Kernels {
           ch += (len + kK5LvlQ - 1) / kK5LvlQ;
         }
         L.c0[npair] = ch;
-        if (ch > 0)
-          k5_sample_level<K><<<(unsigned)ch, kK5LvlNT, 0, s>>>(L, ck, cv, nk, nv);
+        lv[l] = L, lch[l] = ch;
         K5Level N{};
         N.q = npair;
         for (int m = 0; m <= N.q; ++m) N.ro[m] = L.ro[std::min(2 * m, L.q)];
         L = N;
+      }
+    }
+    return k5_launch(R, lv, lch, levels, p, M, R.ntiles, B, dst, s);
+  }
+
+  // Scratch of one K5 merge for M samples and T tiles (k5_plan's layout).
+  struct K5Bufs {
+    K *skey, *tkey, *mkey;
+    uint32_t *sid, *tid, *mid;
+    int64_t* states;
+  };
+  static K5Bufs k5_carve(char* w, int64_t M, int64_t T, int p) {
+    auto take = [&](size_t b) {
+      char* q = w;
+      w += align_up(b, 256);
+      return q;
+    };
+    K5Bufs B;
+    B.skey = reinterpret_cast<K*>(take((size_t)M * sizeof(K)));
+    B.tkey = reinterpret_cast<K*>(take((size_t)M * sizeof(K)));
+    B.mkey = reinterpret_cast<K*>(take((size_t)M * sizeof(K)));
+    B.sid = reinterpret_cast<uint32_t*>(take((size_t)M * 4));
+    B.tid = reinterpret_cast<uint32_t*>(take((size_t)M * 4));
+    B.mid = reinterpret_cast<uint32_t*>(take((size_t)M * 4));
+    B.states = reinterpret_cast<int64_t*>(take((size_t)(T + 1) * p * 8));
+    return B;
+  }
+
+  // The K5 launches for a geometry given by value (RS = K5Runs, LS =
+  // K5Level) or by device pointers (const K5Runs*, const K5Level*); Mgrid /
+  // Tgrid / lch are the exact counts or, device-planned, upper bounds.
+  template <class RS, class LS>
+  static msort_status k5_launch(const RS& R, const LS* lv, const int64_t* lch, int levels, int p,
+                                int64_t Mgrid, int64_t Tgrid, const K5Bufs& B, K* dst,
+                                cudaStream_t s) {
+    {
+      LaunchScope ls(KC_PARTITION, s);
+      k5_samples<K, RS><<<(unsigned)((Mgrid + 255) / 256), 256, 0, s>>>(R, B.skey, B.sid);
+      // ceil(log2 p) levels of pairwise merges of the sample runs (ties to
+      // the lower run), ping-ponging so the last lands in (mkey, mid); the
+      // unmerged samples (skey) stay for the rank searches of k5_bounds
+      const K* ck = B.skey;
+      const uint32_t* cv = B.sid;
+      for (int l = 0; l < levels; ++l) {
+        const bool to_m = (levels - 1 - l) % 2 == 0;  // the last level writes (mkey, mid)
+        K* nk = to_m ? B.mkey : B.tkey;
+        uint32_t* nv = to_m ? B.mid : B.tid;
+        if (lch[l] > 0)
+          k5_sample_level<K, LS><<<(unsigned)lch[l], kK5LvlNT, 0, s>>>(lv[l], ck, cv, nk, nv);
         ck = nk, cv = nv;
       }
-      const int64_t nb = (R.ntiles + 1) * p;
-      k5_bounds<K><<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(R, skey, ck, cv, states);
+      const int64_t nb = (Tgrid + 1) * p;
+      k5_bounds<K, RS><<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(R, B.skey, ck, cv, B.states);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
-    {
+    if (Tgrid > 0) {
       LaunchScope ls(KC_KWAY, s);
       const int P2 = P2of(p);
-      const unsigned T = (unsigned)R.ntiles;
-      if (P2 <= 2) k5_merge<K, K5NT, K5VT, K5MINB, 2><<<T, K5NT, k5_smem, s>>>(R, states, dst);
-      else if (P2 == 4) k5_merge<K, K5NT, K5VT, K5MINB, 4><<<T, K5NT, k5_smem, s>>>(R, states, dst);
-      else if (P2 == 8) k5_merge<K, K5NT, K5VT, K5MINB, 8><<<T, K5NT, k5_smem, s>>>(R, states, dst);
-      else k5_merge<K, K5NT, K5VT, K5MINB, 16><<<T, K5NT, k5_smem, s>>>(R, states, dst);
+      const unsigned T = (unsigned)Tgrid;
+      if (P2 <= 2) k5_merge<K, K5NT, K5VT, K5MINB, 2, RS><<<T, K5NT, k5_smem, s>>>(R, B.states, dst);
+      else if (P2 == 4) k5_merge<K, K5NT, K5VT, K5MINB, 4, RS><<<T, K5NT, k5_smem, s>>>(R, B.states, dst);
+      else if (P2 == 8) k5_merge<K, K5NT, K5VT, K5MINB, 8, RS><<<T, K5NT, k5_smem, s>>>(R, B.states, dst);
+      else k5_merge<K, K5NT, K5VT, K5MINB, 16, RS><<<T, K5NT, k5_smem, s>>>(R, B.states, dst);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
 #ifdef MSORT_K3_CHECK
@@ -1345,21 +1374,79 @@ struct Kernels {
 #endif
     return MSORT_SUCCESS;
   }
+
+  // K5 planned on the device (k5_plan_dev): rank `me` of p merges its
+  // segments of every rank's sorted shard (split matrix `split` and shard
+  // table `bases`, both device memory) into dst, n_out keys in all.  No host
+  // synchronisation: the grids are upper bounds from n_out.  scratch: >=
+  // k5_dev_bytes(n_out, p).
+  static void k5_dev_geometry(int64_t n_out, int p, int64_t& S, int64_t& g, int64_t& Mmax,
+                              int64_t& Tmax) {
+    const int64_t C = K5S::cap(P2of(p));
+    g = MSORT_K5_G * (int64_t)p;
+    S = std::max<int64_t>(1, (C + p) / (g + p));
+    Mmax = n_out / S + p;  // sum of ceil(n_j / S) <= n_out / S + p
+    Tmax = std::max<int64_t>(1, (Mmax + g - 1) / g);
+  }
+  static size_t k5_dev_bytes(int64_t n_out, int p) {
+    int64_t S, g, Mmax, Tmax;
+    k5_dev_geometry(n_out, p, S, g, Mmax, Tmax);
+    return 3 * align_up((size_t)Mmax * sizeof(K), 256) + 3 * align_up((size_t)Mmax * 4, 256) +
+           align_up((size_t)(Tmax + 1) * p * 8, 256) + align_up(sizeof(K5Geo), 256);
+  }
+  static msort_status kway5_dev(const int64_t* split, int me, int p, const void* const* bases,
+                                K* dst, int64_t n_out, char* scratch, size_t scratch_bytes,
+                                cudaStream_t s) {
+    if (p < 2 || p > kK5MaxRuns) {
+      set_error("k5: run count out of range");
+      return MSORT_ERROR_NOT_SUPPORTED;
+    }
+    if (k5_dev_bytes(n_out, p) > scratch_bytes) {
+      set_error("k5: scratch too small");
+      return MSORT_ERROR_INVALID_VALUE;
+    }
+    int64_t S, g, Mmax, Tmax;
+    k5_dev_geometry(n_out, p, S, g, Mmax, Tmax);
+    if (Mmax >= ((int64_t)1 << 32)) {
+      set_error("k5: too many samples");
+      return MSORT_ERROR_NOT_SUPPORTED;
+    }
+    int dev = 0;
+    MSORT_CUDA_TRY(cudaGetDevice(&dev));
+    MSORT_TRY(k5_init(dev));
+    const K5Bufs B = k5_carve(scratch, Mmax, Tmax, p);
+    K5Geo* G = reinterpret_cast<K5Geo*>(
+        scratch + 3 * align_up((size_t)Mmax * sizeof(K), 256) + 3 * align_up((size_t)Mmax * 4, 256) +
+        align_up((size_t)(Tmax + 1) * p * 8, 256));
+    {
+      LaunchScope ls(KC_PARTITION, s);
+      k5_plan_dev<<<1, 32, 0, s>>>(G, split, me, p, bases, (int)sizeof(K), S, g);
+    }
+    MSORT_CUDA_TRY(cudaGetLastError());
+    const K5Level* lv[kK5MaxLevels];
+    int64_t lch[kK5MaxLevels];
+    int levels = 0;
+    while ((1 << levels) < p) ++levels;
+    for (int l = 0; l < levels; ++l) lv[l] = &G->L[l], lch[l] = (Mmax + kK5LvlQ - 1) / kK5LvlQ + p;
+    const K5Runs* Rp = &G->R;
+    return k5_launch(Rp, lv, lch, levels, p, Mmax, Tmax, B, dst, s);
+  }
+  template <class RS>
+  static msort_status k5_attr() {
+    auto set = [](auto f) {
+      return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k5_smem);
+    };
+    MSORT_CUDA_TRY(set(k5_merge<K, K5NT, K5VT, K5MINB, 2, RS>));
+    MSORT_CUDA_TRY(set(k5_merge<K, K5NT, K5VT, K5MINB, 4, RS>));
+    MSORT_CUDA_TRY(set(k5_merge<K, K5NT, K5VT, K5MINB, 8, RS>));
+    MSORT_CUDA_TRY(set(k5_merge<K, K5NT, K5VT, K5MINB, 16, RS>));
+    return MSORT_SUCCESS;
+  }
   static msort_status k5_init(int dev) {
     static std::atomic<bool> done[64];
     if (done[dev & 63].load(std::memory_order_acquire)) return MSORT_SUCCESS;
-    MSORT_CUDA_TRY(cudaFuncSetAttribute(k5_merge<K, K5NT, K5VT, K5MINB, 2>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)k5_smem));
-    MSORT_CUDA_TRY(cudaFuncSetAttribute(k5_merge<K, K5NT, K5VT, K5MINB, 4>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)k5_smem));
-    MSORT_CUDA_TRY(cudaFuncSetAttribute(k5_merge<K, K5NT, K5VT, K5MINB, 8>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)k5_smem));
-    MSORT_CUDA_TRY(cudaFuncSetAttribute(k5_merge<K, K5NT, K5VT, K5MINB, 16>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)k5_smem));
+    MSORT_TRY(k5_attr<K5Runs>());
+    MSORT_TRY(k5_attr<const K5Runs*>());
     done[dev & 63].store(true, std::memory_order_release);
     return MSORT_SUCCESS;
   }
@@ -1549,6 +1636,27 @@ msort_status kway5_dispatch(const PullRuns& pr, void* dst, msort_dtype kd, void*
     case MSORT_UINT32: return kway5_k<uint32_t>(pr, dst, scratch, scratch_bytes, s);
     case MSORT_INT64: return kway5_k<int64_t>(pr, dst, scratch, scratch_bytes, s);
     case MSORT_UINT64: return kway5_k<uint64_t>(pr, dst, scratch, scratch_bytes, s);
+    default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
+  }
+}
+
+size_t kway5_dev_bytes(int64_t n_out, int p, msort_dtype kd) {
+  return dtype_size(kd) == 4 ? Kernels<int32_t, false>::k5_dev_bytes(n_out, p)
+                             : Kernels<int64_t, false>::k5_dev_bytes(n_out, p);
+}
+
+msort_status kway5_dev_dispatch(const int64_t* split, int me, int p, const void* const* bases,
+                                void* dst, int64_t n_out, msort_dtype kd, void* scratch,
+                                size_t scratch_bytes, cudaStream_t s) {
+  switch (kd) {
+#define K5D(T)                                                                                 \
+  return Kernels<T, false>::kway5_dev(split, me, p, bases, (T*)dst, n_out, (char*)scratch,    \
+                                      scratch_bytes, s)
+    case MSORT_INT32: K5D(int32_t);
+    case MSORT_UINT32: K5D(uint32_t);
+    case MSORT_INT64: K5D(int64_t);
+    case MSORT_UINT64: K5D(uint64_t);
+#undef K5D
     default: set_error("unknown key dtype"); return MSORT_ERROR_INVALID_VALUE;
   }
 }

@@ -106,6 +106,22 @@ def _worker(rank, p, port, outdir):
                 ms.set_exchange_mode(0)
 
         check_balanced(comm, "own-comm")
+        # the reserved pull exchange: no host synchronisation inside the call
+        # (keys, 3..8 ranks); output checked after a device sync
+        if p >= 3:
+            ks, _ = _shards(p, "equal")
+            cat = np.concatenate(ks)
+            ek = oracle.sort(cat)
+            comm.reserve(max(k.size for k in ks))
+            ms.set_exchange_mode(1)
+            for rep in range(3):
+                kd = torch.from_numpy(ks[rank].copy()).to(dev)
+                ms.msort_sort_distributed(kd, comm)
+                torch.cuda.synchronize()
+                a = rank * ks[0].size
+                if not np.array_equal(kd.cpu().numpy(), ek[a:a + ks[rank].size]):
+                    fail(f"reserved pull rep {rep}: keys differ from the oracle slice")
+            ms.set_exchange_mode(0)
         # the paper's rank tree (f4): rank 0 gathers everything
         for pairs in (False, True):
             ks, vs = _shards(p, "unequal")
