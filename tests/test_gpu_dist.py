@@ -188,6 +188,35 @@ def test_nccl_one_rank(ms, orc):
     comm.close()
 
 
+def test_nccl_one_rank_reserve_pull(ms, orc):
+    """msort_comm_reserve on the real NCCL communicator (one rank): the
+    exchange buffer is allocated and published through CUDA IPC, the device
+    shard table written; pull-mode sorts within the reservation are exact
+    (at one rank the call is the local sort; the multi-GPU test covers the
+    reserved K5 path)."""
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    comm = ms.Comm()
+    n = 70001
+    comm.reserve(n)
+    ms.set_exchange_mode(1)
+    try:
+        for seed in (1, 2):
+            k = mi.keys(n - seed, 80 + seed, "i32")
+            kd = _dev(k)
+            ms.msort_sort_distributed(kd, comm)
+            torch.cuda.synchronize()
+            assert np.array_equal(_host(kd, np.int32), orc.sort(k))
+    finally:
+        ms.set_exchange_mode(0)
+        comm.close()
+
+
 def test_nccl_wait_timeout_aborts(tmp_path):
     """Failure detection (include/msort.h): with MSORT_NCCL_TIMEOUT_S set, a
     distributed call whose stream does not drain in time (here: held up by a
