@@ -673,9 +673,7 @@ def main():
             d_in = torch.empty_like(kin)
 
             def e2e_step():
-                d_in.copy_(h_in, non_blocking=True)
-                ms.msort_sort_distributed_out(d_in, kout, comm, ws=ws, stream=stream)
-                h_out.copy_(kout, non_blocking=True)
+                ms.msort_sort_distributed_host(h_in, h_out, d_in, comm, ws=ws, stream=stream)
 
             e2e_step()
             barrier()
@@ -689,7 +687,8 @@ def main():
             te = f0.elapsed_time(f1)
             o = h_out.numpy()
             ok &= (host_digest(o) == exp) if exp else bool(np.all(o[1:] >= o[:-1]))
-            path = "pinned host -> cudaMemcpyAsync -> msort_sort_distributed_out_ws -> pinned host"
+            path = ("msort_sort_distributed_host (pinned host -> device -> distributed sort -> "
+                    "pinned host)")
         if world > 1:
             t = torch.tensor([te], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)

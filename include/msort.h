@@ -267,6 +267,22 @@ msort_status msort_sort_distributed_out_ws(const void *in_keys, const void *in_v
                                            msort_comm_t comm, void *ws, size_t ws_bytes,
                                            msort_stream_t stream, int64_t *split_matrix_out);
 
+/* End-to-end distributed sort of HOST arrays (bench.py's N > 1 e2e path):
+ * host_keys[0..n_local) (host_vals) are copied into the caller's device
+ * buffers dev_keys (dev_vals), sorted there by msort_sort_distributed_ws (same
+ * workspace, same collective contract), and this rank's output slice is
+ * copied back to host_keys_out (host_vals_out).  Enqueued on `stream`; with
+ * page-locked host buffers the copies are asynchronous -- synchronise the
+ * stream before reading host_keys_out (the sort itself synchronises once
+ * unless the communicator is reserved for the pull exchange).  Errors: as
+ * msort_sort_distributed_ws, plus INVALID_VALUE for NULL host pointers. */
+msort_status msort_sort_distributed_host(const void *host_keys, const void *host_vals,
+                                         void *host_keys_out, void *host_vals_out,
+                                         size_t n_local, msort_dtype key_dtype,
+                                         msort_dtype val_dtype, msort_comm_t comm,
+                                         void *dev_keys, void *dev_vals, void *ws,
+                                         size_t ws_bytes, msort_stream_t stream);
+
 /* Single-process emulation of the distributed sort for `world` virtual ranks
  * whose shards all live on the current device: the same kernels, the same
  * splitter planning and the same k-way merge, with the NCCL collectives

@@ -46,7 +46,7 @@ EXPORTED = (
     "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
     "msort_plan_tree_rounds", "msort_plan_tree_role", "msort_comm_wrap",
     "msort_merge_runs", "msort_merge_runs_workspace_bytes", "msort_debug_tile_sort",
-    "msort_comm_reserve",
+    "msort_comm_reserve", "msort_sort_distributed_host",
 )
 
 
@@ -76,6 +76,7 @@ def _load():
     L.msort_comm_destroy.argtypes = [vp]
     L.msort_comm_wrap.argtypes = [vp, c.POINTER(vp)]
     L.msort_comm_reserve.argtypes = [vp, sz, i32, i32, vp]
+    L.msort_sort_distributed_host.argtypes = [vp, vp, vp, vp, sz, i32, i32, vp, vp, vp, vp, sz, vp]
     L.msort_sort_distributed.argtypes = [vp, vp, sz, i32, i32, vp, vp, i64p]
     L.msort_sort_distributed_ws.argtypes = [vp, vp, sz, i32, i32, vp, vp, sz, vp, i64p]
     L.msort_sort_distributed_emulated.argtypes = [c.POINTER(vp), c.POINTER(vp),
@@ -121,7 +122,7 @@ def _load():
               "msort_segmented_workspace_bytes", "msort_sort_segmented",
               "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
               "msort_comm_wrap", "msort_merge_runs", "msort_merge_runs_workspace_bytes",
-              "msort_comm_reserve"):
+              "msort_comm_reserve", "msort_sort_distributed_host"):
         getattr(L, f).restype = i32
     return L
 
@@ -496,6 +497,32 @@ def msort_sort_distributed(keys: torch.Tensor, comm: Comm, vals: torch.Tensor | 
     if return_split:
         return keys, vals, split.reshape(comm.world + 1, comm.world)
     return keys, vals
+
+
+def msort_sort_distributed_host(host_keys: torch.Tensor, host_keys_out: torch.Tensor,
+                                dev_keys: torch.Tensor, comm: Comm, host_vals=None,
+                                host_vals_out=None, dev_vals=None, ws: torch.Tensor | None = None,
+                                stream=None):
+    """End-to-end collective sort of host tensors (include/msort.h
+    msort_sort_distributed_host): upload into dev_keys, sort across the
+    ranks, copy this rank's slice back to host_keys_out."""
+    for t, name in ((host_keys, "host_keys"), (host_keys_out, "host_keys_out")):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous host tensor")
+    _check_tensor(dev_keys, "dev_keys")
+    n = host_keys.numel()
+    if host_keys_out.numel() != n or dev_keys.numel() != n:
+        raise ValueError("host/device sizes differ")
+    kd, vd = _dt(dev_keys), _vdt(dev_vals)
+    if ws is None:
+        ws = workspace(n, dev_keys.dtype, dev_vals is not None, world=comm.world,
+                       device=dev_keys.device)
+    with _on(dev_keys.device):
+        _check(lib.msort_sort_distributed_host(
+            _ptr(host_keys), _ptr(host_vals), _ptr(host_keys_out), _ptr(host_vals_out), n, kd, vd,
+            comm.handle, _ptr(dev_keys), _ptr(dev_vals), _ptr(ws), ws.numel(),
+            ctypes.c_void_p(_stream(stream))), "msort_sort_distributed_host")
+    return host_keys_out, host_vals_out
 
 
 def msort_sort_distributed_out(in_keys: torch.Tensor, keys_out: torch.Tensor, comm: Comm,

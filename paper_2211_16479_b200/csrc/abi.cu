@@ -555,6 +555,45 @@ msort_status msort_sort_distributed_out_ws(const void* in_keys, const void* in_v
                    (cudaStream_t)stream, split_matrix_out);
 }
 
+msort_status msort_sort_distributed_host(const void* host_keys, const void* host_vals,
+                                         void* host_keys_out, void* host_vals_out,
+                                         size_t n_local, msort_dtype key_dtype,
+                                         msort_dtype val_dtype, msort_comm_t comm,
+                                         void* dev_keys, void* dev_vals, void* ws,
+                                         size_t ws_bytes, msort_stream_t stream) {
+  if (!comm) {
+    set_error("comm is NULL");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  const bool pairs = val_dtype != MSORT_NONE;
+  if (n_local > 0 && (!host_keys || !host_keys_out || (pairs && (!host_vals || !host_vals_out)))) {
+    set_error("msort_sort_distributed_host: NULL host pointer");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  MSORT_TRY(validate(dev_keys, pairs ? dev_vals : nullptr, n_local, key_dtype, val_dtype, false));
+  MSORT_TRY(check_device());
+  const int world = comm_world(comm);
+  MSORT_TRY(validate_ws(dev_keys, pairs ? dev_vals : nullptr, n_local, key_dtype, val_dtype, ws,
+                        ws_bytes, dist_ws_bytes(n_local, key_dtype, val_dtype, world)));
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t kb = n_local * dtype_size(key_dtype);
+  if (n_local > 0) {
+    MSORT_CUDA_TRY(cudaMemcpyAsync(dev_keys, host_keys, kb, cudaMemcpyHostToDevice, s));
+    if (pairs)
+      MSORT_CUDA_TRY(
+          cudaMemcpyAsync(dev_vals, host_vals, n_local * 4, cudaMemcpyHostToDevice, s));
+  }
+  MSORT_TRY(dist_nccl(dev_keys, pairs ? dev_vals : nullptr, dev_keys, pairs ? dev_vals : nullptr,
+                      n_local, key_dtype, val_dtype, comm, ws, s, nullptr));
+  if (n_local > 0) {
+    MSORT_CUDA_TRY(cudaMemcpyAsync(host_keys_out, dev_keys, kb, cudaMemcpyDeviceToHost, s));
+    if (pairs)
+      MSORT_CUDA_TRY(
+          cudaMemcpyAsync(host_vals_out, dev_vals, n_local * 4, cudaMemcpyDeviceToHost, s));
+  }
+  return MSORT_SUCCESS;
+}
+
 msort_status msort_sort_distributed(void* keys, void* vals, size_t n_local,
                                     msort_dtype key_dtype, msort_dtype val_dtype,
                                     msort_comm_t comm, msort_stream_t stream,

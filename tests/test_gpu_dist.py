@@ -217,6 +217,30 @@ def test_nccl_one_rank_reserve_pull(ms, orc):
         comm.close()
 
 
+def test_nccl_one_rank_host_buffers(ms, orc):
+    """msort_sort_distributed_host (bench.py's N > 1 e2e path) on the one-rank
+    NCCL communicator: pinned host keys in, the sorted slice back in host
+    memory."""
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    comm = ms.Comm()
+    n = 123457
+    k = mi.keys(n, 91, "i32")
+    h_in = torch.from_numpy(k.copy()).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    d = torch.empty(n, dtype=torch.int32, device="cuda")
+    ms.msort_sort_distributed_host(h_in, h_out, d, comm)
+    torch.cuda.synchronize()
+    assert np.array_equal(h_out.numpy(), orc.sort(k))
+    assert np.array_equal(h_in.numpy(), k)
+    comm.close()
+
+
 def test_nccl_wait_timeout_aborts(tmp_path):
     """Failure detection (include/msort.h): with MSORT_NCCL_TIMEOUT_S set, a
     distributed call whose stream does not drain in time (here: held up by a
