@@ -60,8 +60,10 @@ def parse():
     ap.add_argument("--no-batched", action="store_true",
                     help="skip the batched (segmented) sort lines (SURVEY §8(f) f3)")
     ap.add_argument("--e2e-streams", type=int, default=3, help="streams the e2e steps rotate over")
-    ap.add_argument("--exchange", choices=["alltoall", "pull"], default="alltoall",
-                    help="N > 1: NCCL all-to-all + k-way merge, or the fused pull exchange")
+    ap.add_argument("--exchange", choices=["auto", "alltoall", "pull"], default="auto",
+                    help="N > 1: NCCL all-to-all + k-way merge, the fused pull exchange "
+                         "(reserved: no host sync per step), or auto = pull if a first "
+                         "verified step agrees on every rank, else all-to-all")
     return ap.parse_args()
 
 
@@ -432,6 +434,44 @@ def configs_bench(ms, mi, dev, peak, reps=20):
                         "out of place from the pristine input", "results": out}
 
 
+def choose_exchange(args, ms, comm, dist, dev, kin, kout, ws, stream, world, rank, n, last_split):
+    """N > 1: the exchange mode of the timed steps.  "pull" (and "auto")
+    reserve the communicator for the fused pull exchange (msort_comm_reserve)
+    and run ONE verified step: its output is checked against the oracle's
+    digest (or order + rank edges when there is none) and every rank's
+    verdict -- including a raised error -- is combined (MIN over ranks), so
+    all ranks take the same decision.  "auto" falls back to the NCCL
+    all-to-all when the pull step fails anywhere; "pull" then raises."""
+    import torch
+
+    if args.exchange == "alltoall":
+        ms.set_exchange_mode(0)
+        return "alltoall"
+    ok = 1
+    err = None
+    try:
+        ms.set_exchange_mode(1)
+        comm.reserve(n, torch.int32, False, stream=stream)
+        last_split[0] = ms.msort_sort_distributed_out(kin, kout, comm, ws=ws, stream=stream,
+                                                      return_split=True)[2]
+        torch.cuda.synchronize()
+        exp = expected_digest(world, rank, n)
+        if exp is not None:
+            ok = int(host_digest(kout.cpu().numpy()) == exp)
+        else:
+            ok = int(bool((kout[1:] >= kout[:-1]).all()))
+    except Exception as e:  # noqa: BLE001 -- decided collectively below
+        ok, err = 0, str(e)[:200]
+    t = torch.tensor([ok], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if int(t.item()) == 1:
+        return "pull"
+    if args.exchange == "pull":
+        raise RuntimeError(f"pull exchange failed on some rank (here: {err})")
+    ms.set_exchange_mode(0)
+    return "alltoall (pull check failed: %s)" % (err or "output mismatch on some rank")
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -457,7 +497,6 @@ def main():
 
         dist.init_process_group("nccl", device_id=dev)
         comm = ms.Comm()
-        ms.set_exchange_mode(1 if args.exchange == "pull" else 0)
 
     n = args.n
     kin = mi.keys_torch(n, SEED0 + rank, "u31", device=dev)
@@ -466,10 +505,16 @@ def main():
     stream = torch.cuda.current_stream()
 
     last_split = [None]
+    exchange = None
+    if world > 1:
+        exchange = choose_exchange(args, ms, comm, dist, dev, kin, kout, ws, stream, world, rank,
+                                   n, last_split)
 
     def step():
         if world == 1:
             ms.msort_sort_out(kin, kout, ws=ws, stream=stream)
+        elif exchange == "pull":  # reserved pull: no host synchronisation inside the call
+            ms.msort_sort_distributed_out(kin, kout, comm, ws=ws, stream=stream)
         else:
             last_split[0] = ms.msort_sort_distributed_out(kin, kout, comm, ws=ws, stream=stream,
                                                           return_split=True)[2]
@@ -579,12 +624,15 @@ def main():
     # receives over NVLink (its segments to / from the other ranks, from the
     # split matrix of the last step) per exchange, over the exchange's live
     # CUDA-event time; the slowest rank is reported
+    # (pull exchange: the transfer happens inside the K5 merge kernel, which
+    # reads every peer's segment in place -- its time is the exchange's)
     xroof = None
-    if world > 1 and prof.get("exchange", (0, 0.0))[0]:
+    xclass = "kway_merge" if exchange == "pull" else "exchange"
+    if world > 1 and prof.get(xclass, (0, 0.0))[0] and last_split[0] is not None:
         S = last_split[0]
         sent = sum(int(S[j + 1][rank] - S[j][rank]) for j in range(world) if j != rank) * wk
         recv = sum(int(S[rank + 1][j] - S[rank][j]) for j in range(world) if j != rank) * wk
-        xl, xms = prof["exchange"]
+        xl, xms = prof[xclass]
         ach = max(sent, recv) / (xms / xl / 1e3) / 1e9
         t = torch.tensor([ach], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
@@ -592,6 +640,8 @@ def main():
         xroof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 770.0, "unit": "GB/s",
                  "frac": round(ach / 770.0, 4), "bytes_sent": sent, "bytes_received": recv,
                  "avg_exchange_ms": round(xms / xl, 4),
+                 "timed_kernel": "k5_merge (exchange fused into the merge)" if exchange == "pull"
+                 else "grouped ncclSend/ncclRecv",
                  "peak_source": "measured peer copy per direction (B200_PROFILING.md; 900 nominal)"}
         # the same exchange against a uniform NCCL all-to-all of
         # the same byte count (torch's all_to_all_single, equal splits), timed
@@ -730,7 +780,7 @@ def main():
                        "l2": "inputs larger than L2 (1 GiB/GPU vs 126 MB); no flush; "
                              "out-of-place sort from the pristine input each step",
                        "parallelism": f"dp{world}" if world > 1 else "single",
-                       "exchange": args.exchange if world > 1 else None},
+                       "exchange": exchange},
             "roofline": roof,
             "exchange_roofline": xroof,
             "step_roofline": {"bytes_per_gpu": step_bytes, "t_roof_ms": t_roof * 1e3,

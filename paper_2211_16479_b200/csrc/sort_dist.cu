@@ -652,12 +652,15 @@ static msort_status dist_run(Coll& C, RankIO* io, int nloc, msort_dtype kd, msor
     for (int l = 0; l < nloc && fits; ++l)
       fits = kway5_dev_bytes((int64_t)io[l].n, p, kd) <= io[l].ws.sort_ws_bytes;
     if (fits) {
-      for (int l = 0; l < nloc; ++l)
-        MSORT_TRY(kway5_dev_dispatch(io[l].ws.split, C.rank_of(l), p, bases, io[l].keys,
-                                     (int64_t)io[l].n, kd, io[l].ws.sort_ws,
-                                     io[l].ws.sort_ws_bytes, s));
+      msort_status st = MSORT_SUCCESS;
+      for (int l = 0; l < nloc && st == MSORT_SUCCESS; ++l)
+        st = kway5_dev_dispatch(io[l].ws.split, C.rank_of(l), p, bases, io[l].keys,
+                                (int64_t)io[l].n, kd, io[l].ws.sort_ws, io[l].ws.sort_ws_bytes, s);
       // every rank has read the others' segments: exchange buffers are free
+      // (the barrier is entered even after a local launch error, so no peer
+      // is left waiting in it)
       MSORT_TRY(C.barrier(io));
+      if (st != MSORT_SUCCESS) return st;
       if (split_out)  // the only host synchronisation, and only when asked for
         MSORT_TRY(C.fetch(split_out, io[0].ws.split, S.size() * 8, "split matrix"));
       return MSORT_SUCCESS;

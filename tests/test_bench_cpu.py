@@ -38,3 +38,83 @@ def test_parser_accepts_driver_flags():
     finally:
         sys.argv = old
     assert (a.gpus, a.steps, a.warmup, a.exchange) == (8, 10, 3, "pull")
+
+
+def _bench_module():
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod2", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+class _FakeDist:
+    """torch.distributed stand-in for one rank: all_reduce(MIN) combines the
+    local flag with the other ranks' (given) flags."""
+
+    class ReduceOp:
+        MIN = "min"
+
+    def __init__(self, others):
+        self.others = others
+
+    def all_reduce(self, t, op=None):
+        t.fill_(min([int(t.item())] + list(self.others)))
+
+
+class _FakeMs:
+    def __init__(self, fail_sort=False):
+        self.mode = None
+        self.fail_sort = fail_sort
+
+    def set_exchange_mode(self, m):
+        self.mode = m
+
+    def msort_sort_distributed_out(self, kin, kout, comm, ws=None, stream=None, return_split=False):
+        import torch
+
+        if self.fail_sort:
+            raise RuntimeError("simulated IPC failure")
+        kout.copy_(torch.sort(kin)[0])
+        return kout, None, [[0], [kin.numel()]]
+
+
+class _FakeComm:
+    def reserve(self, n, keys_dtype=None, with_vals=False, stream=None):
+        self.reserved = n
+
+
+def _choose(monkeypatch, exchange, others, fail_sort=False):
+    import argparse
+
+    import torch
+
+    mod = _bench_module()
+    monkeypatch.setattr(torch.cuda, "synchronize", lambda *a, **k: None)
+    ms = _FakeMs(fail_sort)
+    kin = torch.randint(0, 1000, (4096,), dtype=torch.int32)
+    kout = torch.empty_like(kin)
+    args = argparse.Namespace(exchange=exchange)
+    last = [None]
+    got = mod.choose_exchange(args, ms, _FakeComm(), _FakeDist(others), "cpu", kin, kout, None,
+                              None, 2, 0, kin.numel(), last)
+    return got, ms.mode, last[0]
+
+
+def test_choose_exchange_agreement(monkeypatch):
+    """bench.py N > 1: the pull exchange is used only when the verified first
+    step succeeds on EVERY rank (MIN over ranks); otherwise all ranks take
+    the all-to-all together ("auto") or fail together ("pull")."""
+    import pytest
+
+    got, mode, split = _choose(monkeypatch, "auto", [1])
+    assert got == "pull" and mode == 1 and split is not None
+    got, mode, _ = _choose(monkeypatch, "auto", [0])  # another rank failed
+    assert got.startswith("alltoall") and mode == 0
+    got, mode, _ = _choose(monkeypatch, "auto", [1], fail_sort=True)  # this rank failed
+    assert got.startswith("alltoall") and mode == 0 and "simulated" in got
+    got, mode, _ = _choose(monkeypatch, "alltoall", [1])
+    assert got == "alltoall" and mode == 0
+    with pytest.raises(RuntimeError):
+        _choose(monkeypatch, "pull", [0])
