@@ -324,7 +324,8 @@ def config_digest(name):
 
 def configs_bench(ms, mi, dev, peak, reps=20):
     """BASELINE.json's single-GPU configs beside the headline:
-    C1 (2^16 int32), C2 (2^24 int32), C3 (2^26 int64 in [0,1000) + uint32
+    C1 (2^16 int32), C2 (2^24 int32; C2s / C2r: the same keys already sorted /
+    reverse-sorted -- P:142's "unaffected by the initial array"), C3 (2^26 int64 in [0,1000) + uint32
     index payload), C4 (2^27 uint32 + uint32 index payload).  Per config:
     median device ms of `reps` out-of-place sorts from the pristine input
     (CUDA events around each call; an untimed L2 flush before each for C1/C2,
@@ -339,12 +340,16 @@ def configs_bench(ms, mi, dev, peak, reps=20):
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     out = {}
-    for name in ("C1", "C2", "C3", "C4"):
-        c = mi.CONFIGS[name]
+    for name in ("C1", "C2", "C2s", "C2r", "C3", "C4"):
+        c = mi.CONFIGS[name[:2]]
         n, pairs = c["n"], c["pairs"]
         k = mi.keys_torch(n, c["seed"], c["dist"], device=dev)
         if c["dist"] == "u32":
             k = k.view(torch.uint32)
+        if name in ("C2s", "C2r"):  # BASELINE config 2's already-sorted / reverse-sorted arrays
+            k = torch.sort(k)[0]   # (reading R8: the sorted C2 array and its reversal)
+            if name == "C2r":
+                k = torch.flip(k, [0]).contiguous()
         kin = k
         vin = torch.arange(n, dtype=torch.int32, device=dev).view(torch.uint32) if pairs else None
         kout = torch.empty_like(kin)
@@ -387,7 +392,7 @@ def configs_bench(ms, mi, dev, peak, reps=20):
                     "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
                     "avg_launch_ms": round(mp_ms / mp_l, 4), "merge_levels": levels}
         t_roof = (levels + 1) * per_pass / (peak * 1e9) * 1e3
-        exp = config_digest(name)
+        exp = config_digest(name[:2])  # C2s / C2r sort to C2's output (same multiset)
         ok = None
         if exp:
             a = kout.view(torch.int64 if wk == 8 else torch.int32).cpu().numpy()
@@ -430,8 +435,12 @@ def configs_bench(ms, mi, dev, peak, reps=20):
         out[name] = d
         del k, kin, vin, kout, vout, ws
         torch.cuda.empty_cache()
-    return {"workload": "BASELINE.json configs 1-4 (msort_inputs.CONFIGS), one GPU, "
-                        "out of place from the pristine input", "results": out}
+    r = {"workload": "BASELINE.json configs 1-4 (msort_inputs.CONFIGS), one GPU, "
+                     "out of place from the pristine input", "results": out}
+    if "C2" in out and "C2s" in out and "C2r" in out:
+        r["t_C2s_over_C2"] = round(out["C2s"]["ms"] / out["C2"]["ms"], 3)
+        r["t_C2r_over_C2"] = round(out["C2r"]["ms"] / out["C2"]["ms"], 3)
+    return r
 
 
 def choose_exchange(args, ms, comm, dist, dev, kin, kout, ws, stream, world, rank, n, last_split):

@@ -199,13 +199,21 @@ __global__ void __launch_bounds__(kK0NT, 1)
     const int j0 = d0 - i0;
     // the two windows, from the peers: A[i0, i1) then B[j0, j0 + lb)
     {
-      // all VT loads of a thread in flight at once (DSMEM latency), then stores
+      // all VT loads of a thread in flight at once (DSMEM latency), then
+      // stores.  Each window (<= Q keys) spans at most two chunks: the chunk
+      // of its first key and the next, so a compare replaces the divisions.
+      const int ga = a_start + i0, gb = b_start + j0;
+      const int ca = ga / Q, cb = gb / Q;
+      const int ea = (ca + 1) * Q, eb = (cb + 1) * Q;  // first key of the next chunk
       K v[VT];
 #pragma unroll
       for (int k = 0; k < VT; ++k) {
         const int e = tid + k * NT;
-        const int g = e < la ? a_start + i0 + e : b_start + j0 + (e - la);
-        if (e < len) v[k] = k0_at(chunk, Q, g);
+        const bool inA = e < la;
+        const int g = inA ? ga + e : gb + (e - la);
+        const int c0 = inA ? ca : cb;
+        const int c1 = g < (inA ? ea : eb) ? c0 : c0 + 1;
+        if (e < len) v[k] = chunk[c1][sidx<K, true>(g - c1 * Q)];
       }
 #pragma unroll
       for (int k = 0; k < VT; ++k) {
