@@ -83,6 +83,23 @@ def test_emulated_random_unequal_sizes(ms, orc, p, pairs):
         run_emulated(ms, orc, shards, pairs)
 
 
+@pytest.mark.parametrize("p", [3, 5, 8])
+def test_emulated_skewed_ranges(ms, orc, p):
+    """Rank j holds keys only in [ (p-1-j) 2^20, (p-j) 2^20 ) (reversed rank
+    order) or all in one narrow band: every rank's output comes from one or
+    two source ranks, so the K5 runs are extremely unequal (most empty) --
+    the device-planned K5 of the pull exchange and the received-run K5 of
+    the all-to-all both see it."""
+    shards = []
+    for r in range(p):
+        z = mi.splitmix64(30000 + 1000 * r, 700 + r) % np.uint64(1 << 20)
+        shards.append((z.astype(np.int64) + ((p - 1 - r) << 20)).astype(np.int32))
+    run_emulated(ms, orc, shards, False)
+    band = [(mi.splitmix64(25000, 800 + r) % np.uint64(64)).astype(np.int32) + 7 for r in range(p)]
+    band[1] = band[1][:0]  # and an empty rank
+    run_emulated(ms, orc, band, False)
+
+
 @pytest.mark.parametrize("dtype,dist", [(np.int64, ("mod", 5)), (np.uint32, "eq"),
                                         (np.int32, "eq"), (np.uint64, "u64"),
                                         (np.int64, ("mod", 1000))])
