@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="keys per GPU (default 2^28)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--distributed-path", action="store_true",
+                    help="run the N > 1 code path even at N = 1 (a one-rank NCCL group; a "
+                         "smoke test of the distributed bench on a one-GPU box)")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config lines (C1-C4, BASELINE.json configs 1-4)")
     ap.add_argument("--no-batched", action="store_true",
@@ -501,10 +504,16 @@ def main():
     dev = torch.device("cuda", local)
     dist = None
     comm = None
-    if world > 1:
+    dpath = world > 1 or args.distributed_path  # the distributed code path
+    if dpath:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29531")
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         comm = ms.Comm()
 
     n = args.n
@@ -515,12 +524,12 @@ def main():
 
     last_split = [None]
     exchange = None
-    if world > 1:
+    if dpath:
         exchange = choose_exchange(args, ms, comm, dist, dev, kin, kout, ws, stream, world, rank,
                                    n, last_split)
 
     def step():
-        if world == 1:
+        if not dpath:
             ms.msort_sort_out(kin, kout, ws=ws, stream=stream)
         elif exchange == "pull":  # reserved pull: no host synchronisation inside the call
             ms.msort_sort_distributed_out(kin, kout, comm, ws=ws, stream=stream)
@@ -529,7 +538,7 @@ def main():
                                                           return_split=True)[2]
 
     def barrier():
-        if world > 1:
+        if dpath:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -557,7 +566,7 @@ def main():
     time.sleep(0.2)
     sampler.stop()
     ms_total = e0.elapsed_time(e1)
-    if world > 1:
+    if dpath:
         t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
@@ -578,7 +587,7 @@ def main():
         vmethod = "order + multiset sum (+ rank edges); no oracle digest for this size / world"
         if world == 1:
             ok &= int(kout.sum(dtype=torch.int64)) == int(kin.sum(dtype=torch.int64))
-    if world > 1:
+    if dpath:
         if exp is None:
             edge = torch.tensor([int(kout[0]), int(kout[-1])], dtype=torch.int64, device=dev)
             edges = [torch.zeros_like(edge) for _ in range(world)]
@@ -697,7 +706,7 @@ def main():
     if not args.no_e2e:
         h_in = kin.cpu().pin_memory()
         ke = max(6, min(args.steps, 12))
-        if world == 1:
+        if not dpath:
             NS = max(1, args.e2e_streams)
             h_out = [torch.empty_like(h_in).pin_memory() for _ in range(NS)]
             d_buf = [torch.empty_like(kin) for _ in range(NS)]
@@ -748,14 +757,14 @@ def main():
             ok &= (host_digest(o) == exp) if exp else bool(np.all(o[1:] >= o[:-1]))
             path = ("msort_sort_distributed_host (pinned host -> device -> distributed sort -> "
                     "pinned host)")
-        if world > 1:
+        if dpath:
             t = torch.tensor([te], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         e2e = {"value": world * n * ke / (te / 1e3), "unit": "keys/s",
                "h2d_bytes_per_step": n * wk, "d2h_bytes_per_step": n * wk,
                "ms_per_step": te / ke, "steps": ke, "path": path}
-        if world == 1:
+        if not dpath:
             # the PCIe ceiling of this e2e step: the same upload and download
             # alone, both directions at once on two streams (no sort)
             fl = pcie_duplex_ms(h_in, h_out[0], d_buf[0], kin, strs)
@@ -763,14 +772,14 @@ def main():
             e2e["frac_of_pcie"] = round(fl / (te / ke), 4)
 
     batched = None
-    if rank == 0 and world == 1 and not args.no_batched:
+    if rank == 0 and not dpath and not args.no_batched:
         batched = batched_bench(ms, mi, dev)
     per_config = None
-    if rank == 0 and world == 1 and not args.no_configs:
+    if rank == 0 and not dpath and not args.no_configs:
         per_config = configs_bench(ms, mi, dev, peak)
 
     cpu = cpu_mp = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not dpath and not args.no_cpu_baseline:
         cpu = cpu_baseline(n, 1, SEED0)       # O-1 on the full rank-0 shard
         cpu_mp = cpu_paper_mp(n, SEED0)       # O-c on the same shard, all host cores
 
