@@ -226,6 +226,26 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+#ifdef MSORT_K3_TRACE
+// Tuning builds only: per-tile publish times (index pass * ntiles + q) and
+// per-chunk times (grab, inputs ready, co-ranks searched, CTA) of the last
+// fused K3 launch.
+constexpr int kK3TraceTiles = 1 << 20, kK3TraceChunks = 1 << 18;
+__device__ unsigned long long g_k3_tiles[kK3TraceTiles];
+__device__ unsigned long long g_k3_chunks[kK3TraceChunks * 4];
+__device__ __forceinline__ unsigned long long gtimer2() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void k3_trace_chunk(int64_t g, int slot, unsigned long long v) {
+  if (g < kK3TraceChunks) g_k3_chunks[g * 4 + slot] = v;
+}
+#define K3_TRACE_CHUNK(g, slot, v) k3_trace_chunk((g), (slot), (v))
+#else
+#define K3_TRACE_CHUNK(g, slot, v) ((void)0)
+#endif
+
 // All merge levels of one sort: level p merges runs of L_p = T * 2^p from
 // buffer bk[p & 1] into bk[(p+1) & 1]; every level has the same tile count.
 template <class K>
@@ -298,6 +318,10 @@ struct FusedPasses {
     fence_proxy_async_global();
 #endif
     red_release_gpu_add(done + pair_base[pass] + pair_of(pass, q, Tm), 1u);
+#ifdef MSORT_K3_TRACE
+    const int64_t ti = (int64_t)pass * ntiles + q;
+    if (ti < kK3TraceTiles) g_k3_tiles[ti] = gtimer2();
+#endif
   }
 };
 
@@ -485,6 +509,10 @@ __device__ __forceinline__ int64_t corank_warp(const Src& src, int pass, int64_t
 }
 
 constexpr int kK3Extra = 96;  // producer, searcher and store warps
+#ifndef MSORT_SEARCH_PL
+#define MSORT_SEARCH_PL 1
+#endif
+constexpr int kSearchPL = MSORT_SEARCH_PL;  // probes per lane per round (group searches)
 
 template <class K, bool PAIRS, int NC, int VT, int S, int MINB, class Src>
 __global__ void __launch_bounds__(NC + kK3Extra, MINB)
@@ -536,7 +564,9 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
     int pass, cnt;
     int64_t q0;
     src.chunk(c, pass, q0, cnt);
+    if (threadIdx.x == 0) K3_TRACE_CHUNK(c, 0, gtimer2()), K3_TRACE_CHUNK(c, 3, blockIdx.x);
     if (warp == 0) src.wait_ready(pass, q0, cnt, lane, Tm);
+    if (threadIdx.x == 0) K3_TRACE_CHUNK(c, 1, gtimer2());
     __syncthreads();
     for (int w = warp; w <= cnt; w += NW) {
       const int64_t q = q0 + w;
@@ -545,6 +575,10 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
     }
     if (threadIdx.x == 0) ring[0].q0 = q0, ring[0].cnt = cnt, ring[0].pass = pass;
   }
+#ifdef MSORT_K3_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) K3_TRACE_CHUNK(*first_chunk, 2, gtimer2());
+#endif
   __syncthreads();
 #ifdef MSORT_K3_TRACE
   if (threadIdx.x == 0) K3_TRACE(1, gtimer() - t_start);
@@ -593,11 +627,81 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
           if (p_ != pass0) break;
           ++mm1;
         }
+#ifdef MSORT_K3_TRACE
+        if (lane == 0)
+          for (int mm = mm0; mm < mm1; ++mm)
+            K3_TRACE_CHUNK(c0 + mm, 0, gtimer2()), K3_TRACE_CHUNK(c0 + mm, 3, blockIdx.x);
+#endif
         for (int mm = mm0; mm < mm1; ++mm) {
           int p_, c_;
           int64_t q2;
           src.chunk(c0 + mm, p_, q2, c_);
           src.wait_ready(p_, q2, c_, lane, Tm);
+        }
+#ifdef MSORT_K3_TRACE
+        if (lane == 0)
+          for (int mm = mm0; mm < mm1; ++mm) K3_TRACE_CHUNK(c0 + mm, 1, gtimer2());
+#endif
+        if (G == 1) {
+          // One chunk per grab (small sorts): its <= kChunk + 1 co-ranks are
+          // searched by lane GROUPS -- the two edges by 16 lanes each, then
+          // the inner ones (inside the edges' bracket) by 32 / (cnt - 1)
+          // lanes each -- so the probe latency chain is log_16 of the range,
+          // not log2 (the searcher is the critical path of a small sort).
+          int p_, cnt1;
+          int64_t q01;
+          src.chunk(c0 + mm0, p_, q01, cnt1);
+          const int e = lane >> 4, gl = lane & 15;
+          const int je = e ? cnt1 : 0;
+          const bool ve = q01 + je < src.tiles(pass0);
+          int64_t A0e = -1, nae = 0, nbe = 0, dle = 0;  // -1: no pair (bracket unused)
+          if (ve) src.locate(pass0, q01 + je, Tm, A0e, nae, nbe, dle);
+          const K* rae = ve ? src.pa(pass0, q01 + je, A0e, nae) : nullptr;
+          const K* rbe = ve ? src.pb(pass0, q01 + je, A0e, nae) : nullptr;
+          const int64_t ve_ = merge_path_global_group<kSearchPL>(
+              rae, rbe, dle, dle - nbe > 0 ? dle - nbe : 0, dle < nae ? dle : nae, ve, gl, 4,
+              e << 4);
+          const int64_t v0 = __shfl_sync(0xffffffffu, ve ? ve_ : 0, 0);
+          const int64_t a00 = __shfl_sync(0xffffffffu, A0e, 0);
+          const int64_t vN = __shfl_sync(0xffffffffu, ve ? ve_ : 0, 16);
+          const int64_t a0N = __shfl_sync(0xffffffffu, A0e, 16);
+          const int ni = cnt1 - 1;  // inner co-ranks
+          int64_t vi = 0;
+          int ji = 0;
+          bool vin = false;
+          if (ni > 0) {
+            const int LG = ni == 1 ? 5 : ni == 2 ? 4 : ni <= 4 ? 3 : 2;
+            const int grp = lane >> LG;
+            ji = 1 + grp;
+            vin = grp < ni && q01 + ji < src.tiles(pass0);
+            int64_t A0 = 0, na = 0, nb = 0, dl = 0;
+            int64_t lo = 0, hi = 0;
+            const K* ra = nullptr;
+            const K* rbp = nullptr;
+            if (vin) {
+              src.locate(pass0, q01 + ji, Tm, A0, na, nb, dl);
+              ra = src.pa(pass0, q01 + ji, A0, na);
+              rbp = src.pb(pass0, q01 + ji, A0, na);
+              lo = dl - nb > 0 ? dl - nb : 0;
+              hi = dl < na ? dl : na;
+              if (a00 == A0) lo = max(lo, v0), hi = min(hi, v0 + (int64_t)ji * Tm);
+              if (a0N == A0) lo = max(lo, vN - (int64_t)(cnt1 - ji) * Tm), hi = min(hi, vN);
+            }
+            vi = merge_path_global_group<kSearchPL>(ra, rbp, dl, lo, hi, vin, lane & ((1 << LG) - 1),
+                                         LG, grp << LG);
+            vin = vin && (lane & ((1 << LG) - 1)) == 0;
+          }
+#ifdef MSORT_K3_TRACE
+          if (lane == 0) K3_TRACE_CHUNK(c0 + mm0, 2, gtimer2());
+#endif
+          const int r = (int)((g * G + mm0) % R);
+          if (lane == 0) ring[r].co[0] = v0;
+          if (lane == 16) ring[r].co[cnt1] = vN;
+          if (vin) ring[r].co[ji] = vi;
+          if (lane == 0) ring[r].q0 = q01, ring[r].cnt = cnt1, ring[r].pass = p_;
+          mbar_arrive(&sfull[r]);
+          mm0 = mm0 + 1;
+          continue;
         }
         // Two rounds: the chunk's first and last co-ranks by full searches,
         // then the inner ones inside the bracket those give (co-ranks are
@@ -638,6 +742,11 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
           }
           v = merge_path_global_range(ra, rbp, dl, lo, hi);
         }
+#ifdef MSORT_K3_TRACE
+        __syncwarp();
+        if (lane == 0)
+          for (int mm = mm0; mm < mm1; ++mm) K3_TRACE_CHUNK(c0 + mm, 2, gtimer2());
+#endif
         for (int mm = mm0; mm < mm1; ++mm) {
           const int r = (int)((g * G + mm) % R);
           if (m == mm && j <= cntm) ring[r].co[j] = v;

@@ -139,6 +139,60 @@ __device__ __forceinline__ int64_t merge_path_global_range(const K* __restrict__
   return lo;
 }
 
+// The same search by a group of GS = 2^LG lanes of a warp (lanes gbase ..
+// gbase+GS-1; every lane of the warp calls it, `active` false for lanes
+// without a search), each lane probing PL candidates per round: a round
+// probes C = GS * PL evenly spaced candidates of [lo, hi) -- all of its
+// 2C loads in flight at once -- and keeps the bucket where the monotone
+// predicate A[i] > B[d-1-i] turns true, so the dependent probe latency is
+// paid log_C(range) times instead of log2(range).  Used where a warp has
+// fewer searches than lanes and probe latency is on the critical path (small
+// sorts: K3's searcher with one chunk per grab).
+template <int PL, class K>
+__device__ __forceinline__ int64_t merge_path_global_group(const K* __restrict__ a,
+                                                           const K* __restrict__ b, int64_t d,
+                                                           int64_t lo, int64_t hi, bool active,
+                                                           int gl, int LG, int gbase) {
+  const uint64_t pol = probe_policy();
+  const int GS = 1 << LG;
+  const unsigned gm = GS == 32 ? 0xffffffffu : ((1u << GS) - 1u);
+  const int64_t C = (int64_t)GS * PL;
+  while (__any_sync(0xffffffffu, active && hi > lo)) {
+    const bool act = active && hi > lo;
+    const int64_t span = hi - lo;
+    const int64_t step = (span + C - 1) / C;
+    int t1 = PL;  // first candidate of this lane where the predicate holds
+    if (act) {
+      K av[PL], bv[PL];
+#pragma unroll
+      for (int t = 0; t < PL; ++t) {
+        const int64_t off = step * (gl * PL + t + 1);
+        const int64_t p = lo + (off < span ? off : span) - 1;
+        av[t] = probe_ld(a + p, pol);
+        bv[t] = probe_ld(b + (d - 1 - p), pol);
+      }
+#pragma unroll
+      for (int t = PL - 1; t >= 0; --t)
+        if (av[t] > bv[t]) t1 = t;
+    }
+    const unsigned m = (__ballot_sync(0xffffffffu, t1 < PL) >> gbase) & gm;
+    const int f = m ? __ffs(m) - 1 : 0;
+    const int tf = __shfl_sync(0xffffffffu, t1, gbase + f);
+    if (act) {
+      if (m == 0) {
+        lo = hi;
+      } else {
+        const int64_t k = (int64_t)f * PL + tf;  // first candidate where it holds
+        const int64_t ok = step * (k + 1), ok0 = step * k;
+        const int64_t nlo = k > 0 ? lo + (ok0 < span ? ok0 : span) : lo;
+        hi = lo + (ok < span ? ok : span) - 1;
+        lo = nlo;
+      }
+    }
+  }
+  return lo;
+}
+
 // Serial stable merge of VT outputs starting at (ai, bi): take B only when
 // B < A (strict), so ties go to A.  Positions are indices into the shared
 // buffer s; `pos` records the source position of each output (for payload

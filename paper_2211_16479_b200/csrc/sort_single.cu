@@ -433,6 +433,20 @@ extern "C" int msort_debug_k0_trace(unsigned long long* host) {
 extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, g_k3_trace, sizeof(unsigned long long) * n);
 }
+extern "C" int msort_debug_k3_trace2(unsigned long long* tiles, int nt, unsigned long long* chunks,
+                                     int nc) {
+  int e = (int)cudaMemcpyFromSymbol(tiles, g_k3_tiles, sizeof(unsigned long long) * nt);
+  if (e) return e;
+  return (int)cudaMemcpyFromSymbol(chunks, g_k3_chunks, sizeof(unsigned long long) * nc * 4);
+}
+extern "C" int msort_debug_k3_trace_clear() {
+  void *pt = nullptr, *pc = nullptr;
+  cudaError_t e = cudaGetSymbolAddress(&pt, g_k3_tiles);
+  if (!e) e = cudaGetSymbolAddress(&pc, g_k3_chunks);
+  if (!e) e = cudaMemset(pt, 0, sizeof(unsigned long long) * kK3TraceTiles);
+  if (!e) e = cudaMemset(pc, 0, sizeof(unsigned long long) * kK3TraceChunks * 4);
+  return (int)e;
+}
 #endif
 
 // ------------------------------------------------------------ host driver
@@ -449,6 +463,9 @@ extern "C" int msort_debug_k3_trace(unsigned long long* host, int n) {
 #define MSORT_K3_VT 17  // outputs per merging thread (even: two chains per thread)
 #endif
 
+#ifndef MSORT_K3_GRABDIV
+#define MSORT_K3_GRABDIV 4  // grabs of kGrab chunks per CTA per level below which grabs are single
+#endif
 #ifndef MSORT_K3_CHDIV
 #define MSORT_K3_CHDIV 2  // full chunks per CTA per level below which chunks shrink
 #endif
@@ -640,6 +657,17 @@ struct Kernels {
   static int chunk_tiles(int64_t tiles, int dev) {
     const int64_t per = tiles / (MSORT_K3_CHDIV * (int64_t)std::max(grid3(dev), 1));
     return (int)std::max<int64_t>(1, std::min<int64_t>(kChunk, per));
+  }
+  // Chunks per atomic grab: kGrab only when every CTA gets >= MSORT_K3_GRABDIV
+  // grabs per level, else 1 -- a grab of kGrab full chunks is 24 tiles, and
+  // with ~1-2 grabs per CTA and level the level waits for the CTAs that got
+  // one more (2^26 int32: 2.04 -> 1.64 ms); with one chunk per grab the
+  // searcher's lanes search that chunk's co-ranks in groups (k3_merge.cuh).
+  static int grab_for(int64_t tiles, int ch, int dev) {
+    if (ch < kChunk) return 1;
+    const int64_t need =
+        (int64_t)MSORT_K3_GRABDIV * std::max(grid3(dev), 1) * (int64_t)ch * kGrab;
+    return tiles >= need ? kGrab : 1;
   }
 
   // Kernel attributes are set lazily, per kernel instance and device, the
@@ -865,7 +893,7 @@ struct Kernels {
       sp.src_k = bk[cur], sp.src_v = bv[cur], sp.dst_k = bk[cur ^ 1], sp.dst_v = bv[cur ^ 1];
       sp.ntiles = (int64_t)((n + Tm - 1) / Tm);
       sp.ch = chunk_tiles(sp.ntiles, dev);
-      sp.grab = sp.ch < kChunk ? 1 : kGrab;
+      sp.grab = grab_for(sp.ntiles, sp.ch, dev);
       MSORT_TRY(launch_k3(sp, (sp.ntiles + sp.ch - 1) / sp.ch, ctr + p, s, KC_MERGE));
       cur ^= 1;
     }
@@ -886,7 +914,7 @@ struct Kernels {
     f.pair_base[left] = pb;
     MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * 8 + pb * 4, s));
     f.ch = chunk_tiles(f.ntiles, dev);
-    f.grab = f.ch < kChunk ? 1 : kGrab;  // small sorts: one chunk per CTA at a time
+    f.grab = grab_for(f.ntiles, f.ch, dev);
     return launch_k3(f, (int64_t)left * ((f.ntiles + f.ch - 1) / f.ch), ctr, s, KC_MERGE);
   }
 
@@ -1159,7 +1187,7 @@ struct Kernels {
       f.lev = reinterpret_cast<const int*>(tab + 3 * nxl + 1);
       f.nseg = (int)nxl, f.T = T, f.ntiles = ntl_all, f.P = Pmax, f.done = done;
       f.ch = chunk_tiles(ntl_all, dev);
-      f.grab = f.ch < kChunk ? 1 : kGrab;
+      f.grab = grab_for(f.ntiles, f.ch, dev);
       f.cbase[0] = 0;
       int64_t act = nxl;  // segments with more than p levels (a prefix of xo)
       for (int p = 0; p < Pmax; ++p) {
@@ -1211,7 +1239,7 @@ struct Kernels {
     if (tiles == 0) return MSORT_SUCCESS;
     src.dst_k = out_k, src.dst_v = out_v, src.ntiles = tiles;
     src.ch = chunk_tiles(tiles, dev);
-    src.grab = src.ch < kChunk ? 1 : kGrab;
+    src.grab = grab_for(src.ntiles, src.ch, dev);
     MSORT_CUDA_TRY(cudaMemsetAsync(ctr, 0, kMaxLaunches * sizeof(unsigned long long), s));
     return launch_k3(src, (tiles + src.ch - 1) / src.ch, ctr, s, KC_KWAY);
   }
@@ -1508,7 +1536,7 @@ struct Kernels {
       // tile <= q, which is never an empty one
       if (tiles > 0) {
         src.ch = chunk_tiles(tiles, dev);
-        src.grab = src.ch < kChunk ? 1 : kGrab;
+        src.grab = grab_for(src.ntiles, src.ch, dev);
         MSORT_TRY(launch_k3(src, (tiles + src.ch - 1) / src.ch, ctr + round, s, kc));
       }
       int nr = pm.npairs;
