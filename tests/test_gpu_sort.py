@@ -290,3 +290,20 @@ def test_small_cluster_sort_c1_out_of_place_and_graph(ms, orc):
         g.replay()
         torch.cuda.synchronize()
         assert np.array_equal(to_host(kout, np.int32), orc.sort(k2))
+
+
+# ---- K3 chunk scheduling: single-chunk grabs whose co-ranks are searched by
+# lane groups (edges by 16 lanes, inner ones inside the edges' bracket), with
+# ragged last chunks at every level and chunk sizes 1..8 tiles
+@pytest.mark.parametrize("n,dist,dtype,pairs", [
+    ((1 << 21) + 4321, "rand", np.int32, False),     # chunks of 1 tile
+    (9 * (1 << 20) + 77, "dup", np.int32, False),    # 2-tile chunks, heavy ties
+    ((1 << 24) + 12345, "rand", np.uint32, False),   # 3-tile chunks (C2 + a tail)
+    (3 * (1 << 24) + 11, "rand", np.int32, False),   # 8-tile chunks, one per grab
+    ((1 << 25) - 5, "dup", np.int64, True),          # 8-byte keys + payload
+    ((1 << 26) + 999, "rand", np.int32, False),      # 2^26: single-chunk grabs
+])
+def test_k3_single_chunk_grabs(ms, orc, n, dist, dtype, pairs):
+    k = _keys(n, 7100 + n % 97, dist, dtype)
+    v = mi.index_payload(n) if pairs else None
+    check_parity(ms, orc, k, v)
