@@ -4,7 +4,7 @@
 // fixed costs dominate (P:332, P:565 -- multiprocessing loses to the
 // sequential sort at 10^4 keys).  On the GPU the general path costs two
 // kernels (tile sort + fused merge levels), each latency-bound at this size
-// (2^16 int32: ~25 us each).  K0 sorts n <= CL * NT * VT keys (CL <= 8 CTAs
+// (2^16 int32: ~25 us each).  K0 sorts n <= CL * NT * VT keys (CL <= 16 CTAs
 // of one thread-block CLUSTER) in a single launch, keys only:
 //   1. each CTA sorts its chunk of Q = ceil(n / CL) keys: a per-thread
 //      register network on VT keys, then log2(NT) merge-path rounds in
@@ -27,21 +27,35 @@ namespace msort {
 
 #ifdef MSORT_K0_TRACE
 // Tuning builds only (-DMSORT_K0_TRACE): globaltimer per CTA and phase.
-__device__ unsigned long long g_k0_trace[8 * 16];
+__device__ unsigned long long g_k0_trace[16 * 32];  // [CTA][slot]
 __device__ __forceinline__ void k0_mark(int slot) {
   if (threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_k0_trace[blockIdx.x * 16 + slot] = t;
+    g_k0_trace[blockIdx.x * 32 + slot] = t;
   }
 }
 #else
 __device__ __forceinline__ void k0_mark(int) {}
 #endif
 
-constexpr int kK0NT = 512, kK0VT = 16, kK0Chunk = kK0NT * kK0VT;  // 8192 keys per CTA
-constexpr int kK0MaxCL = 8;                                         // portable cluster size
-constexpr int64_t kK0MaxN = (int64_t)kK0MaxCL * kK0Chunk;           // 65536 = 2^16
+// 512 threads x 8 keys per CTA, up to 16 CTAs (a non-portable cluster size,
+// schedulable on B200): C1 (2^16 int32) 38.9 -> 30.7 us per sort (CUDA-graph
+// replay) against 512 x 16 x 8 CTAs; 1024 x 4 x 16: 34.8, 256 x 16 x 16:
+// 34.8 (profiles/r02/k0/).
+#ifndef MSORT_K0_NT
+#define MSORT_K0_NT 512
+#endif
+#ifndef MSORT_K0_VT
+#define MSORT_K0_VT 8
+#endif
+#ifndef MSORT_K0_MAXCL
+#define MSORT_K0_MAXCL 16
+#endif
+constexpr int kK0NT = MSORT_K0_NT, kK0VT = MSORT_K0_VT, kK0Chunk = kK0NT * kK0VT;  // keys per CTA
+constexpr int kK0MaxCL = MSORT_K0_MAXCL;  // cluster size (> 8: non-portable, B200 allows 16)
+constexpr int64_t kK0MaxN = (int64_t)kK0MaxCL * kK0Chunk;  // 65536 = 2^16
+static_assert(kK0MaxN >= 65536, "K0 covers C1 (2^16 keys)");
 
 // Shared-memory buffers are padded (one spare word per 128 bytes, sidx):
 // a thread's VT = 16 consecutive keys then sit in distinct banks across a
@@ -244,10 +258,10 @@ __global__ void __launch_bounds__(kK0NT, 1)
     k0_mark(6 + 3 * lvl);
     cluster.sync();  // level written everywhere; nobody still reads the old buffers
   }
-  k0_mark(14);
+  k0_mark(30);
   // keep every CTA's shared memory alive until the peers' last reads are done
   cluster.sync();
-  k0_mark(15);
+  k0_mark(31);
 }
 
 }  // namespace msort

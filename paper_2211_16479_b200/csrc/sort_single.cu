@@ -426,7 +426,7 @@ extern "C" int msort_debug_tile_sort(const void* in, void* out, int64_t n, int v
 
 #ifdef MSORT_K0_TRACE
 extern "C" int msort_debug_k0_trace(unsigned long long* host) {
-  return (int)cudaMemcpyFromSymbol(host, g_k0_trace, sizeof(unsigned long long) * 8 * 16);
+  return (int)cudaMemcpyFromSymbol(host, g_k0_trace, sizeof(unsigned long long) * 16 * 32);
 }
 #endif
 #ifdef MSORT_K3_TRACE
@@ -766,7 +766,8 @@ struct Kernels {
     }
     if constexpr (!PAIRS) {
       // small keys-only sorts: the whole sort in one cluster launch (K0)
-      if ((int64_t)n <= kK0MaxN && k0_enabled()) return small_sort(in_k, keys, (int64_t)n, s);
+      if ((int64_t)n <= kK0MaxN && k0_enabled() && (int64_t)n <= k0_limit())
+        return small_sort(in_k, keys, (int64_t)n, s);
     }
     const int64_t ntiles = (int64_t)((n + T - 1) / T);
     int passes = 0;
@@ -932,9 +933,44 @@ struct Kernels {
     if (!done[dev & 63].load(std::memory_order_acquire)) {
       MSORT_CUDA_TRY(cudaFuncSetAttribute(k0_small_sort<K, SHFL>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (kK0MaxCL > 8)
+        MSORT_CUDA_TRY(cudaFuncSetAttribute(k0_small_sort<K, SHFL>,
+                                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       done[dev & 63].store(true, std::memory_order_release);
     }
     return MSORT_SUCCESS;
+  }
+  // Largest n K0 takes on this device: kK0MaxN when a cluster of kK0MaxCL
+  // CTAs (16: non-portable) is schedulable, else what 8 CTAs hold (the
+  // general path takes the rest).  Queried once per device.
+  static int64_t k0_limit() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    static std::atomic<int64_t> lim[64];
+    int64_t v = lim[dev & 63].load(std::memory_order_acquire);
+    if (v) return v;
+    v = (int64_t)std::min(kK0MaxCL, 8) * kK0Chunk;
+    constexpr size_t smem = 3 * (size_t)k0_padded<K>() * sizeof(K);
+    if (kK0MaxCL > 8 && k0_attr<true>(dev, smem) == MSORT_SUCCESS) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)kK0MaxCL, 1, 1);
+      cfg.blockDim = dim3(kK0NT, 1, 1);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = (unsigned)kK0MaxCL;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, k0_small_sort<K, true>, &cfg) == cudaSuccess &&
+          nc > 0)
+        v = kK0MaxN;
+      cudaGetLastError();  // a refused query is not an error of this call
+    }
+    lim[dev & 63].store(v, std::memory_order_release);
+    return v;
   }
   static msort_status small_sort(const K* in, K* out, int64_t n, cudaStream_t s) {
     int dev = 0;

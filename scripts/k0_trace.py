@@ -22,11 +22,14 @@ kout = torch.empty_like(kin)
 for _ in range(5):
     ms.msort_sort_out(kin, kout)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 128)()
+buf = (ctypes.c_ulonglong * (16 * 32))()
 ms.lib.msort_debug_k0_trace(buf)
-t = [[buf[c * 16 + s] for s in range(16)] for c in range(8)]
+t = [[buf[c * 32 + s] for s in range(32)] for c in range(16)]
 t0 = min(x for row in t for x in row if x)
-names = ["start", "bitonic", "phase1", "cl_sync0", "l0_search", "l0_merge", "l0_done", "l1_search",
-         "l1_merge", "l1_done", "l2_search", "l2_merge", "l2_done", "-", "end", "end_sync"]
-for c in range(8):
-    print(json.dumps({names[s]: round((t[c][s] - t0) / 1e3, 2) for s in range(16) if t[c][s]}))
+names = {0: "start", 1: "bitonic", 2: "phase1", 3: "cl_sync0", 30: "end", 31: "end_sync"}
+for l in range(4):
+    names[4 + 3 * l], names[5 + 3 * l], names[6 + 3 * l] = f"l{l}_search", f"l{l}_copy", f"l{l}_done"
+for c in range(16):
+    if any(t[c]):
+        print(json.dumps({names.get(s, str(s)): round((t[c][s] - t0) / 1e3, 2)
+                          for s in range(32) if t[c][s]}))
