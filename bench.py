@@ -457,12 +457,12 @@ def choose_exchange(args, ms, comm, dist, dev, kin, kout, ws, stream, world, ran
     import torch
 
     if args.exchange == "alltoall":
-        ms.set_exchange_mode(0)
+        comm.set_exchange(0)
         return "alltoall"
     ok = 1
     err = None
     try:
-        ms.set_exchange_mode(1)
+        comm.set_exchange(1)  # this communicator only (include/msort.h msort_comm_set_exchange)
         comm.reserve(n, torch.int32, False, stream=stream)
         last_split[0] = ms.msort_sort_distributed_out(kin, kout, comm, ws=ws, stream=stream,
                                                       return_split=True)[2]
@@ -480,7 +480,7 @@ def choose_exchange(args, ms, comm, dist, dev, kin, kout, ws, stream, world, ran
         return "pull"
     if args.exchange == "pull":
         raise RuntimeError(f"pull exchange failed on some rank (here: {err})")
-    ms.set_exchange_mode(0)
+    comm.set_exchange(0)
     return "alltoall (pull check failed: %s)" % (err or "output mismatch on some rank")
 
 

@@ -215,7 +215,17 @@ msort_status msort_comm_wrap(void *nccl_comm, msort_comm_t *out);
  * or msort_comm_wrap (frees only the wrapper). */
 msort_status msort_comm_destroy(msort_comm_t comm);
 
-/* Reserve the pull exchange (msort_debug_set_exchange(1)) for calls with up to
+/* Exchange mode of the distributed calls on this communicator: 0 = the NCCL
+ * all-to-all + local k-way merge, 1 = the fused pull exchange (see
+ * msort_debug_set_exchange for both), -1 = the process default (the
+ * environment variable MSORT_EXCHANGE=pull or msort_debug_set_exchange; the
+ * initial value).  Every rank of the communicator must set the same mode
+ * (the two modes run different collectives).  Not synchronised with calls in
+ * flight on the communicator: set it between calls.  Errors:
+ * MSORT_ERROR_INVALID_VALUE for a null communicator or another mode. */
+msort_status msort_comm_set_exchange(msort_comm_t comm, int mode);
+
+/* Reserve the pull exchange (msort_comm_set_exchange(comm, 1)) for calls with up to
  * n_max local elements of these dtypes: the communicator allocates its
  * exchange buffer (cudaMalloc), publishes it through CUDA IPC and opens every
  * peer's, once.  Collective (every rank calls it; synchronises `stream`).

@@ -46,7 +46,7 @@ EXPORTED = (
     "msort_sort_distributed_tree", "msort_sort_distributed_tree_emulated",
     "msort_plan_tree_rounds", "msort_plan_tree_role", "msort_comm_wrap",
     "msort_merge_runs", "msort_merge_runs_workspace_bytes", "msort_debug_tile_sort",
-    "msort_comm_reserve", "msort_sort_distributed_host",
+    "msort_comm_reserve", "msort_sort_distributed_host", "msort_comm_set_exchange",
 )
 
 
@@ -76,6 +76,7 @@ def _load():
     L.msort_comm_destroy.argtypes = [vp]
     L.msort_comm_wrap.argtypes = [vp, c.POINTER(vp)]
     L.msort_comm_reserve.argtypes = [vp, sz, i32, i32, vp]
+    L.msort_comm_set_exchange.argtypes = [vp, i32]
     L.msort_sort_distributed_host.argtypes = [vp, vp, vp, vp, sz, i32, i32, vp, vp, vp, vp, sz, vp]
     L.msort_sort_distributed.argtypes = [vp, vp, sz, i32, i32, vp, vp, i64p]
     L.msort_sort_distributed_ws.argtypes = [vp, vp, sz, i32, i32, vp, vp, sz, vp, i64p]
@@ -445,6 +446,13 @@ class Comm:
         _check(lib.msort_comm_reserve(self.handle, int(n_max), _TORCH_DT[keys_dtype],
                                       MSORT_UINT32 if with_vals else MSORT_NONE,
                                       ctypes.c_void_p(_stream(stream))), "msort_comm_reserve")
+
+    def set_exchange(self, mode: int) -> None:
+        """Exchange mode of this communicator's distributed calls
+        (include/msort.h msort_comm_set_exchange): 0 NCCL all-to-all + k-way
+        merge, 1 fused pull exchange, -1 the process default.  Every rank
+        must set the same mode."""
+        _check(lib.msort_comm_set_exchange(self.handle, int(mode)), "msort_comm_set_exchange")
 
     def close(self):
         if self.handle:

@@ -22,6 +22,7 @@
 #include <cstring>
 #include <thread>
 #include <chrono>
+#include <atomic>
 #include <map>
 #include <string>
 #include <vector>
@@ -39,6 +40,7 @@ struct msort_comm_s {
   std::map<std::pair<int, std::string>, void*> ipc_open;
   bool aborted = false;  // set when a failure aborted the NCCL communicator
   bool owned = true;     // false: wraps a caller's communicator (never destroyed / aborted here)
+  int exchange = -1;     // exchange mode of this communicator (-1: the process default)
   // page-locked staging for the small host<->device copies of a call (split
   // matrix, sizes, IPC records): copies from/to pageable memory would block
   // the host inside cudaMemcpyAsync, out of reach of the failure detection
@@ -782,7 +784,8 @@ msort_status dist_nccl(const void* in_keys, const void* in_vals, void* keys, voi
     return MSORT_ERROR_NOT_SUPPORTED;
   }
   const bool pv = vd != MSORT_NONE;
-  const bool pull = exchange_mode() == 1 && comm->world > 1;
+  const int mode = comm->exchange >= 0 ? comm->exchange : exchange_mode();
+  const bool pull = mode == 1 && comm->world > 1;
   RankIO io{in_keys, pv ? in_vals : nullptr, keys, pv ? vals : nullptr, n,
             carve(ws, n, kd, vd, comm->world), nullptr, nullptr};
   io.sk = io.keys;
@@ -1121,15 +1124,22 @@ msort_status tree_emulated(const void* const* keys, const void* const* vals, con
   return tree_run(C, ranks, ik, iv, nall, kd, vd, root_k, root_v, s);
 }
 
-static int g_exchange_mode = -1;
+// Process default of the exchange mode (communicators may override it):
+// MSORT_EXCHANGE=pull, or msort_debug_set_exchange.  Atomic: a concurrent
+// call sees either the old or the new mode.
+static std::atomic<int> g_exchange_mode{-1};
 int exchange_mode() {
-  if (g_exchange_mode < 0) {
+  int m = g_exchange_mode.load(std::memory_order_acquire);
+  if (m < 0) {
     const char* e = getenv("MSORT_EXCHANGE");
-    g_exchange_mode = e && std::string(e) == "pull" ? 1 : 0;
+    m = e && std::string(e) == "pull" ? 1 : 0;
+    int expect = -1;
+    g_exchange_mode.compare_exchange_strong(expect, m, std::memory_order_acq_rel);
+    m = g_exchange_mode.load(std::memory_order_acquire);
   }
-  return g_exchange_mode;
+  return m;
 }
-void set_exchange_mode(int m) { g_exchange_mode = m; }
+void set_exchange_mode(int m) { g_exchange_mode.store(m, std::memory_order_release); }
 
 msort_status comm_unique_id(void* out) {
   ncclUniqueId id;
@@ -1210,5 +1220,14 @@ int comm_world(msort_comm_s* c) { return c->world; }
 extern "C" int msort_debug_set_exchange(int mode) {
   msort::set_exchange_mode(mode ? 1 : 0);
   return 0;
+}
+
+extern "C" msort_status msort_comm_set_exchange(msort_comm_t comm, int mode) {
+  if (!comm || mode < -1 || mode > 1) {
+    msort::set_error("msort_comm_set_exchange: null communicator or mode not in {-1, 0, 1}");
+    return MSORT_ERROR_INVALID_VALUE;
+  }
+  comm->exchange = mode;
+  return MSORT_SUCCESS;
 }
 

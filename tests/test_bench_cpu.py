@@ -81,6 +81,12 @@ class _FakeMs:
 
 
 class _FakeComm:
+    def __init__(self, ms):
+        self.ms = ms
+
+    def set_exchange(self, m):
+        self.ms.mode = m
+
     def reserve(self, n, keys_dtype=None, with_vals=False, stream=None):
         self.reserved = n
 
@@ -97,7 +103,7 @@ def _choose(monkeypatch, exchange, others, fail_sort=False):
     kout = torch.empty_like(kin)
     args = argparse.Namespace(exchange=exchange)
     last = [None]
-    got = mod.choose_exchange(args, ms, _FakeComm(), _FakeDist(others), "cpu", kin, kout, None,
+    got = mod.choose_exchange(args, ms, _FakeComm(ms), _FakeDist(others), "cpu", kin, kout, None,
                               None, 2, 0, kin.numel(), last)
     return got, ms.mode, last[0]
 

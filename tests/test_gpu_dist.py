@@ -221,7 +221,7 @@ def test_nccl_one_rank_reserve_pull(ms, orc):
     comm = ms.Comm()
     n = 70001
     comm.reserve(n)
-    ms.set_exchange_mode(1)
+    comm.set_exchange(1)  # per communicator (the process default stays 0)
     try:
         for seed in (1, 2):
             k = mi.keys(n - seed, 80 + seed, "i32")
@@ -229,8 +229,15 @@ def test_nccl_one_rank_reserve_pull(ms, orc):
             ms.msort_sort_distributed(kd, comm)
             torch.cuda.synchronize()
             assert np.array_equal(_host(kd, np.int32), orc.sort(k))
+        comm.set_exchange(-1)  # back to the process default
+        k = mi.keys(n, 83, "i32")
+        kd = _dev(k)
+        ms.msort_sort_distributed(kd, comm)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(kd, np.int32), orc.sort(k))
+        with pytest.raises(ms.MsortError):
+            comm.set_exchange(2)
     finally:
-        ms.set_exchange_mode(0)
         comm.close()
 
 

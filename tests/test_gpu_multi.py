@@ -113,7 +113,7 @@ def _worker(rank, p, port, outdir):
             cat = np.concatenate(ks)
             ek = oracle.sort(cat)
             comm.reserve(max(k.size for k in ks))
-            ms.set_exchange_mode(1)
+            comm.set_exchange(1)  # per communicator (msort_comm_set_exchange)
             for rep in range(3):
                 kd = torch.from_numpy(ks[rank].copy()).to(dev)
                 ms.msort_sort_distributed(kd, comm)
@@ -121,7 +121,7 @@ def _worker(rank, p, port, outdir):
                 a = rank * ks[0].size
                 if not np.array_equal(kd.cpu().numpy(), ek[a:a + ks[rank].size]):
                     fail(f"reserved pull rep {rep}: keys differ from the oracle slice")
-            ms.set_exchange_mode(0)
+            comm.set_exchange(-1)
         # the paper's rank tree (f4): rank 0 gathers everything
         for pairs in (False, True):
             ks, vs = _shards(p, "unequal")
