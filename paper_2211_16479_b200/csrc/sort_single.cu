@@ -456,6 +456,16 @@ extern "C" int msort_debug_k3_trace_clear() {
 #ifndef MSORT_K1_NT
 #define MSORT_K1_NT 128  // keys-only K1 threads (4-byte keys)
 #endif
+#ifndef MSORT_K1P_NT
+#define MSORT_K1P_NT 512  // pairs K1 threads, 4-byte keys (x 17 keys)
+#endif
+#ifndef MSORT_K1P8_NT
+// pairs K1 threads, 8-byte keys (x 17 keys): 256 (T = 4352, 70 KB of shared
+// memory, 3 CTAs/SM) -- C3 K1 1.98 -> 1.29 ms for one more merge level
+// (+0.24 ms): C3 5.36 -> 4.91 ms.  4-byte keys keep 512 (T = 8704): 256 gives
+// K1 2.13 -> 1.74 but a 15th level, C4 7.24 -> 7.20 (noise).
+#define MSORT_K1P8_NT 256
+#endif
 #ifndef MSORT_K1_VT
 #define MSORT_K1_VT 68  // keys-only K1 items per thread (NT x VT = 8704)
 #endif
@@ -596,7 +606,8 @@ struct Kernels {
   // (4-byte keys: 128 x 68 -- 1.53 ms vs 1.74 for 256 x 34 and 1.99 for 64 x
   // 136 on 2^28 int32; 8-byte keys keep 256 x 34: twice the registers per key)
   static constexpr int VT = PAIRS ? 17 : (sizeof(K) == 4 ? MSORT_K1_VT : 34);
-  static constexpr int NT1 = PAIRS ? 512 : (sizeof(K) == 4 ? MSORT_K1_NT : 256);
+  static constexpr int NT1 =
+      PAIRS ? (sizeof(K) == 8 ? MSORT_K1P8_NT : MSORT_K1P_NT) : (sizeof(K) == 4 ? MSORT_K1_NT : 256);
   static constexpr int T = NT1 * VT;  // tile sort size
   // 4-byte keys: 512 mergers x 17 = one 8704-key output tile (= T) per stage,
   // 2 CTAs/SM -- half the tiles (and co-rank searches) of 256 x 17, measured
