@@ -367,21 +367,27 @@ def configs_bench(ms, mi, dev, peak, reps=20):
         for _ in range(3):
             call()
         torch.cuda.synchronize()
-        ts = []
+        fits_l2 = n * (wk + wv) <= (64 << 20)  # C1, C2: flushed (the headline) and unflushed
+
+        def timed(do_flush):
+            ts_ = []
+            for _ in range(reps):
+                if do_flush:
+                    flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                call()
+                e1.record()
+                e1.synchronize()
+                ts_.append(e0.elapsed_time(e1))
+            return sorted(ts_)
+
+        unflushed = timed(False) if fits_l2 else None
         ms.profile_reset()
         ms.profile_enable(True)
-        for _ in range(reps):
-            if n * (wk + wv) < (64 << 20):
-                flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            call()
-            e1.record()
-            e1.synchronize()
-            ts.append(e0.elapsed_time(e1))
+        ts = timed(fits_l2)
         ms.profile_enable(False)
         prof = ms.profile_read()
-        ts.sort()
         med = ts[len(ts) // 2]
         kd = {4: ms.MSORT_INT32, 8: ms.MSORT_INT64}[wk]
         T = ms.tile_size(kd, ms.MSORT_UINT32 if pairs else ms.MSORT_NONE)
@@ -410,7 +416,9 @@ def configs_bench(ms, mi, dev, peak, reps=20):
              "step_roofline": {"passes": levels + 1, "t_roof_ms": round(t_roof, 4),
                                "frac": round(t_roof / med, 4),
                                "floor_frac": round(per_pass / (peak * 1e9) * 1e3 / med, 4)},
-             "l2_flush": n * (wk + wv) < (64 << 20), "verified": ok}
+             "l2_flush": fits_l2, "verified": ok}
+        if unflushed:
+            d["ms_unflushed"] = round(unflushed[len(unflushed) // 2], 4)
         if name == "C1":
             s = torch.cuda.Stream(device=dev)
             g = torch.cuda.CUDAGraph()
