@@ -510,7 +510,7 @@ __device__ __forceinline__ int64_t corank_warp(const Src& src, int pass, int64_t
 
 constexpr int kK3Extra = 96;  // producer, searcher and store warps
 #ifndef MSORT_SEARCH_PL
-#define MSORT_SEARCH_PL 1
+#define MSORT_SEARCH_PL 2  // 1: +1% on 2^24-2^26 (profiles/r02/c2/pl_ab.log); 8: spills, slower
 #endif
 constexpr int kSearchPL = MSORT_SEARCH_PL;  // probes per lane per round (group searches)
 
