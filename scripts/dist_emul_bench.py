@@ -38,17 +38,23 @@ for p in [int(x) for x in a.ps.split(",")]:
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
+            if rep == 2:
+                ms.profile_reset()
+                ms.profile_enable(True)
             e0.record()
             ms.msort_sort_distributed_emulated(kd)
             e1.record()
             e1.synchronize()
+            if rep == 2:
+                ms.profile_enable(False)
+                phases = {k: round(v[1], 3) for k, v in ms.profile_read().items() if v[0]}
             if rep >= 2:
                 ts.append(e0.elapsed_time(e1))
         ok = all(bool((k[1:] >= k[:-1]).all()) for k in kd)
         med = statistics.median(ts)
         print(json.dumps({"p": p, "n_per_rank": n, "mode": ["alltoall", "pull"][mode],
                           "ms_all_ranks": round(med, 3), "ms_per_rank": round(med / p, 3),
-                          "sorted": ok}), flush=True)
+                          "phases_ms_all_ranks": phases, "sorted": ok}), flush=True)
         del kd
     ms.set_exchange_mode(0)
     # the paper's rank-tree gather (all data ends on the root)
