@@ -624,14 +624,20 @@ struct Kernels {
 #ifndef MSORT_K3_S
 #define MSORT_K3_S 3
 #endif
-  static constexpr int S = WIDE3 ? MSORT_K3_S : (WIDE8 ? 2 : 3);  // stage ring depth
+#ifndef MSORT_K3P_S
+#define MSORT_K3P_S 3  // 4-byte keys + payload
+#endif
+#ifndef MSORT_K3P_MINB
+#define MSORT_K3P_MINB 2
+#endif
+  static constexpr int S = WIDE3 ? MSORT_K3_S : (WIDE8 ? 2 : MSORT_K3P_S);  // stage ring depth
   using LY = K3Layout<K, PAIRS, NC, VT3, S>;
   // CTAs per SM the register budget is tuned for (shared memory allows 4 for
   // 4-byte keys without payload, 2-3 otherwise)
 #ifndef MSORT_K3_MINB
 #define MSORT_K3_MINB 2
 #endif
-  static constexpr int MINB = WIDE3 ? MSORT_K3_MINB : (WIDE8 ? 1 : 2);  // CTAs/SM for registers
+  static constexpr int MINB = WIDE3 ? MSORT_K3_MINB : (WIDE8 ? 1 : MSORT_K3P_MINB);  // CTAs/SM for registers
   static constexpr size_t k1_smem =
       PAIRS ? (size_t)T * sizeof(K) + (size_t)T * 8 : K1KeysShape<K, NT1, VT>::smem;
   static constexpr size_t k3_smem = LY::bytes;
