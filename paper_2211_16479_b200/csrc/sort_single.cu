@@ -618,11 +618,14 @@ struct Kernels {
   // CTA/SM (C3: 4.25 -> 3.67 ms of merging); 4-byte keys with a payload keep
   // 256 mergers and three stages (512 x 2 stages: C4 5.40 -> 6.10 ms).
   static constexpr bool WIDE8 = sizeof(K) == 8;
-  static constexpr int NC = WIDE3 ? MSORT_K3_NC : (WIDE8 ? 512 : 256);
+  static constexpr int NC = WIDE3 ? MSORT_K3_NC : (WIDE8 ? 512 : MSORT_K3P_NC);
   static constexpr int VT3 = PAIRS ? 17 : MSORT_K3_VT;
   static constexpr int Tm = NC * VT3;  // merge output tile (divides 2T)
 #ifndef MSORT_K3_S
 #define MSORT_K3_S 3
+#endif
+#ifndef MSORT_K3P_NC
+#define MSORT_K3P_NC 256  // 4-byte keys + payload: mergers per CTA
 #endif
 #ifndef MSORT_K3P_S
 #define MSORT_K3P_S 3  // 4-byte keys + payload
