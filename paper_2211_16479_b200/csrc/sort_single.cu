@@ -456,6 +456,9 @@ extern "C" int msort_debug_k3_trace_clear() {
 #ifndef MSORT_K1_NT
 #define MSORT_K1_NT 128  // keys-only K1 threads (4-byte keys)
 #endif
+#ifndef MSORT_K3P_NC
+#define MSORT_K3P_NC 256  // 4-byte keys + payload: mergers per CTA
+#endif
 #ifndef MSORT_K1P_NT
 #define MSORT_K1P_NT 512  // pairs K1 threads, 4-byte keys (x 17 keys)
 #endif
@@ -623,9 +626,6 @@ struct Kernels {
   static constexpr int Tm = NC * VT3;  // merge output tile (divides 2T)
 #ifndef MSORT_K3_S
 #define MSORT_K3_S 3
-#endif
-#ifndef MSORT_K3P_NC
-#define MSORT_K3P_NC 256  // 4-byte keys + payload: mergers per CTA
 #endif
 #ifndef MSORT_K3P_S
 #define MSORT_K3P_S 3  // 4-byte keys + payload
