@@ -155,18 +155,20 @@ static msort_status check_device() {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  // cache per device id (small fixed table)
-  static int cached_major[64], cached_minor[64];
-  static bool cached[64] = {};
-  if (dev < 64 && cached[dev]) {
-    major = cached_major[dev];
-    minor = cached_minor[dev];
+  // cache per device id (small fixed table; one atomic word per device:
+  // 0 = unknown, else 1 + major * 64 + minor -- calls may come from many threads)
+  static std::atomic<int> cached[64];
+  const int c = dev < 64 ? cached[dev].load(std::memory_order_acquire) : 0;
+  if (c) {
+    major = (c - 1) / 64;
+    minor = (c - 1) % 64;
   } else {
-    cudaDeviceProp p;
-    e = cudaGetDeviceProperties(&p, dev);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
-    major = p.major, minor = p.minor;
-    if (dev < 64) cached_major[dev] = major, cached_minor[dev] = minor, cached[dev] = true;
+    int ma = 0, mi = 0;
+    e = cudaDeviceGetAttribute(&ma, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&mi, cudaDevAttrComputeCapabilityMinor, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    major = ma, minor = mi;
+    if (dev < 64) cached[dev].store(1 + major * 64 + minor, std::memory_order_release);
   }
   if (major != 10 || minor != 0) {
     set_error("device is sm_" + std::to_string(major) + std::to_string(minor) +

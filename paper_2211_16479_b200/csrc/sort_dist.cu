@@ -105,11 +105,10 @@ struct NcclGroup {
 // MSORT_NCCL_TIMEOUT_S seconds (environment, default 0 = no timeout), abort
 // the communicator (it is unusable afterwards) and return MSORT_ERROR_NCCL.
 static msort_status wait_stream_nccl(msort_comm_s* c, cudaStream_t s, const char* what) {
-  static double limit = -1.0;
-  if (limit < 0) {
+  static const double limit = [] {  // read once (thread-safe static initialisation)
     const char* e = getenv("MSORT_NCCL_TIMEOUT_S");
-    limit = e ? atof(e) : 0.0;
-  }
+    return e ? atof(e) : 0.0;
+  }();
   const auto t0 = std::chrono::steady_clock::now();
   for (unsigned spin = 0;; ++spin) {
     const cudaError_t q = cudaStreamQuery(s);

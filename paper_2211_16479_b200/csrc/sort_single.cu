@@ -660,15 +660,18 @@ struct Kernels {
   static int64_t k6_units_max(int64_t n) { return n / kK6XS + n / (4 * (int64_t)T) + 2; }
   static_assert(kK6XS >= 3998, "msort_workspace_bytes sizes the K6 area for XS >= 3998");
   static int64_t k6_extra_max(int64_t n) { return n / kK6YS + k6_units_max(n) + 1; }
-  static int& k6_grid(int dev) {
-    static int g[64] = {};
+  // Per-device grid sizes, set once by init() / k6_init() (release) and read
+  // by any thread (acquire): 0 = not initialised on that device yet.
+  static std::atomic<int>& k6_grid_slot(int dev) {
+    static std::atomic<int> g[64];
     return g[dev & 63];
   }
-
-  static int& grid3(int dev) {
-    static int g[64] = {};
+  static int k6_grid(int dev) { return k6_grid_slot(dev).load(std::memory_order_acquire); }
+  static std::atomic<int>& grid3_slot(int dev) {
+    static std::atomic<int> g[64];
     return g[dev & 63];
   }
+  static int grid3(int dev) { return grid3_slot(dev).load(std::memory_order_acquire); }
 
   // Tiles per scheduled chunk for a level of `tiles` output tiles: kChunk
   // when every CTA gets >= 2 full chunks per level (few searches, long bulk
@@ -727,7 +730,7 @@ struct Kernels {
       set_error("merge pass kernel does not fit on an SM");
       return MSORT_ERROR_NOT_SUPPORTED;
     }
-    grid3(dev) = sms * occ;
+    grid3_slot(dev).store(sms * occ, std::memory_order_release);
     return MSORT_SUCCESS;
   }
 
@@ -742,7 +745,7 @@ struct Kernels {
       MSORT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       MSORT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o6, k6, K6S::NT1,
                                                                    K6S::KEYS * sizeof(K)));
-      k6_grid(dev) = sms * std::max(o6, 1);
+      k6_grid_slot(dev).store(sms * std::max(o6, 1), std::memory_order_release);
     }
     return MSORT_SUCCESS;
   }
