@@ -33,6 +33,28 @@
 
 namespace msort {
 
+// VT outputs of the stable merge of A (from ai) and B (from bi) in s, ties to
+// A, with the in-tile index of each output gathered through src_idx; no end
+// checks -- the caller guarantees neither run ends within VT steps.
+template <class K, int VT>
+__device__ __forceinline__ void merge_pairs_nocheck(const K* s, const int* src_idx, int ai, int bi,
+                                                    K (&key)[VT], int (&idx)[VT]) {
+  K ak = s[ai], bk = s[bi];
+#pragma unroll
+  for (int k = 0; k < VT; ++k) {
+    const bool takeB = bk < ak;
+    key[k] = takeB ? bk : ak;
+    idx[k] = src_idx[takeB ? bi : ai];
+    ai += takeB ? 0 : 1;
+    bi += takeB ? 1 : 0;
+    if (k + 1 < VT) {
+      const K nv = s[takeB ? bi : ai];
+      ak = takeB ? ak : nv;
+      bk = takeB ? nv : bk;
+    }
+  }
+}
+
 // ----------------------------------------------------------------- K1
 // NT threads x VT items (VT odd: "blocked" shared accesses at stride VT are
 // bank-conflict free without padding).
@@ -116,8 +138,13 @@ __global__ void __launch_bounds__(NT)
     }
     int i = merge_path<K, false>(sk, g0, w, g0 + w, w, d);
     if constexpr (PAIRS) {
-      serial_merge<K, false, true, VT>(sk, si, g0 + i, g0 + w, g0 + w + d - i, g0 + 2 * w, T - 1,
-                                       key, idx);
+      const int ai = g0 + i, bi = g0 + w + d - i;
+      // check-free steps when no lane's run can end within VT outputs (the
+      // common case), else the checked merge
+      if (__all_sync(0xffffffffu, ai + VT <= g0 + w && bi + VT <= g0 + 2 * w))
+        merge_pairs_nocheck<K, VT>(sk, si, ai, bi, key, idx);
+      else
+        serial_merge<K, false, true, VT>(sk, si, ai, g0 + w, bi, g0 + 2 * w, T - 1, key, idx);
     } else {
       serial_merge_fast<K, false, VT>(sk, g0 + i, g0 + w, g0 + w + d - i, g0 + 2 * w, T - 1,
                                       key, idx);
