@@ -141,22 +141,50 @@ __global__ void k4_init(uint64_t* lohi, int nb, uint64_t umax) {
   if (r < nb) lohi[2 * r] = 0, lohi[2 * r + 1] = umax;
 }
 
-// cnt[r*B + b] = #{x in local shard : image(x) <= candidate b of boundary r}
+// First index i of the sorted shard keys[0, n) with image(keys[i]) > c
+// (UPPER: the count of keys <= c) or >= c (lower: the count of keys < c), by
+// one warp: each round probes 32 evenly spaced candidates of [lo, hi) and
+// keeps the bucket where the monotone predicate turns true -- log32(n)
+// dependent rounds of global-memory probes instead of log2(n) (the splitter
+// rounds are latency-bound; D2 is latency-bound).
+template <class K, bool UPPER>
+__device__ __forceinline__ int64_t warp_bound(const K* __restrict__ keys, int64_t n, uint64_t c,
+                                              int lane) {
+  int64_t lo = 0, hi = n;
+  while (hi > lo) {
+    const int64_t span = hi - lo;
+    const int64_t step = (span + 31) >> 5;
+    const int64_t off = step * (lane + 1);
+    const int64_t p = lo + (off < span ? off : span) - 1;
+    const uint64_t x = (uint64_t)KeyTraits<K>::image(__ldg(keys + p));
+    const bool past = UPPER ? x > c : x >= c;
+    const unsigned m = __ballot_sync(0xffffffffu, past);
+    if (m == 0) {
+      lo = hi;
+    } else {
+      const int f = __ffs(m) - 1;
+      const int64_t pf = __shfl_sync(0xffffffffu, p, f);
+      const int64_t pp = __shfl_sync(0xffffffffu, p, f > 0 ? f - 1 : 0);
+      hi = pf;
+      if (f > 0) lo = pp + 1;
+    }
+  }
+  return lo;
+}
+
+// cnt[r*B + b] = #{x in local shard : image(x) <= candidate b of boundary r};
+// one warp per (boundary, candidate)
 template <class K>
 __global__ void __launch_bounds__(256)
     k4_count(const K* __restrict__ keys, int64_t n, const uint64_t* __restrict__ lohi, int nb,
              uint64_t* __restrict__ cnt) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nb * B) return;
-  int r = t / B, b = t % B;
-  uint64_t c = plan::candidate(lohi[2 * r], lohi[2 * r + 1], b, B);
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {  // upper bound in image space (images are monotone in key order)
-    int64_t mid = (lo + hi) >> 1;
-    if ((uint64_t)KeyTraits<K>::image(__ldg(keys + mid)) <= c) lo = mid + 1;
-    else hi = mid;
-  }
-  cnt[t] = (uint64_t)lo;
+  const int t = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= nb * B) return;  // warp-uniform
+  const int r = t / B, b = t % B;
+  const uint64_t c = plan::candidate(lohi[2 * r], lohi[2 * r + 1], b, B);
+  const int64_t lo = warp_bound<K, true>(keys, n, c, lane);
+  if (lane == 0) cnt[t] = (uint64_t)lo;
 }
 
 // One thread per boundary r = 1..world-1: narrow [lo, hi] from the global counts.
@@ -171,22 +199,19 @@ __global__ void k4_narrow(uint64_t* lohi, const uint64_t* __restrict__ total,
   lohi[2 * r] = lo, lohi[2 * r + 1] = hi;
 }
 
-// (lt, eq) of the local shard at v*_r = lo_r (= hi_r after the last round).
+// (lt, eq) of the local shard at v*_r = lo_r (= hi_r after the last round);
+// one warp per bound
 template <class K>
 __global__ void k4_lteq(const K* __restrict__ keys, int64_t n, const uint64_t* __restrict__ lohi,
                         int nb, uint64_t* __restrict__ lteq) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 2 * nb) return;
-  int r = t / 2, upper = t % 2;
-  uint64_t v = lohi[2 * r];
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    uint64_t x = (uint64_t)KeyTraits<K>::image(__ldg(keys + mid));
-    if (upper ? x <= v : x < v) lo = mid + 1;
-    else hi = mid;
-  }
-  lteq[t] = (uint64_t)lo;  // t even: lower bound (lt); odd: upper bound (le)
+  const int t = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= 2 * nb) return;  // warp-uniform
+  const int r = t / 2, upper = t % 2;
+  const uint64_t v = lohi[2 * r];
+  const int64_t lo = upper ? warp_bound<K, true>(keys, n, v, lane)
+                           : warp_bound<K, false>(keys, n, v, lane);
+  if (lane == 0) lteq[t] = (uint64_t)lo;  // t even: lower bound (lt); odd: upper bound (le)
 }
 
 // le -> eq in place after the gather would need a pass; instead convert locally
@@ -567,14 +592,14 @@ struct EmulColl {
 
 template <class K>
 static void launch_count(const RankIO& io, int nb, cudaStream_t s) {
-  int tot = nb * B;
-  k4_count<K><<<(tot + 255) / 256, 256, 0, s>>>((const K*)io.sk, (int64_t)io.n, io.ws.lohi, nb,
-                                                io.ws.cnt);
+  const int warps = nb * B;  // one warp per search
+  k4_count<K><<<(warps + 7) / 8, 256, 0, s>>>((const K*)io.sk, (int64_t)io.n, io.ws.lohi, nb,
+                                              io.ws.cnt);
 }
 template <class K>
 static void launch_lteq(const RankIO& io, int nb, cudaStream_t s) {
-  k4_lteq<K><<<(2 * nb + 255) / 256, 256, 0, s>>>((const K*)io.sk, (int64_t)io.n, io.ws.lohi,
-                                                  nb, io.ws.lteq);
+  k4_lteq<K><<<(2 * nb + 7) / 8, 256, 0, s>>>((const K*)io.sk, (int64_t)io.n, io.ws.lohi,
+                                              nb, io.ws.lteq);
 }
 
 static int rounds_for(msort_dtype kd) { return dtype_size(kd) == 4 ? 4 : 8; }
