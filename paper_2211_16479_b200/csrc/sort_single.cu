@@ -483,6 +483,9 @@ extern "C" int msort_debug_k3_trace_clear() {
 #ifndef MSORT_K1_NT
 #define MSORT_K1_NT 128  // keys-only K1 threads (4-byte keys)
 #endif
+#ifndef MSORT_K3P_VT
+#define MSORT_K3P_VT 17  // 4-byte keys + payload: outputs per merger
+#endif
 #ifndef MSORT_K3P_NC
 #define MSORT_K3P_NC 256  // 4-byte keys + payload: mergers per CTA
 #endif
@@ -649,7 +652,7 @@ struct Kernels {
   // 256 mergers and three stages (512 x 2 stages: C4 5.40 -> 6.10 ms).
   static constexpr bool WIDE8 = sizeof(K) == 8;
   static constexpr int NC = WIDE3 ? MSORT_K3_NC : (WIDE8 ? 512 : MSORT_K3P_NC);
-  static constexpr int VT3 = PAIRS ? 17 : MSORT_K3_VT;
+  static constexpr int VT3 = PAIRS ? (sizeof(K) == 4 ? MSORT_K3P_VT : 17) : MSORT_K3_VT;
   static constexpr int Tm = NC * VT3;  // merge output tile (divides 2T)
 #ifndef MSORT_K3_S
 #define MSORT_K3_S 3
