@@ -136,6 +136,13 @@ struct PeerPairs {
 #endif
 constexpr int kChunk = MSORT_K3_CHUNK;  // tiles per dynamically scheduled chunk
 constexpr int kGrab = MSORT_K3_GRAB;    // chunks taken per atomic
+#ifndef MSORT_K3_RING1
+#define MSORT_K3_RING1 2
+#endif
+// chunk-descriptor ring slots when a grab is one chunk (the searcher may run
+// kRing1 - 1 chunks ahead of the producer); <= the 2 * kGrab slots allocated
+constexpr int kRing1 = MSORT_K3_RING1;
+static_assert(kRing1 >= 2 && kRing1 <= 2 * kGrab, "ring of single-chunk grabs");
 constexpr int kMaxFusedPasses = 48;
 
 struct TileMeta {
@@ -520,7 +527,7 @@ __global__ void __launch_bounds__(NC + kK3Extra, MINB)
   using LY = K3Layout<K, PAIRS, NC, VT, S>;
   constexpr int Tm = LY::Tm, EK = LY::EK, CH = kChunk;
   const int G = src.grab;  // chunks per grab (<= kGrab); chunk ring of R = 2G slots
-  const int R = 2 * G;
+  const int R = G == 1 ? kRing1 : 2 * G;
   constexpr int NW = (NC + kK3Extra) / 32;  // warps per CTA
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + LY::bars);
