@@ -144,15 +144,16 @@ __global__ void __launch_bounds__(kK0NT, 1)
   while (CP2 < Q) CP2 *= 2;
   const bool active = tid * VT < CP2;  // this thread holds keys of the padded chunk
   if constexpr (SHFL) {
-    // warp w takes keys [512 w, 512 (w + 1)), lane-striped loads
-    if (warp * 32 * VT < CP2) {
+    // warp w takes keys [32 VT w, 32 VT (w + 1)), lane-striped loads.  Every
+    // warp runs the network (warps past the chunk sort MAX padding): in
+    // convergent code the shuffles need no per-shuffle WARPSYNC /
+    // ENDCOLLECTIVE, which a warp-dependent branch around them costs.
 #pragma unroll
-      for (int k = 0; k < VT; ++k) {
-        const int i = warp * 32 * VT + k * 32 + lane;
-        key[k] = i < len ? in[base + i] : KeyTraits<K>::max_key();
-      }
-      warp_bitonic_keys<VT>(key, lane);
+    for (int k = 0; k < VT; ++k) {
+      const int i = warp * 32 * VT + k * 32 + lane;
+      key[k] = i < len ? in[base + i] : KeyTraits<K>::max_key();
     }
+    warp_bitonic_keys<VT>(key, lane);
     k0_mark(1);
   } else {
 #pragma unroll

@@ -186,9 +186,14 @@ __global__ void __launch_bounds__(128)
   const int64_t d = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   if (d >= cnt) return;
   const int64_t base = desc[2 * d];
+  // the segment length as a ballot (a warp-uniform value the compiler can see
+  // as such): the network chosen by it runs in convergent code, so its
+  // shuffles need no per-shuffle WARPSYNC / ENDCOLLECTIVE
   const int len = (int)desc[2 * d + 1];
-  if (len <= 64) warp_sort_segment<K, PAIRS, 2>(keys, vals, base, len, lane);
-  else if (len <= 128) warp_sort_segment<K, PAIRS, 4>(keys, vals, base, len, lane);
+  const unsigned cls = __ballot_sync(0xffffffffu, lane == 0 ? len > 64 : false) |
+                       (__ballot_sync(0xffffffffu, lane == 0 ? len > 128 : false) << 1);
+  if (cls == 0) warp_sort_segment<K, PAIRS, 2>(keys, vals, base, len, lane);
+  else if (cls == 1) warp_sort_segment<K, PAIRS, 4>(keys, vals, base, len, lane);
   else warp_sort_segment<K, PAIRS, 8>(keys, vals, base, len, lane);
 }
 
