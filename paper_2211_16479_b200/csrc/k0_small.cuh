@@ -57,23 +57,28 @@ constexpr int kK0MaxCL = MSORT_K0_MAXCL;  // cluster size (> 8: non-portable, B2
 constexpr int64_t kK0MaxN = (int64_t)kK0MaxCL * kK0Chunk;  // 65536 = 2^16
 static_assert(kK0MaxN >= 65536, "K0 covers C1 (2^16 keys)");
 
-// Shared-memory buffers are padded (one spare word per 128 bytes, sidx):
-// a thread's VT = 16 consecutive keys then sit in distinct banks across a
-// warp's lanes (blocked stores are conflict-free).
+// Shared-memory buffers are plain arrays of kK0Chunk keys plus slack: a
+// thread's VT keys leave as 16-byte vector stores, and the cross-cluster
+// window copies move 16-byte vectors (a chunk holds Q keys, Q a multiple of
+// the vector width, so no vector straddles two chunks).
 template <class K>
 constexpr int k0_padded() {
-  return padded_len<K, kK0Chunk>();
+  return kK0Chunk + 16;
+}
+template <class K>
+constexpr int k0_vec() {
+  return 16 / (int)sizeof(K);
 }
 
 // VT outputs [d, d + VT) of merge(A, B) into key[] (ties to A); A = s[a0, a0+na),
-// B = s[b0, b0+nb) (logical indices into a padded buffer), s[0..lim] addressable.
+// B = s[b0, b0+nb), s[0..lim] addressable.
 template <class K, int VT>
 __device__ __forceinline__ void k0_merge_thread(const K* s, int a0, int na, int b0, int nb, int d,
                                                 int lim, K (&key)[VT]) {
-  const int i = merge_path<K, true>(s, a0, na, b0, nb, d);
+  const int i = merge_path<K, false>(s, a0, na, b0, nb, d);
   int pos[VT];
-  serial_merge<K, true, false, VT>(s, nullptr, a0 + i, a0 + na, b0 + d - i, b0 + nb, lim, key,
-                                   pos);
+  serial_merge<K, false, false, VT>(s, nullptr, a0 + i, a0 + na, b0 + d - i, b0 + nb, lim, key,
+                                    pos);
 }
 
 // Key g of the cluster's global view (chunk g / Q, offset g % Q); n <= 2^16
@@ -81,7 +86,7 @@ __device__ __forceinline__ void k0_merge_thread(const K* s, int a0, int na, int 
 template <class K>
 __device__ __forceinline__ K k0_at(const K* const* chunk, int Q, int g) {
   const int c = g / Q;
-  return chunk[c][sidx<K, true>(g - c * Q)];
+  return chunk[c][g - c * Q];
 }
 
 template <class K>
@@ -127,7 +132,8 @@ __global__ void __launch_bounds__(kK0NT, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = blockIdx.x;
   const int N = (int)n;  // <= 2^16
-  const int Q = (N + CL - 1) / CL;
+  constexpr int EK = k0_vec<K>();
+  const int Q = ((N + CL - 1) / CL + EK - 1) / EK * EK;  // keys per chunk, whole vectors
   const int base = c * Q;
   const int len = N - base <= 0 ? 0 : min(Q, N - base);
   // the chunk's sort only spans the warps / rounds that hold real keys:
@@ -166,7 +172,7 @@ __global__ void __launch_bounds__(kK0NT, 1)
   int cur = 0;
   if (active) {
 #pragma unroll
-    for (int k = 0; k < VT; ++k) buf[0][sidx<K, true>(tid * VT + k)] = key[k];
+    store_vec<K, VT>(buf[0] + tid * VT, key);
   }
 #pragma unroll 1
   for (int w = w0; w < CP2; w *= 2) {
@@ -175,16 +181,14 @@ __global__ void __launch_bounds__(kK0NT, 1)
       const K* src = buf[cur];
       const int d0 = tid * VT, g0 = d0 / (2 * w) * (2 * w);
       k0_merge_thread<K, VT>(src, g0, w, g0 + w, w, d0 - g0, CP2 - 1, key);
-      K* dst = buf[cur ^ 1];
-#pragma unroll
-      for (int k = 0; k < VT; ++k) dst[sidx<K, true>(d0 + k)] = key[k];
+      store_vec<K, VT>(buf[cur ^ 1] + d0, key);
     }
     cur ^= 1;
   }
   k0_mark(2);
   if (CL == 1) {
     __syncthreads();
-    for (int i = tid; i < len; i += NT) out[base + i] = buf[cur][sidx<K, true>(i)];
+    for (int i = tid; i < len; i += NT) out[base + i] = buf[cur][i];
     return;
   }
   // ---- 2. merge levels across the cluster (DSMEM)
@@ -212,28 +216,26 @@ __global__ void __launch_bounds__(kK0NT, 1)
     const int i0 = (int)s_co[0], i1 = (int)s_co[1];
     const int la = i1 - i0, lb = len - la;
     const int j0 = d0 - i0;
-    // the two windows, from the peers: A[i0, i1) then B[j0, j0 + lb)
+    // the two windows, from the peers: A[i0, i1) then B[j0, j0 + lb), as
+    // 16-byte vectors (the vectors holding them; a vector never straddles
+    // two chunks).  In win each window keeps its global phase mod EK: A at
+    // pa = ga mod EK, B at pb = (first vector after A) * EK + gb mod EK.
+    const int ga = a_start + i0, gb = b_start + j0;
+    const int pa = ga % EK;
+    const int wb = la > 0 ? (pa + la + EK - 1) / EK : 0;  // first win vector of B
+    const int pb = wb * EK + gb % EK;
     {
-      // all VT loads of a thread in flight at once (DSMEM latency), then
-      // stores.  Each window (<= Q keys) spans at most two chunks: the chunk
-      // of its first key and the next, so a compare replaces the divisions.
-      const int ga = a_start + i0, gb = b_start + j0;
+      const int va0 = ga / EK, nva = la > 0 ? (ga + la + EK - 1) / EK - va0 : 0;
+      const int vb0 = gb / EK, nvb = lb > 0 ? (gb + lb + EK - 1) / EK - vb0 : 0;
       const int ca = ga / Q, cb = gb / Q;
       const int ea = (ca + 1) * Q, eb = (cb + 1) * Q;  // first key of the next chunk
-      K v[VT];
-#pragma unroll
-      for (int k = 0; k < VT; ++k) {
-        const int e = tid + k * NT;
-        const bool inA = e < la;
-        const int g = inA ? ga + e : gb + (e - la);
+      for (int e = tid; e < nva + nvb; e += NT) {
+        const bool inA = e < nva;
+        const int g = (inA ? va0 + e : vb0 + (e - nva)) * EK;
         const int c0 = inA ? ca : cb;
         const int c1 = g < (inA ? ea : eb) ? c0 : c0 + 1;
-        if (e < len) v[k] = chunk[c1][sidx<K, true>(g - c1 * Q)];
-      }
-#pragma unroll
-      for (int k = 0; k < VT; ++k) {
-        const int e = tid + k * NT;
-        if (e < len) win[sidx<K, true>(e)] = v[k];
+        const uint4 v = *reinterpret_cast<const uint4*>(chunk[c1] + (g - c1 * Q));
+        *reinterpret_cast<uint4*>(win + (inA ? e : wb + (e - nva)) * EK) = v;
       }
     }
     __syncthreads();
@@ -241,17 +243,21 @@ __global__ void __launch_bounds__(kK0NT, 1)
     const bool last = 2 * span >= CL;
     const int d = tid * VT;
     if (d < len) {
-      k0_merge_thread<K, VT>(win, 0, la, la, lb, d, max(len - 1, 0), key);
+      k0_merge_thread<K, VT>(win, pa, la, pb, lb, d, CP - 1, key);
       const int e = min(VT, len - d);
       K* dst = buf[cur ^ 1];
+      if (e == VT) {
+        store_vec<K, VT>(dst + d, key);
+      } else {
 #pragma unroll
-      for (int k = 0; k < VT; ++k)
-        if (k < e) dst[sidx<K, true>(d + k)] = key[k];
+        for (int k = 0; k < VT; ++k)
+          if (k < e) dst[d + k] = key[k];
+      }
     }
     if (last) {  // the sorted slice leaves by coalesced stores
       __syncthreads();
       const K* o = buf[cur ^ 1];
-      for (int i = tid; i < len; i += NT) out[base + i] = o[sidx<K, true>(i)];
+      for (int i = tid; i < len; i += NT) out[base + i] = o[i];
       break;
     }
     cur ^= 1;
