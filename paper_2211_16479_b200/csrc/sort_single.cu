@@ -973,29 +973,53 @@ struct Kernels {
   }
 
   // ---- K0: n <= kK0MaxN keys in one launch (k0_small.cuh) -------------
-  // MSORT_K0 (environment): 0 disables K0, 2 selects its A/B variant
-  // without the warp-shuffle network
+  // MSORT_K0 (environment): 0 disables K0; 1 (default) the one-step
+  // multiway cluster merge; 3 the pairwise cluster levels (round-2 A/B
+  // variant); 2 the pairwise levels without the warp-shuffle network
   static int k0_mode() {
     const char* e = getenv("MSORT_K0");
-    return e && *e ? atoi(e) : 1;
+    const int m = e && *e ? atoi(e) : 1;
+    return m < 0 || m > 3 ? 1 : m;
   }
   static bool k0_enabled() { return k0_mode() != 0; }
-  template <bool SHFL>
-  static msort_status k0_attr(int dev, size_t smem) {
+  template <bool SHFL, bool MW>
+  static msort_status k0_attr(int dev) {
     static std::atomic<bool> done[64];
     if (!done[dev & 63].load(std::memory_order_acquire)) {
-      MSORT_CUDA_TRY(cudaFuncSetAttribute(k0_small_sort<K, SHFL>,
+      constexpr size_t smem = (size_t)k0_smem_keys<K, MW>() * sizeof(K);
+      MSORT_CUDA_TRY(cudaFuncSetAttribute(k0_small_sort<K, SHFL, MW>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       if (kK0MaxCL > 8)
-        MSORT_CUDA_TRY(cudaFuncSetAttribute(k0_small_sort<K, SHFL>,
+        MSORT_CUDA_TRY(cudaFuncSetAttribute(k0_small_sort<K, SHFL, MW>,
                                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       done[dev & 63].store(true, std::memory_order_release);
     }
     return MSORT_SUCCESS;
   }
+  template <bool SHFL, bool MW>
+  static bool k0_fits16(int dev) {
+    if (k0_attr<SHFL, MW>(dev) != MSORT_SUCCESS) return false;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)kK0MaxCL, 1, 1);
+    cfg.blockDim = dim3(kK0NT, 1, 1);
+    cfg.dynamicSmemBytes = (size_t)k0_smem_keys<K, MW>() * sizeof(K);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)kK0MaxCL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    const bool ok = cudaOccupancyMaxActiveClusters(&nc, k0_small_sort<K, SHFL, MW>, &cfg) ==
+                        cudaSuccess && nc > 0;
+    cudaGetLastError();  // a refused query is not an error of this call
+    return ok;
+  }
   // Largest n K0 takes on this device: kK0MaxN when a cluster of kK0MaxCL
   // CTAs (16: non-portable) is schedulable, else what 8 CTAs hold (the
-  // general path takes the rest).  Queried once per device.
+  // general path takes the rest).  Queried once per device (every variant
+  // is checked, so the limit does not depend on MSORT_K0).
   static int64_t k0_limit() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
@@ -1003,40 +1027,26 @@ struct Kernels {
     int64_t v = lim[dev & 63].load(std::memory_order_acquire);
     if (v) return v;
     v = (int64_t)std::min(kK0MaxCL, 8) * kK0Chunk;
-    constexpr size_t smem = 3 * (size_t)k0_padded<K>() * sizeof(K);
-    if (kK0MaxCL > 8 && k0_attr<true>(dev, smem) == MSORT_SUCCESS) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)kK0MaxCL, 1, 1);
-      cfg.blockDim = dim3(kK0NT, 1, 1);
-      cfg.dynamicSmemBytes = smem;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = (unsigned)kK0MaxCL;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      int nc = 0;
-      if (cudaOccupancyMaxActiveClusters(&nc, k0_small_sort<K, true>, &cfg) == cudaSuccess &&
-          nc > 0)
-        v = kK0MaxN;
-      cudaGetLastError();  // a refused query is not an error of this call
-    }
+    if (kK0MaxCL > 8 && k0_fits16<true, true>(dev) && k0_fits16<true, false>(dev) &&
+        k0_fits16<false, false>(dev))
+      v = kK0MaxN;
     lim[dev & 63].store(v, std::memory_order_release);
     return v;
   }
   static msort_status small_sort(const K* in, K* out, int64_t n, cudaStream_t s) {
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
-    constexpr size_t smem = 3 * (size_t)k0_padded<K>() * sizeof(K);
-    const bool shfl = k0_mode() != 2;
-    MSORT_TRY(shfl ? k0_attr<true>(dev, smem) : k0_attr<false>(dev, smem));
+    const int mode = k0_mode();
+    if (mode == 2) MSORT_TRY((k0_attr<false, false>(dev)));
+    else if (mode == 3) MSORT_TRY((k0_attr<true, false>(dev)));
+    else MSORT_TRY((k0_attr<true, true>(dev)));
     int CL = 1;
     while ((int64_t)CL * kK0Chunk < n) CL *= 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)CL, 1, 1);
     cfg.blockDim = dim3(kK0NT, 1, 1);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes =
+        (size_t)(mode == 1 ? k0_smem_keys<K, true>() : k0_smem_keys<K, false>()) * sizeof(K);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1047,8 +1057,12 @@ struct Kernels {
     cfg.numAttrs = CL > 1 ? 1 : 0;
     {
       LaunchScope ls(KC_TILE_SORT, s);
-      if (shfl) MSORT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k0_small_sort<K, true>, in, out, n, CL));
-      else MSORT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k0_small_sort<K, false>, in, out, n, CL));
+      if (mode == 2)
+        MSORT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k0_small_sort<K, false, false>, in, out, n, CL));
+      else if (mode == 3)
+        MSORT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k0_small_sort<K, true, false>, in, out, n, CL));
+      else
+        MSORT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k0_small_sort<K, true, true>, in, out, n, CL));
     }
     return MSORT_SUCCESS;
   }
