@@ -16,11 +16,14 @@
 //      its own samples among all CL sample lists (a local copy), and the
 //      sample of merged rank t*g starts output tile t (K5's sample-bounded
 //      tiles, k5_kway.cuh: a tile never exceeds S(g + CL) - CL keys); CTA t
-//      finds its tile's exact start/end STATE per chunk by one 32-lane DSMEM
-//      probe round inside the S keys between two samples, copies its CL
-//      windows in and merges them in log2(CL) in-CTA rounds (K5's engine),
+//      finds its tile's exact start/end STATE per chunk by one DSMEM probe
+//      round (16 lanes x 2) inside the S keys between two samples, copies its
+//      CL windows in (16-byte DSMEM vectors) and merges them in log2(CL)
+//      in-CTA rounds (K5's engine, ping-pong buffers, one barrier per round),
 //      writing HBM from the last round.  Three cluster barriers in all, the
 //      last one split (arrive after the window copies, wait before exit).
+//      C1 (2^16 int32): 26.6 -> 22.0 us per CUDA-graph replay against the
+//      pairwise levels (profiles/r02/k0mw/).
 //      The round-2 variant (MW = false, MSORT_K0=3): log2(CL) pairwise merge
 //      levels across the cluster -- co-ranks by 32-ary DSMEM searches, the
 //      two windows copied in, a per-thread merge, one cluster barrier per level.
