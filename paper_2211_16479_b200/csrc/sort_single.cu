@@ -974,12 +974,15 @@ struct Kernels {
 
   // ---- K0: n <= kK0MaxN keys in one launch (k0_small.cuh) -------------
   // MSORT_K0 (environment): 0 disables K0; 1 (default) the one-step
-  // multiway cluster merge; 3 the pairwise cluster levels (round-2 A/B
-  // variant); 2 the pairwise levels without the warp-shuffle network
+  // multiway cluster merge for clusters of 4 or more CTAs and the pairwise
+  // cluster level below (2^13 keys: 14.4 vs 16.4 us, profiles/r02/k0mw/);
+  // 4 the multiway step at every cluster size; 3 the pairwise cluster levels
+  // (round-2 A/B variant); 2 the pairwise levels without the warp-shuffle
+  // network
   static int k0_mode() {
     const char* e = getenv("MSORT_K0");
     const int m = e && *e ? atoi(e) : 1;
-    return m < 0 || m > 3 ? 1 : m;
+    return m < 0 || m > 4 ? 1 : m;
   }
   static bool k0_enabled() { return k0_mode() != 0; }
   template <bool SHFL, bool MW>
@@ -1036,17 +1039,18 @@ struct Kernels {
   static msort_status small_sort(const K* in, K* out, int64_t n, cudaStream_t s) {
     int dev = 0;
     MSORT_CUDA_TRY(cudaGetDevice(&dev));
-    const int mode = k0_mode();
+    int CL = 1;
+    while ((int64_t)CL * kK0Chunk < n) CL *= 2;
+    int mode = k0_mode();
+    if (mode == 1) mode = CL >= 4 ? 4 : 3;
     if (mode == 2) MSORT_TRY((k0_attr<false, false>(dev)));
     else if (mode == 3) MSORT_TRY((k0_attr<true, false>(dev)));
     else MSORT_TRY((k0_attr<true, true>(dev)));
-    int CL = 1;
-    while ((int64_t)CL * kK0Chunk < n) CL *= 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)CL, 1, 1);
     cfg.blockDim = dim3(kK0NT, 1, 1);
     cfg.dynamicSmemBytes =
-        (size_t)(mode == 1 ? k0_smem_keys<K, true>() : k0_smem_keys<K, false>()) * sizeof(K);
+        (size_t)(mode == 4 ? k0_smem_keys<K, true>() : k0_smem_keys<K, false>()) * sizeof(K);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

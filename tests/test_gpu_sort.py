@@ -269,6 +269,19 @@ def test_small_cluster_sort_structured(ms, orc, dist):
             check_parity(ms, orc, _keys(n, 7, dist, dtype), None)
 
 
+@pytest.mark.parametrize("mode", ["2", "3", "4"])
+def test_small_cluster_sort_variants(ms, orc, mode, monkeypatch):
+    """Every K0 variant at every cluster size (MSORT_K0 is read per call):
+    4 = the one-step multiway cluster merge also for 2-CTA clusters (the
+    default uses it from 4 CTAs on), 3 = pairwise cluster levels, 2 = the
+    same without the warp-shuffle network."""
+    monkeypatch.setenv("MSORT_K0", mode)
+    for i, n in enumerate([4097, 6000, 8192, 8193, 16384, 24577, 32768, 40000, 65535, 65536]):
+        for dtype in (np.int32, np.uint64):
+            for dist in ("rand", "dup", "eq", "desc"):
+                check_parity(ms, orc, _keys(n, 300 + i, dist, dtype), None)
+
+
 def test_small_cluster_sort_c1_out_of_place_and_graph(ms, orc):
     """C1 (2^16 int32, seed 0) out of place, then captured in a CUDA graph and
     replayed on new data: bit-exact every time."""
