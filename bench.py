@@ -211,6 +211,46 @@ def cpu_paper_mp(n_sample: int, seed: int = SEED0 + 200):
                       f"(oracle/msort_oracle.c msort_oracle_paper_mp), {t:.1f} s"}
 
 
+def configs_cpu(per_config):
+    """SURVEY §8(d) O-1 and O-c on BASELINE.json's configs 1-4, beside the GPU
+    numbers of `configs`: the oracle as it stands (single-threaded top-down
+    merge sort; min of 3 for C1/C2, one run for C3/C4) and the paper's
+    multiprocessing merge sort on all host cores (min of 3), on the same
+    seeded inputs (keys + index payload for C3/C4).  Rank 0, N = 1 only."""
+    import msort_inputs as mi
+    import oracle
+
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    for name in ("C1", "C2", "C3", "C4"):
+        d = per_config["results"].get(name)
+        if d is None:
+            continue
+        k0, v0 = mi.config_input(name)
+        n = k0.size
+
+        def run(fn, reps):
+            best = None
+            for _ in range(reps):
+                k = k0.copy()
+                v = v0.copy() if v0 is not None else None
+                t0 = time.perf_counter()
+                fn(k, v)
+                t = time.perf_counter() - t0
+                best = t if best is None else min(best, t)
+            return best
+
+        t1 = run(lambda k, v: oracle.sort_inplace(k, v), 3 if n <= (1 << 24) else 1)
+        tc = run(lambda k, v: oracle.paper_mp_inplace(k, v, cores), 3)
+        d["cpu_oracle"] = {"ms": round(t1 * 1e3, 3), "keys_per_s": n / t1, "cores": 1,
+                           "kind": "oracle", "reps": 3 if n <= (1 << 24) else 1}
+        d["cpu_paper_mp"] = {"ms": round(tc * 1e3, 3), "keys_per_s": n / tc, "cores": cores,
+                             "kind": "oracle_paper_mp", "reps": 3}
+        d["gpu_over_oracle"] = round(t1 * 1e3 / d["ms"], 1)
+        d["gpu_over_paper_mp"] = round(tc * 1e3 / d["ms"], 1)
+    per_config["cpu_model"] = cpu_model()
+
+
 def reference_arm(args, rank):
     """--impl reference: the CPU oracle on a bounded sample per step."""
     if rank != 0:
@@ -392,6 +432,9 @@ def configs_bench(ms, mi, dev, peak, reps=20):
         kd = {4: ms.MSORT_INT32, 8: ms.MSORT_INT64}[wk]
         T = ms.tile_size(kd, ms.MSORT_UINT32 if pairs else ms.MSORT_NONE)
         levels = ((n + T - 1) // T - 1).bit_length()
+        k0 = not pairs and n <= 65536  # K0: the whole sort in one cluster launch, one HBM pass
+        if k0:
+            levels = 0
         per_pass = 2 * n * (wk + wv)
         mp_l, mp_ms = prof["merge_pass"]
         roof = None
@@ -410,7 +453,8 @@ def configs_bench(ms, mi, dev, peak, reps=20):
                 ok &= host_digest(vout.view(torch.int32).cpu().numpy()) == exp["vals_sha256"]
         d = {"n": n, "key": str(kin.dtype).replace("torch.", ""), "payload": "uint32 index" if pairs
              else None, "ms": round(med, 4), "min_ms": round(ts[0], 4),
-             "keys_per_s": n / (med / 1e3), "tile": T, "merge_levels": levels,
+             "keys_per_s": n / (med / 1e3), "tile": "K0 cluster (16 x 4096)" if k0 else T,
+             "merge_levels": levels,
              "phases_ms": {k2: round(v[1] / reps, 4) for k2, v in prof.items() if v[0]},
              "roofline": roof,
              "step_roofline": {"passes": levels + 1, "t_roof_ms": round(t_roof, 4),
@@ -790,6 +834,8 @@ def main():
     if rank == 0 and not dpath and not args.no_cpu_baseline:
         cpu = cpu_baseline(n, 1, SEED0)       # O-1 on the full rank-0 shard
         cpu_mp = cpu_paper_mp(n, SEED0)       # O-c on the same shard, all host cores
+        if per_config is not None:
+            configs_cpu(per_config)           # O-1 / O-c on configs 1-4
 
     if rank == 0:
         value = world * n * args.steps / (ms_total / 1e3)
