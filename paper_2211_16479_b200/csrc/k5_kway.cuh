@@ -64,11 +64,12 @@ __device__ __forceinline__ const K5Runs& k5r(const K5Runs& r) { return r; }
 __device__ __forceinline__ const K5Runs& k5r(const K5Runs* r) { return *r; }
 
 // Shape of the merge CTA: NT threads x VT keys per thread and round;
-// capacity C = (NT - P2 / 2) * VT keys for P2 (p rounded up to a power of
-// two) runs, so that a round's ceil(len / VT) threads per pair fit in NT.
+// capacity C = (31 NT / 32 - P2 / 2) * VT keys for P2 (p rounded up to a
+// power of two) runs, so that a round's ceil(len / VT) output threads per
+// pair fit in the 31 output lanes of each warp.
 template <int NT, int VT>
 struct K5Shape {
-  static constexpr int cap(int P2) { return (NT - P2 / 2) * VT; }
+  static constexpr int cap(int P2) { return (NT / 32 * 31 - P2 / 2) * VT; }  // 31 output threads per warp
   // keys of shared memory: capacity + per-run slack (<= 3 phase + 2
   // sentinels + 3 rounding) + guard
   static constexpr int keys(int P2) { return cap(P2) + 8 * P2 + 16; }
@@ -307,13 +308,17 @@ __global__ void k5_plan_dev(K5Geo* __restrict__ G, const int64_t* __restrict__ s
 
 // ---------------------------------------------------------------- merge
 // One CTA per tile; P2 = p rounded up to a power of two (runs p..P2-1 are
-// empty), R = log2(P2) rounds.  The whole round structure is laid out once
-// by thread 0 (sizes are known from the tile's states): round r has P2 >> r
-// runs; run i of round r = the merge of runs 2i, 2i+1 of round r-1; round
-// r's pair m = (run 2m = A, run 2m+1 = B) sits in shared memory as
-// [MIN | B | MAX .. MIN | A | MAX] (B below A: merge_keys_dual clamps A at
-// its MAX and B at its MIN sentinel with one bound each); its threads are
-// [tp[r][m], tp[r][m+1]), one per VT outputs.
+// empty), R = log2(P2) rounds: round r has P2 >> r runs; run i of round r =
+// the merge of runs 2i, 2i+1 of round r-1; round r's pair m = (run 2m = A,
+// run 2m+1 = B) sits in shared memory as [MIN | B | MAX .. MIN | A | MAX]
+// (B below A: merge_keys_dual clamps A at its MAX and B at its MIN sentinel
+// with one bound each).  The layout is computed with warp shuffles (lane j =
+// run j; sizes from the tile's states): warp 0 lays out round 0, arms the
+// barrier and issues the window copies, while warps 1.. lay out the later
+// rounds and the thread ranges under the copies' latency.  Output thread
+// o = 31 warp + lane (lanes 0..30) merges VT outputs; lane 31 only searches
+// the co-rank at the next warp's first diagonal, so every thread's end
+// co-rank is its neighbour's start (a shuffle): two barriers per round.
 template <class K, int NT, int VT, int MINB, int P2, class RS>
 __global__ void __launch_bounds__(NT, MINB)
     k5_merge(const __grid_constant__ RS Rin, const int64_t* __restrict__ states,
@@ -321,18 +326,19 @@ __global__ void __launch_bounds__(NT, MINB)
   const K5Runs& R = k5r(Rin);
   if ((int64_t)blockIdx.x >= R.ntiles) return;  // upper-bound grid (device-planned)
   constexpr int RR = __builtin_ctz(P2);  // rounds
+  constexpr int NW = NT / 32;
+  static_assert(NW >= 2 && P2 <= 32, "a layout warp besides warp 0; one lane per run");
   constexpr uint32_t Z = sizeof(K);
+  constexpr unsigned F = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem[];
   K* sk = reinterpret_cast<K*>(smem);
   const char* sb = reinterpret_cast<const char*>(smem);
   __shared__ uint64_t bar;
   __shared__ int s_len[RR + 1][P2];     // run sizes per round (round RR: the tile)
-  __shared__ int s_off[RR + 1][P2];     // run offsets (keys) per round; RR: the output phase
-  __shared__ int s_tp[RR][P2 / 2 + 1];  // first thread of each pair per round
-  __shared__ int cr[NT + 1];            // co-ranks of the threads' first diagonals
+  __shared__ int s_off[RR][P2];         // run offsets (keys) per round
+  __shared__ int s_tp[RR][P2 / 2 + 1];  // first output thread of each pair per round
   __shared__ int64_t s_src[P2];
-  __shared__ int64_t s_out;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int p = R.p;
   const int64_t t = blockIdx.x;
 
@@ -340,105 +346,103 @@ __global__ void __launch_bounds__(NT, MINB)
     mbar_init(&bar, 32);
     fence_mbar_init();
   }
-  if (tid < P2) {
-    int64_t a = 0, b = 0;
-    if (tid < p) a = states[t * p + tid], b = states[(t + 1) * p + tid];
-    s_src[tid] = a;
-    s_len[0][tid] = (int)(b - a);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    // round 0: windows at their global 16-byte phase (TMA), MIN slot before
-    int o = 0;
-    for (int m = 0; m < P2 / 2; ++m) {
+  auto scan_excl = [&](int v) {  // exclusive prefix over lanes 0..P2-1
+    int inc = v;
 #pragma unroll
-      for (int h = 1; h >= 0; --h) {
-        const int j = 2 * m + h;
-        const int ph = j < p ? stage_offset(static_cast<const K*>(R.k[j]) + s_src[j]) : 0;
-        const int at = ((o + 4) & ~3) + ph;
-        s_off[0][j] = at;
-        o = at + s_len[0][j] + 1;
-      }
+    for (int d = 1; d < P2; d <<= 1) {
+      const int x = __shfl_up_sync(F, inc, d);
+      if (lane >= d) inc += x;
     }
-    int64_t out = 0;
-    for (int j = 0; j < p; ++j) out += s_src[j];
-    s_out = out;
-    // rounds 1..RR-1: 16-byte aligned runs (a full thread's outputs leave as
-    // vectors); round RR (the output) at the destination's 16-byte phase
+    return inc - v;
+  };
+  // every warp: lane j < p holds run j's window [a, b) of this tile
+  int64_t a = 0, b = 0;
+  if (lane < p) a = states[t * p + lane], b = states[(t + 1) * p + lane];
+  const int l0 = (int)(b - a);
+  int64_t out = a;
 #pragma unroll
-    for (int r = 1; r <= RR; ++r) {
-      int o2 = 0;
-      const int nr = P2 >> r;
-      for (int q = 0; q < (nr + 1) / 2; ++q) {
+  for (int d = 1; d < P2; d <<= 1) out += __shfl_xor_sync(F, out, d);
+  out = __shfl_sync(F, out, 0);  // lanes 0..P2-1 summed their group
+  const int sh = stage_offset(dst + out);  // the output's 16-byte phase
+  __syncthreads();  // barrier initialised
+  if (warp == 0) {
+    const K* g = lane < p ? static_cast<const K*>(R.k[lane]) + a : nullptr;
+    const int ph = lane < p ? stage_offset(g) : 0;
+    const int fp = lane < P2 ? (ph + l0 + 8) & ~3 : 0;  // MIN slot, phase, run, MAX, rounding
+    const int base = __shfl_sync(F, scan_excl(__shfl_sync(F, fp, lane ^ 1)), lane ^ 1);
+    const int o0 = base + 4 + ph;
+    uint32_t tx = lane < p ? window_bulk_bytes(g, l0) : 0u;
 #pragma unroll
-        for (int h = 1; h >= 0; --h) {
-          const int j = 2 * q + h;
-          if (j >= nr) continue;
-          s_len[r][j] = s_len[r - 1][2 * j] + s_len[r - 1][2 * j + 1];
-          const int at = (o2 + 4) & ~3;
-          s_off[r][j] = at;
-          o2 = at + s_len[r][j] + 1;
+    for (int d = 1; d < P2; d <<= 1) tx += __shfl_xor_sync(F, tx, d);
+    if (lane < P2) {
+      s_off[0][lane] = o0;
+      s_len[0][lane] = l0;
+      s_src[lane] = a;
+      sk[o0 - 1] = KeyTraits<K>::min_key();
+      sk[o0 + l0] = KeyTraits<K>::max_key();
+    }
+    if (lane == 0) mbar_expect_tx(&bar, tx);
+    __syncwarp();
+    for (int j = 0; j < p; ++j)
+      stage_window(sk + s_off[0][j], static_cast<const K*>(R.k[j]) + s_src[j], s_len[0][j], &bar,
+                   lane == 0, lane, 32);
+    mbar_arrive(&bar);
+  } else {
+    for (int r = warp - 1; r < RR; r += NW - 1) {
+      // run j of round r = runs [j 2^r, (j+1) 2^r) of round 0: group sums by
+      // xor-reduction, gathered from the group's first lane
+      int gs = l0;
+      for (int d = 1; d < (1 << r); d <<= 1) gs += __shfl_xor_sync(F, gs, d);
+      const int gs2 = gs + __shfl_xor_sync(F, gs, 1 << r);
+      const int nr = P2 >> r, np = nr / 2;
+      const int l = __shfl_sync(F, gs, (lane << r) & 31);
+      const int l2 = __shfl_sync(F, gs2, (lane << (r + 1)) & 31);
+      if (r > 0) {
+        const int fp = lane < nr ? (l + 8) & ~3 : 0;
+        const int base = __shfl_sync(F, scan_excl(__shfl_sync(F, fp, lane ^ 1)), lane ^ 1);
+        if (lane < nr) {
+          s_off[r][lane] = base + 4;
+          s_len[r][lane] = l;
         }
       }
-    }
-    s_off[RR][0] = stage_offset(dst + out);
-#pragma unroll
-    for (int r = 0; r < RR; ++r) {
-      int tp = 0;
-      const int np = P2 >> (r + 1);
-      // the last round's diagonals are shifted by the output phase ph
-      // (thread k: [k VT - ph, (k+1) VT - ph)), so every full thread's
+      // the last round's diagonals are shifted by the output phase sh
+      // (thread k: [k VT - sh, (k+1) VT - sh)), so every full thread's
       // outputs start 16-byte aligned in the phase-matched output buffer
-      const int sh = r + 1 == RR ? s_off[RR][0] : 0;
-      for (int m = 0; m < np; ++m) {
-        s_tp[r][m] = tp;
-        tp += (s_len[r + 1][m] + sh + VT - 1) / VT;
-      }
-      s_tp[r][np] = tp;
+      const int shr = r + 1 == RR ? sh : 0;
+      const int cnt = lane < np ? (l2 + shr + VT - 1) / VT : 0;
+      const int tp = scan_excl(cnt);
+      if (lane < np) s_tp[r][lane] = tp;
+      if (lane == np - 1) s_tp[r][np] = tp + cnt;
+      if (r + 1 == RR && lane == 0) s_len[RR][0] = l2;
     }
-    uint32_t tx = 0;
-    for (int j = 0; j < p; ++j)
-      tx += window_bulk_bytes(static_cast<const K*>(R.k[j]) + s_src[j], s_len[0][j]);
-    mbar_expect_tx(&bar, tx);
   }
-  __syncthreads();
-  if (tid < P2) {
-    sk[s_off[0][tid] - 1] = KeyTraits<K>::min_key();
-    sk[s_off[0][tid] + s_len[0][tid]] = KeyTraits<K>::max_key();
-  }
-  if (tid < 32) {
-    for (int j = 0; j < p; ++j) {
-      const K* g = static_cast<const K*>(R.k[j]) + s_src[j];
-      stage_window(sk + s_off[0][j], g, s_len[0][j], &bar, tid == 0, tid, 32);
-    }
-    mbar_arrive(&bar);
-  }
+  __syncthreads();  // layout and round-0 sentinels visible
   mbar_wait(&bar, 0);
-  __syncthreads();  // sentinels written by other threads
 
   K key[VT];
   const int tot = s_len[RR][0];
+  const int o = warp * 31 + lane;
 #pragma unroll 1
   for (int r = 0; r < RR; ++r) {
     const int npair = P2 >> (r + 1);
     int m = 0;
 #pragma unroll
     for (int q = 1; q < P2 / 2; ++q)
-      if (q < npair && s_tp[r][q] <= tid) m = q;
-    const bool act = tid < s_tp[r][npair];
+      if (q < npair && s_tp[r][q] <= o) m = q;
+    const bool in = o < s_tp[r][npair];
     const int la = s_len[r][2 * m], lb = s_len[r][2 * m + 1], len = la + lb;
     const uint32_t oa = (uint32_t)s_off[r][2 * m] * Z, ob = (uint32_t)s_off[r][2 * m + 1] * Z;
-    const int sh = r + 1 == RR ? s_off[RR][0] : 0;  // output phase (last round)
+    const int shr = r + 1 == RR ? sh : 0;
     int d = 0, c = 0, i0 = 0;
-    if (act) {
-      d = max(0, (tid - s_tp[r][m]) * VT - sh);
-      c = min((tid - s_tp[r][m] + 1) * VT - sh, len) - d;
+    if (in) {
+      d = max(0, (o - s_tp[r][m]) * VT - shr);
+      c = min((o - s_tp[r][m] + 1) * VT - shr, len) - d;
       i0 = merge_path_off<K>(sb, oa, la, ob, lb, d);
-      cr[tid] = i0;
     }
-    __syncthreads();
+    const int nx = __shfl_down_sync(F, i0, 1);
+    const bool act = in && lane < 31;
     if (act) {
-      const int i1 = d + c == len ? la : cr[tid + 1];
+      const int i1 = d + c == len ? la : nx;
       merge_keys_dual<K, VT>(sb, oa + (uint32_t)i0 * Z, oa + (uint32_t)la * Z,
                              ob + (uint32_t)(d - i0) * Z, oa + (uint32_t)i1 * Z,
                              ob + (uint32_t)(d + c - i1) * Z, ob - Z, key);
@@ -458,17 +462,16 @@ __global__ void __launch_bounds__(NT, MINB)
   fence_proxy_async_smem();
   __syncthreads();
   if (tid < 32) {
-    const int ph = s_off[RR][0];
-    K* go = dst + s_out;
+    K* go = dst + out;
     int h, mid;
     window_split(go, tot, h, mid);
     if (tid == 0 && mid) {
-      bulk_s2g(go + h, sk + ph + h, (uint32_t)(mid * sizeof(K)));
+      bulk_s2g(go + h, sk + sh + h, (uint32_t)(mid * sizeof(K)));
       bulk_commit();
     }
     for (int i = tid; i < tot - mid; i += 32) {
       const int j = i < h ? i : i + mid;
-      go[j] = sk[ph + j];
+      go[j] = sk[sh + j];
     }
     if (tid == 0 && mid) bulk_wait_read<0>();  // shared memory must outlive the copy's reads
   }
