@@ -394,10 +394,11 @@ const char *msort_last_error(void);
  * launching stream.  msort_profile_read synchronises those events and
  * returns, per kernel class (0 tile_sort, 1 partition, 2 merge_pass,
  * 3 splitter, 4 kway_merge, 5 NCCL collectives, 6 the D3 exchange -- the
- * all-to-all of the sorted segments, or its emulation), the launch count
- * and total device milliseconds since the last reset.  Host arrays of
+ * all-to-all of the sorted segments, or its emulation, 7 key_range -- the
+ * range / narrow / widen passes of 8-byte-key sorts), the launch count and
+ * total device milliseconds since the last reset.  Host arrays of
  * MSORT_PROFILE_CLASSES. */
-#define MSORT_PROFILE_CLASSES 7
+#define MSORT_PROFILE_CLASSES 8
 void msort_profile_enable(int on);
 void msort_profile_reset(void);
 msort_status msort_profile_read(int64_t *launches, double *ms);

@@ -21,9 +21,9 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MSORT_LIB") or os.path.join(_PKG, "lib", "libmsort.so")
 
 MSORT_INT32, MSORT_UINT32, MSORT_INT64, MSORT_UINT64, MSORT_NONE = 0, 1, 2, 3, 255
-MSORT_PROFILE_CLASSES = 7
+MSORT_PROFILE_CLASSES = 8
 PROFILE_CLASS_NAMES = ("tile_sort", "partition", "merge_pass", "splitter", "kway_merge", "nccl",
-                       "exchange")
+                       "exchange", "key_range")
 
 _TORCH_DT = {torch.int32: MSORT_INT32, torch.int64: MSORT_INT64}
 if hasattr(torch, "uint32"):

@@ -132,7 +132,16 @@ size_t dtype_size(msort_dtype d) {
   }
 }
 
+static size_t single_ws_bytes_w(size_t n, msort_dtype kd, msort_dtype vd);
 size_t single_ws_bytes(size_t n, msort_dtype kd, msort_dtype vd) {
+  if (dtype_size(kd) != 8) return single_ws_bytes_w(n, kd, vd);
+  // 8-byte keys: room for the key-range narrowed sort too (sort_narrowed:
+  // 32-bit keys + the 4-byte sort's workspace, overlapping the 8-byte sort's)
+  // and the range itself in the last 256 bytes
+  const size_t nar = align_up(n * 4, 256) + single_ws_bytes_w(n, MSORT_UINT32, vd);
+  return std::max(single_ws_bytes_w(n, kd, vd), nar) + 256;
+}
+static size_t single_ws_bytes_w(size_t n, msort_dtype kd, msort_dtype vd) {
   const int T = tile_size_for(kd, vd);
   size_t b = align_up(n * dtype_size(kd), 256);
   if (vd != MSORT_NONE) b += align_up(n * 4, 256);

@@ -266,6 +266,10 @@ struct FusedPasses {
   int grab;        // chunks per atomic grab (1..kGrab)
   unsigned* done;  // per level, per pair: tiles completed
   int64_t pair_base[kMaxFusedPasses + 1];
+  // key-range gate (Kernels::sort_narrowed): with gate set the launch does
+  // nothing unless range_narrow(gate) == gate_want
+  const unsigned long long* gate;
+  int gate_want;
   __device__ __forceinline__ int64_t cpp() const { return (ntiles + ch - 1) / ch; }
   __device__ __forceinline__ int64_t nchunks() const { return (int64_t)P * cpp(); }
   __device__ __forceinline__ void chunk(int64_t g, int& pass, int64_t& q0, int& cnt) const {
@@ -521,9 +525,19 @@ constexpr int kK3Extra = 96;  // producer, searcher and store warps
 #endif
 constexpr int kSearchPL = MSORT_SEARCH_PL;  // probes per lane per round (group searches)
 
+template <class Src>
+__device__ __forceinline__ bool k3_gated_off(const Src&) {
+  return false;
+}
+template <class K>
+__device__ __forceinline__ bool k3_gated_off(const FusedPasses<K>& f) {
+  return f.gate && (int)range_narrow(f.gate) != f.gate_want;
+}
+
 template <class K, bool PAIRS, int NC, int VT, int S, int MINB, class Src>
 __global__ void __launch_bounds__(NC + kK3Extra, MINB)
     k3_merge_pass(const __grid_constant__ Src src, unsigned long long* __restrict__ ctr) {
+  if (k3_gated_off(src)) return;
   using LY = K3Layout<K, PAIRS, NC, VT, S>;
   constexpr int Tm = LY::Tm, EK = LY::EK, CH = kChunk;
   const int G = src.grab;  // chunks per grab (<= kGrab); chunk ring of R = 2G slots

@@ -43,6 +43,17 @@ struct KeyTraits<uint64_t> {
   static __host__ __device__ __forceinline__ U image(uint64_t x) { return x; }
 };
 
+// Key-range narrowing of 8-byte keys (Kernels::sort_narrowed): mm[0] / mm[1]
+// = the smallest / largest order-preserving image of a sort's keys.  The
+// keys are sorted as 32-bit offsets from mm[0] when they span < 2^32 values.
+__device__ __forceinline__ bool range_narrow(const unsigned long long* mm) {
+  return mm[1] - mm[0] <= 0xffffffffull;
+}
+template <class K>
+__host__ __device__ __forceinline__ K key_from_image(unsigned long long u) {
+  return sizeof(K) == 8 && K(-1) < K(0) ? (K)(u ^ 0x8000000000000000ull) : (K)u;
+}
+
 // Shared-memory padding: one spare word per 128 bytes, so that "blocked"
 // accesses (thread t touches VT consecutive elements) are conflict-free.
 template <class K, bool PAD>

@@ -28,7 +28,7 @@ msort_status cuda_fail(cudaError_t e, const char* what);
 
 // ------------------------------------------------------ kernel accounting
 enum KernelClass { KC_TILE_SORT = 0, KC_PARTITION = 1, KC_MERGE = 2, KC_SPLITTER = 3,
-                   KC_KWAY = 4, KC_NCCL = 5, KC_EXCHANGE = 6 };
+                   KC_KWAY = 4, KC_NCCL = 5, KC_EXCHANGE = 6, KC_KEY_RANGE = 7 };
 
 // Bracket a kernel launch: counts it, and when profiling is on records a
 // pair of CUDA events on the launching stream.

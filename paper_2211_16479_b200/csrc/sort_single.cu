@@ -62,7 +62,9 @@ template <class K, bool PAIRS, int NT, int VT>
 __global__ void __launch_bounds__(NT)
     k1_tile_sort(const K* __restrict__ in_k, const uint32_t* __restrict__ in_v,
                  K* __restrict__ out_k, uint32_t* __restrict__ out_v, int64_t n,
-                 const int64_t* __restrict__ seg) {
+                 const int64_t* __restrict__ seg, const unsigned long long* __restrict__ gate = nullptr,
+                 int gate_want = 0) {
+  if (gate && (int)range_narrow(gate) != gate_want) return;  // key-range gate (sort_narrowed)
   constexpr int T = NT * VT;
   extern __shared__ __align__(16) unsigned char smem[];
   K* sk = reinterpret_cast<K*>(smem);                 // T keys
@@ -327,7 +329,9 @@ struct K1KeysShape {
 template <class K, int NT, int VT, bool SHFL = false>
 __global__ void __launch_bounds__(NT)
     k1_tile_sort_keys(const K* __restrict__ in_k, K* __restrict__ out_k, int64_t n,
-                      const int64_t* __restrict__ seg) {
+                      const int64_t* __restrict__ seg,
+                      const unsigned long long* __restrict__ gate = nullptr, int gate_want = 0) {
+  if (gate && (int)range_narrow(gate) != gate_want) return;  // key-range gate (sort_narrowed)
   using SH = K1KeysShape<K, NT, VT>;
   static_assert(VT % VecOf<K>::W == 0, "keys-only K1 stores 16-byte vectors");
   constexpr int T = SH::T;
@@ -806,8 +810,12 @@ struct Kernels {
 
   // Sort in_k/in_v into out_k/out_v (in == out: in place; K1 reads a whole
   // tile into shared memory before writing it back, so that is safe).
+  // gate / gate_want: the key-range gate of sort_narrowed (every launch of
+  // this sort does nothing unless range_narrow(gate) == gate_want); the
+  // caller guarantees n > kK0MaxN, so no K0, and K6 is not used.
   static msort_status sort(const K* in_k, const uint32_t* in_v, K* keys, uint32_t* vals,
-                           size_t n, void* ws, size_t ws_bytes, cudaStream_t s) {
+                           size_t n, void* ws, size_t ws_bytes, cudaStream_t s,
+                           const unsigned long long* gate = nullptr, int gate_want = 0) {
     MSORT_TRY(init());
     if (n < 2) {
       if (n == 1 && in_k != keys) {
@@ -832,7 +840,7 @@ struct Kernels {
     int nq = 0;
     int64_t Lq = T;
     if constexpr (!PAIRS) {
-      if (k6_mode()) {
+      if (k6_mode() && !gate) {
         MSORT_TRY(k6_init(dev));
         nq = passes / 2, Lq = (int64_t)T << (2 * nq);
       }
@@ -864,10 +872,11 @@ struct Kernels {
       if constexpr (PAIRS)
         k1_tile_sort<K, PAIRS, NT1, VT>
             <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, in_v, bk[cur], bv[cur], (int64_t)n,
-                                                     nullptr);
+                                                     nullptr, gate, gate_want);
       else
         k1_tile_sort_keys<K, NT1, VT>
-            <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, bk[cur], (int64_t)n, nullptr);
+            <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in_k, bk[cur], (int64_t)n, nullptr, gate,
+                                                     gate_want);
     }
     MSORT_CUDA_TRY(cudaGetLastError());
 #ifdef MSORT_K3_CHECK
@@ -959,6 +968,7 @@ struct Kernels {
     f.bv[0] = bv[cur], f.bv[1] = bv[cur ^ 1];
     f.n = (int64_t)n, f.T = Lq, f.ntiles = (int64_t)((n + Tm - 1) / Tm), f.P = left;
     f.done = done;
+    f.gate = gate, f.gate_want = gate_want;
     int64_t pb = 0;
     for (int p = 0; p < left; ++p) {
       f.pair_base[p] = pb;
@@ -1656,9 +1666,125 @@ struct Kernels {
   }
 };
 
+// ---- key-range narrowing (8-byte keys) ----------------------------------
+// The paper's arrays are numpy integers (int64) drawn from
+// [0, n) with n <= 10^7, and C3's keys lie in [0, 1000): 8-byte
+// keys that span fewer than 2^32 values.  Such a sort runs on 32-bit keys:
+// key -> image(key) - min image, the 4-byte sort (half the key bytes of every
+// merge pass, the 4-byte tile shape), then back.  The map is monotone and
+// injective, so the output (keys, payload order: the stable order) is the
+// one the 8-byte sort gives.  The choice is made on the device: both the
+// narrowed and the 8-byte sort are enqueued, every kernel of each gated on
+// the measured range (k_key_range), so the call stays asynchronous and
+// graph-capturable; the path not taken launches kernels that return at once.
+template <class K>
+__global__ void __launch_bounds__(256) k_key_range(const K* __restrict__ k, int64_t n,
+                                                   unsigned long long* __restrict__ mm) {
+  unsigned long long lo = ~0ull, hi = 0;
+  const int64_t stride = (int64_t)gridDim.x * 256;
+  int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    unsigned long long u[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) u[j] = KeyTraits<K>::image(k[i + j * stride]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) lo = min(lo, u[j]), hi = max(hi, u[j]);
+  }
+  for (; i < n; i += stride) {
+    const unsigned long long u = KeyTraits<K>::image(k[i]);
+    lo = min(lo, u), hi = max(hi, u);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[0], lo);
+    atomicMax(&mm[1], hi);
+  }
+}
+template <class K>
+__global__ void __launch_bounds__(256) k_key_narrow(const K* __restrict__ k, int64_t n,
+                                                    const unsigned long long* __restrict__ mm,
+                                                    uint32_t* __restrict__ o) {
+  if (!range_narrow(mm)) return;
+  const unsigned long long lo = mm[0];
+  const int64_t stride = (int64_t)gridDim.x * 256;
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += stride)
+    o[i] = (uint32_t)(KeyTraits<K>::image(k[i]) - lo);
+}
+template <class K>
+__global__ void __launch_bounds__(256) k_key_widen(const uint32_t* __restrict__ u, int64_t n,
+                                                   const unsigned long long* __restrict__ mm,
+                                                   K* __restrict__ k) {
+  if (!range_narrow(mm)) return;
+  const unsigned long long lo = mm[0];
+  const int64_t stride = (int64_t)gridDim.x * 256;
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += stride)
+    k[i] = key_from_image<K>(lo + u[i]);
+}
+
+// MSORT_NARROW=0 (environment) disables the narrowing (A/B, tests)
+static bool narrow_enabled() {
+  const char* e = getenv("MSORT_NARROW");
+  return !(e && *e == '0');
+}
+
+// Workspace (single_ws_bytes for 8-byte keys): [ 32-bit keys | the 4-byte
+// sort's workspace ] overlapping the 8-byte sort's, the range in the last
+// 256 bytes.  Only one of the two sorts does work; the other's launches
+// (and its counter memsets, enqueued before or after the whole working
+// path) touch nothing the working path still needs.
+template <class K, bool PAIRS>
+static msort_status sort_narrowed(const K* ik, const uint32_t* iv, K* keys, uint32_t* vals,
+                                  size_t n, void* ws, cudaStream_t s) {
+  const msort_dtype kd = K(-1) < K(0) ? MSORT_INT64 : MSORT_UINT64;
+  const msort_dtype vd = PAIRS ? MSORT_UINT32 : MSORT_NONE;
+  const size_t need = single_ws_bytes(n, kd, vd);
+  char* w = static_cast<char*>(ws);
+  auto* mm = reinterpret_cast<unsigned long long*>(w + need - 256);
+  uint32_t* nk = reinterpret_cast<uint32_t*>(w);
+  void* ws32 = w + align_up(n * 4, 256);
+  const size_t ws32_bytes = single_ws_bytes(n, MSORT_UINT32, vd);
+  int dev = 0, sms = 0;
+  MSORT_CUDA_TRY(cudaGetDevice(&dev));
+  MSORT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned grid = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)sms * 8, ((int64_t)n + 255) / 256));
+  MSORT_CUDA_TRY(cudaMemsetAsync(mm, 0xff, 8, s));
+  MSORT_CUDA_TRY(cudaMemsetAsync(mm + 1, 0, 8, s));
+  {
+    LaunchScope ls(KC_KEY_RANGE, s);
+    k_key_range<K><<<grid, 256, 0, s>>>(ik, (int64_t)n, mm);
+  }
+  {
+    LaunchScope ls(KC_KEY_RANGE, s);
+    k_key_narrow<K><<<grid, 256, 0, s>>>(ik, (int64_t)n, mm, nk);
+  }
+  MSORT_CUDA_TRY(cudaGetLastError());
+  MSORT_TRY((Kernels<uint32_t, PAIRS>::sort(nk, iv, nk, vals, n, ws32, ws32_bytes, s, mm, 1)));
+  {
+    LaunchScope ls(KC_KEY_RANGE, s);
+    k_key_widen<K><<<grid, 256, 0, s>>>(nk, (int64_t)n, mm, keys);
+  }
+  MSORT_CUDA_TRY(cudaGetLastError());
+  return Kernels<K, PAIRS>::sort(ik, iv, keys, vals, n, ws, need - 256, s, mm, 0);
+}
+
 template <class K>
 static msort_status sort_k(const void* ik, const void* iv, void* keys, void* vals, size_t n,
                            void* ws, size_t ws_bytes, cudaStream_t s) {
+#ifndef MSORT_K3_PERPASS
+  if constexpr (sizeof(K) == 8) {
+    if (n > (size_t)kK0MaxN && narrow_enabled()) {
+      if (vals)
+        return sort_narrowed<K, true>((const K*)ik, (const uint32_t*)iv, (K*)keys,
+                                      (uint32_t*)vals, n, ws, s);
+      return sort_narrowed<K, false>((const K*)ik, nullptr, (K*)keys, nullptr, n, ws, s);
+    }
+  }
+#endif
   if (vals)
     return Kernels<K, true>::sort((const K*)ik, (const uint32_t*)iv, (K*)keys, (uint32_t*)vals,
                                   n, ws, ws_bytes, s);

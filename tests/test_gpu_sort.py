@@ -320,3 +320,54 @@ def test_k3_single_chunk_grabs(ms, orc, n, dist, dtype, pairs):
     k = _keys(n, 7100 + n % 97, dist, dtype)
     v = mi.index_payload(n) if pairs else None
     check_parity(ms, orc, k, v)
+
+
+# ---- key-range narrowing: 8-byte keys spanning < 2^32 values sort as 32-bit
+# offsets (Kernels::sort_narrowed); the choice is made on the device
+def _range_keys(n, seed, dtype, lo, span):
+    """n keys of `dtype` uniform in [lo, lo + span) (span <= 2^63), plus both ends."""
+    rng = np.random.default_rng(seed)
+    off = rng.integers(0, span, size=n, dtype=np.uint64)
+    if np.dtype(dtype) == np.int64:
+        k = (np.int64(lo) + off.astype(np.int64)).astype(np.int64)
+    else:
+        k = (np.uint64(lo) + off).astype(np.uint64)
+    if n >= 2:
+        k[n // 3] = np.asarray(lo).astype(dtype)
+        k[(2 * n) // 3] = (np.asarray(lo).astype(dtype) + np.asarray(span - 1).astype(dtype))
+    return k
+
+
+@pytest.mark.parametrize("dtype", [np.int64, np.uint64])
+@pytest.mark.parametrize("pairs", [False, True])
+def test_key_range_narrowing(ms, orc, dtype, pairs):
+    """Spans just below / at / above 2^32 (narrowed / narrowed / 8-byte path),
+    negative and extreme bases, ragged sizes above the K0 limit."""
+    big = (1 << 63) - (1 << 33) if dtype == np.int64 else (1 << 64) - (1 << 33)
+    cases = [(0, 1000), (-(1 << 40) if dtype == np.int64 else 1 << 40, (1 << 32) - 1),
+             (-(1 << 63) if dtype == np.int64 else 0, 1 << 32),
+             (big, (1 << 32) + 1), (5, 1 << 40), (7, 1)]
+    for i, (lo, span) in enumerate(cases):
+        for n in (65537, 3 * 8704 + 5, (1 << 20) + 333):
+            k = _range_keys(n, 40 + i, dtype, lo, span)
+            v = mi.index_payload(n) if pairs else None
+            check_parity(ms, orc, k, v)
+
+
+def test_key_range_narrowing_out_of_place_and_off(ms, orc, monkeypatch):
+    """Out of place with a workspace, C3-shaped keys; and the same with the
+    narrowing disabled (MSORT_NARROW=0): identical to the oracle both ways."""
+    n = (1 << 22) + 17
+    k = mi.keys(n, 2, ("mod", 1000)).astype(np.int64)
+    v = mi.index_payload(n)
+    ek, ev = orc.sort(k, v)
+    for mode in ("1", "0"):
+        monkeypatch.setenv("MSORT_NARROW", mode)
+        kin, vin = to_dev(k), to_dev(v)
+        kout, vout = torch.empty_like(kin), torch.empty_like(vin)
+        ws = ms.workspace(n, torch.int64, True, device="cuda")
+        ms.msort_sort_out(kin, kout, in_vals=vin, vals_out=vout, ws=ws)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(kout, np.int64), ek)
+        assert np.array_equal(to_host(vout, np.uint32), ev)
+        assert np.array_equal(to_host(kin, np.int64), k)  # input untouched
