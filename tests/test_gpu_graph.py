@@ -52,3 +52,41 @@ def test_graph_replay(ms, orc, pairs, n):
             assert np.array_equal(to_host(vout, np.int32).view(np.uint32), ev)
         else:
             assert np.array_equal(to_host(kout, np.int32), orc.sort(k))
+
+
+@pytest.mark.parametrize("pairs", [False, True])
+def test_graph_replay_int64_range_decided_on_device(ms, orc, pairs):
+    """One captured 8-byte-key sort serves both key-range paths: the choice
+    between the narrowed (32-bit offsets) and the 8-byte sort is taken on the
+    device at every replay, so replays alternate between narrow-range and
+    full-range inputs and each is bit-exact."""
+    n = (1 << 20) + 77
+    kin = torch.zeros(n, dtype=torch.int64, device="cuda")
+    kout = torch.empty_like(kin)
+    vin = torch.empty(n, dtype=torch.int32, device="cuda") if pairs else None
+    vout = torch.empty_like(vin) if pairs else None
+    ws = ms.workspace(n, torch.int64, pairs, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ms.msort_sort_out(kin, kout, in_vals=vin, vals_out=vout, ws=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ms.msort_sort_out(kin, kout, in_vals=vin, vals_out=vout, ws=ws)
+    v = mi.index_payload(n)
+    for i, span in enumerate([1000, 1 << 62, (1 << 32) - 1, 1 << 32]):
+        rng = np.random.default_rng(100 + i)
+        k = (rng.integers(0, span, n, dtype=np.int64) - (1 << 61)).astype(np.int64)
+        kin.copy_(to_dev(k))
+        if pairs:
+            vin.copy_(to_dev(v).view(torch.int32))
+        g.replay()
+        torch.cuda.synchronize()
+        if pairs:
+            ek, ev = orc.sort(k, v)
+            assert np.array_equal(to_host(kout, np.int64), ek)
+            assert np.array_equal(to_host(vout, np.uint32), ev)
+        else:
+            assert np.array_equal(to_host(kout, np.int64), orc.sort(k))

@@ -85,3 +85,29 @@ def test_sort_workspace_exact(ms, orc, mode, n):
         assert np.array_equal(to_host(kout, np.int32), orc.sort(k))
     finally:
         ms.set_quad_mode(0)
+
+
+@pytest.mark.parametrize("span", [1000, 1 << 40])  # key-range narrowed / the 8-byte path
+@pytest.mark.parametrize("pairs", [False, True])
+@pytest.mark.parametrize("n", [65537, (1 << 21) + 3])
+def test_sort_workspace_exact_int64(ms, orc, span, pairs, n):
+    """8-byte keys with exactly the reported workspace: both enqueued paths
+    (one gated off on the device) and the range slot stay inside it."""
+    rng = np.random.default_rng(n + span)
+    k = (rng.integers(0, span, n, dtype=np.int64) - span // 2).astype(np.int64)
+    v = mi.index_payload(n) if pairs else None
+    kin = to_dev(k)
+    kout = torch.empty_like(kin)
+    vin = to_dev(v) if pairs else None
+    vout = torch.empty_like(vin) if pairs else None
+    nb = ms.msort_workspace_bytes(n, ms.MSORT_INT64, ms.MSORT_UINT32 if pairs else ms.MSORT_NONE)
+    buf, ws = _ws(nb)
+    ms.msort_sort_out(kin, kout, in_vals=vin, vals_out=vout, ws=ws)
+    torch.cuda.synchronize()
+    assert _canary_ok(buf, nb), "8-byte sort wrote past its workspace"
+    if pairs:
+        ek, ev = orc.sort(k, v)
+        assert np.array_equal(to_host(kout, np.int64), ek)
+        assert np.array_equal(to_host(vout, np.uint32), ev)
+    else:
+        assert np.array_equal(to_host(kout, np.int64), orc.sort(k))
