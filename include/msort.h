@@ -91,7 +91,12 @@ msort_status msort_sort_pairs(void *keys, void *vals, size_t n, msort_dtype key_
 /* Bytes of device workspace the *_ws calls need: for world <= 1 about
  * n*(wk+wv) (the O(n) extra space of merge sort) plus n/256*8 bytes of
  * merge-path partitions; for world > 1 (n = local count) also an n*(wk+wv)
- * receive buffer and O(world*256) splitter buffers.  bytes: host out. */
+ * receive buffer and O(world*256) splitter buffers.  For 8-byte keys the
+ * single-GPU size also covers the key-range narrowed path (n > 2^16: keys
+ * whose values span fewer than 2^32 are sorted as 32-bit offsets from their
+ * minimum -- same output, half the key bytes per merge pass; chosen on the
+ * device, so the call stays asynchronous) and 256 bytes for
+ * the measured range.  bytes: host out. */
 msort_status msort_workspace_bytes(size_t n, msort_dtype key_dtype, msort_dtype val_dtype,
                                    int world, size_t *bytes);
 
