@@ -55,12 +55,20 @@ __device__ __forceinline__ void merge_pairs_nocheck(const K* s, const int* src_i
   }
 }
 
+// A K1 input key: KW == K, or (the key-range narrowed sort, sort_narrowed)
+// an 8-byte key narrowed on the fly to its offset from the range minimum mm[0].
+template <class K, class KW>
+__device__ __forceinline__ K k1_in(const KW* p, const unsigned long long* mm) {
+  if constexpr (std::is_same<K, KW>::value) return *p;
+  else return (K)(KeyTraits<KW>::image(*p) - mm[0]);
+}
+
 // ----------------------------------------------------------------- K1
 // NT threads x VT items (VT odd: "blocked" shared accesses at stride VT are
-// bank-conflict free without padding).
-template <class K, bool PAIRS, int NT, int VT>
+// bank-conflict free without padding).  KW: the input key type (see k1_in).
+template <class K, bool PAIRS, int NT, int VT, class KW = K>
 __global__ void __launch_bounds__(NT)
-    k1_tile_sort(const K* __restrict__ in_k, const uint32_t* __restrict__ in_v,
+    k1_tile_sort(const KW* __restrict__ in_k, const uint32_t* __restrict__ in_v,
                  K* __restrict__ out_k, uint32_t* __restrict__ out_v, int64_t n,
                  const int64_t* __restrict__ seg, const unsigned long long* __restrict__ gate = nullptr,
                  int gate_want = 0) {
@@ -84,7 +92,7 @@ __global__ void __launch_bounds__(NT)
     // real elements, so the stable order keeps real keys first.
 #pragma unroll 4
     for (int i = tid; i < T; i += NT) {
-      sk[i] = i < cnt ? in_k[base + i] : KeyTraits<K>::max_key();
+      sk[i] = i < cnt ? k1_in<K>(in_k + base + i, gate) : KeyTraits<K>::max_key();
       if (i < cnt) sv[i] = in_v[base + i];
     }
     __syncthreads();
@@ -100,7 +108,7 @@ __global__ void __launch_bounds__(NT)
 #pragma unroll
     for (int k = 0; k < VT; ++k) {
       const int i = k * NT + tid;
-      key[k] = i < cnt ? in_k[base + i] : KeyTraits<K>::max_key();
+      key[k] = i < cnt ? k1_in<K>(in_k + base + i, gate) : KeyTraits<K>::max_key();
     }
   }
   // Per-thread register network.
@@ -326,9 +334,9 @@ struct K1KeysShape {
 // network (warp_bitonic_keys, no shared memory) instead of the per-thread
 // network + the five in-warp merge rounds; the block rounds then start from
 // runs of 32 VT.
-template <class K, int NT, int VT, bool SHFL = false>
+template <class K, int NT, int VT, bool SHFL = false, class KW = K>
 __global__ void __launch_bounds__(NT)
-    k1_tile_sort_keys(const K* __restrict__ in_k, K* __restrict__ out_k, int64_t n,
+    k1_tile_sort_keys(const KW* __restrict__ in_k, K* __restrict__ out_k, int64_t n,
                       const int64_t* __restrict__ seg,
                       const unsigned long long* __restrict__ gate = nullptr, int gate_want = 0) {
   if (gate && (int)range_narrow(gate) != gate_want) return;  // key-range gate (sort_narrowed)
@@ -352,7 +360,7 @@ __global__ void __launch_bounds__(NT)
 #pragma unroll
   for (int k = 0; k < VT; ++k) {
     const int i = k * NT + tid;
-    key[k] = i < cnt ? in_k[base + i] : KeyTraits<K>::max_key();
+    key[k] = i < cnt ? k1_in<K>(in_k + base + i, gate) : KeyTraits<K>::max_key();
   }
   int r0 = 0;
   if constexpr (SHFL) {
@@ -808,14 +816,49 @@ struct Kernels {
     return MSORT_SUCCESS;
   }
 
+  // K1 of the narrowed sort: reads the caller's 8-byte keys (KW) and narrows
+  // them on the fly (k1_in); its attribute is set on first use per device.
+  template <class KW>
+  static msort_status k1_wide(const KW* in, const uint32_t* in_v, K* ok, uint32_t* ov, size_t n,
+                              int64_t ntiles, const unsigned long long* gate, int want,
+                              cudaStream_t s) {
+    int dev = 0;
+    MSORT_CUDA_TRY(cudaGetDevice(&dev));
+    static std::atomic<bool> ready[64];
+    if (!ready[dev & 63].load(std::memory_order_acquire)) {
+      if constexpr (PAIRS)
+        MSORT_CUDA_TRY(cudaFuncSetAttribute(k1_tile_sort<K, PAIRS, NT1, VT, KW>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)k1_smem));
+      else
+        MSORT_CUDA_TRY(cudaFuncSetAttribute(k1_tile_sort_keys<K, NT1, VT, false, KW>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)k1_smem));
+      ready[dev & 63].store(true, std::memory_order_release);
+    }
+    LaunchScope ls(KC_TILE_SORT, s);
+    if constexpr (PAIRS)
+      k1_tile_sort<K, PAIRS, NT1, VT, KW>
+          <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in, in_v, ok, ov, (int64_t)n, nullptr, gate,
+                                                   want);
+    else
+      k1_tile_sort_keys<K, NT1, VT, false, KW>
+          <<<(unsigned)ntiles, NT1, k1_smem, s>>>(in, ok, (int64_t)n, nullptr, gate, want);
+    return MSORT_SUCCESS;
+  }
+
   // Sort in_k/in_v into out_k/out_v (in == out: in place; K1 reads a whole
   // tile into shared memory before writing it back, so that is safe).
   // gate / gate_want: the key-range gate of sort_narrowed (every launch of
   // this sort does nothing unless range_narrow(gate) == gate_want); the
   // caller guarantees n > kK0MaxN, so no K0, and K6 is not used.
+  // wide / wide_kind (4-byte keys of the narrowed sort only): K1 reads the
+  // caller's 8-byte keys (1 int64, 2 uint64) and narrows them on the fly
+  // (k1_in, gate = the range); in_k is then unused.
   static msort_status sort(const K* in_k, const uint32_t* in_v, K* keys, uint32_t* vals,
                            size_t n, void* ws, size_t ws_bytes, cudaStream_t s,
-                           const unsigned long long* gate = nullptr, int gate_want = 0) {
+                           const unsigned long long* gate = nullptr, int gate_want = 0,
+                           const void* wide = nullptr, int wide_kind = 0) {
     MSORT_TRY(init());
     if (n < 2) {
       if (n == 1 && in_k != keys) {
@@ -867,7 +910,19 @@ struct Kernels {
     uint32_t* bv[2] = {vals, wv};
     // S4: pick K1's destination so the last pass lands in keys
     int cur = (nq + left) % 2;
-    {
+    bool k1_done = false;
+    if constexpr (std::is_same<K, uint32_t>::value) {
+      if (wide_kind != 0) {
+        if (wide_kind == 1)
+          MSORT_TRY(k1_wide<int64_t>(static_cast<const int64_t*>(wide), in_v, bk[cur], bv[cur], n,
+                                     ntiles, gate, gate_want, s));
+        else
+          MSORT_TRY(k1_wide<uint64_t>(static_cast<const uint64_t*>(wide), in_v, bk[cur], bv[cur],
+                                      n, ntiles, gate, gate_want, s));
+        k1_done = true;
+      }
+    }
+    if (!k1_done) {
       LaunchScope ls(KC_TILE_SORT, s);
       if constexpr (PAIRS)
         k1_tile_sort<K, PAIRS, NT1, VT>
@@ -1677,6 +1732,7 @@ struct Kernels {
 // narrowed and the 8-byte sort are enqueued, every kernel of each gated on
 // the measured range (k_key_range), so the call stays asynchronous and
 // graph-capturable; the path not taken launches kernels that return at once.
+// The narrowing itself happens as the 4-byte sort's K1 loads the keys (k1_in).
 template <class K>
 __global__ void __launch_bounds__(256) k_key_range(const K* __restrict__ k, int64_t n,
                                                    unsigned long long* __restrict__ mm) {
@@ -1703,16 +1759,6 @@ __global__ void __launch_bounds__(256) k_key_range(const K* __restrict__ k, int6
     atomicMin(&mm[0], lo);
     atomicMax(&mm[1], hi);
   }
-}
-template <class K>
-__global__ void __launch_bounds__(256) k_key_narrow(const K* __restrict__ k, int64_t n,
-                                                    const unsigned long long* __restrict__ mm,
-                                                    uint32_t* __restrict__ o) {
-  if (!range_narrow(mm)) return;
-  const unsigned long long lo = mm[0];
-  const int64_t stride = (int64_t)gridDim.x * 256;
-  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += stride)
-    o[i] = (uint32_t)(KeyTraits<K>::image(k[i]) - lo);
 }
 template <class K>
 __global__ void __launch_bounds__(256) k_key_widen(const uint32_t* __restrict__ u, int64_t n,
@@ -1758,12 +1804,11 @@ static msort_status sort_narrowed(const K* ik, const uint32_t* iv, K* keys, uint
     LaunchScope ls(KC_KEY_RANGE, s);
     k_key_range<K><<<grid, 256, 0, s>>>(ik, (int64_t)n, mm);
   }
-  {
-    LaunchScope ls(KC_KEY_RANGE, s);
-    k_key_narrow<K><<<grid, 256, 0, s>>>(ik, (int64_t)n, mm, nk);
-  }
   MSORT_CUDA_TRY(cudaGetLastError());
-  MSORT_TRY((Kernels<uint32_t, PAIRS>::sort(nk, iv, nk, vals, n, ws32, ws32_bytes, s, mm, 1)));
+  // the 4-byte sort's K1 reads the 8-byte keys and narrows them as it loads
+  // them (k1_in): no separate narrow pass
+  MSORT_TRY((Kernels<uint32_t, PAIRS>::sort(nk, iv, nk, vals, n, ws32, ws32_bytes, s, mm, 1, ik,
+                                            K(-1) < K(0) ? 1 : 2)));
   {
     LaunchScope ls(KC_KEY_RANGE, s);
     k_key_widen<K><<<grid, 256, 0, s>>>(nk, (int64_t)n, mm, keys);
