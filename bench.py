@@ -555,6 +555,10 @@ def main():
         reference_arm(args, rank)
         return
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    if world > 1:
+        # a dead peer inside a host-synchronised collective becomes an error
+        # (communicator aborted) instead of a hang (include/msort.h)
+        os.environ.setdefault("MSORT_NCCL_TIMEOUT_S", "600")
 
     import numpy as np
     import torch
