@@ -771,7 +771,10 @@ def main():
     e2e = None
     if not args.no_e2e:
         h_in = kin.cpu().pin_memory()
-        ke = max(6, min(args.steps, 12))
+        # as many steps as the timed region (6..40): the pipeline's fill and
+        # drain (the first upload and the last copy-back overlap nothing) are
+        # then amortised the way a streaming caller sees them
+        ke = max(6, min(args.steps, 40))
         if not dpath:
             NS = max(1, args.e2e_streams)
             h_out = [torch.empty_like(h_in).pin_memory() for _ in range(NS)]
