@@ -17,13 +17,14 @@
 //      sample of merged rank t*g starts output tile t (K5's sample-bounded
 //      tiles, k5_kway.cuh: a tile never exceeds S(g + CL) - CL keys); CTA t
 //      finds its tile's exact start/end STATE per chunk by one DSMEM probe
-//      round (16 lanes x 2) inside the S keys between two samples, copies its
+//      round (16 lanes x S/16) inside the S keys between two samples, copies its
 //      CL windows in (16-byte DSMEM vectors) and merges them in log2(CL)
 //      in-CTA rounds (K5's engine, ping-pong buffers, one barrier per round),
 //      writing HBM from the last round.  Three cluster barriers in all, the
 //      last one split (arrive after the window copies, wait before exit).
 //      C1 (2^16 int32): 26.6 -> 22.0 us per CUDA-graph replay against the
-//      pairwise levels (profiles/r02/k0mw/).
+//      pairwise levels (profiles/r02/k0mw/); S = 64 (half the samples to
+//      copy and rank, 4 probes per lane): 22.0 -> 20.5 us.
 //      The round-2 variant (MW = false, MSORT_K0=3): log2(CL) pairwise merge
 //      levels across the cluster -- co-ranks by 32-ary DSMEM searches, the
 //      two windows copied in, a per-thread merge, one cluster barrier per level.
@@ -79,13 +80,13 @@ static_assert(kK0MaxN >= 65536, "K0 covers C1 (2^16 keys)");
 // (a multiple of the 16-byte vector width; the tile bound S(g+CL)-CL <=
 // Q + (S-1) CL keys must fit the round's threads: (bound)/VT2 + CL/2 <= NT).
 #ifndef MSORT_K0_S
-#define MSORT_K0_S 32
+#define MSORT_K0_S 64
 #endif
 #ifndef MSORT_K0_VT2
 #define MSORT_K0_VT2 12
 #endif
 constexpr int kK0S = MSORT_K0_S, kK0VT2 = MSORT_K0_VT2;
-static_assert(kK0S <= 32, "a tile state is finished by one 32-lane probe round");
+static_assert(kK0S % 16 == 0 && kK0S <= 64, "a tile state is finished by one probe round of 16 lanes");
 constexpr int kK0TileMax = kK0Chunk + (kK0S - 1) * kK0MaxCL;  // S (g + CL) - CL, g <= Q / S
 static_assert(kK0TileMax / kK0VT2 + kK0MaxCL / 2 + 1 <= kK0NT / 32 * 31,
               "MW tile fits one round of output threads (31 per warp)");
@@ -283,8 +284,11 @@ __device__ __forceinline__ void k0_multiway(const K* mine, int Q, int N, int CL,
       const int b = task / CL, j = task % CL;
       const K0Bound<K> x = s_bnd[b];
       const int lj = clen(j);
+      constexpr int PR = S / 16;  // probes per lane (16 lanes cover the S - 1 keys)
       int st = -1, lo = 0;
-      bool p1 = false, p2 = false;
+      bool pr[PR];
+#pragma unroll
+      for (int u = 0; u < PR; ++u) pr[u] = false;
       if (x.k < 0) {
         st = lj;
       } else if (j == x.k) {
@@ -296,19 +300,20 @@ __device__ __forceinline__ void k0_multiway(const K* mine, int Q, int N, int CL,
         } else {
           lo = (r - 1) * S + 1;
           const int hi = min(r * S, lj);
-          if (lo + sub < hi) {
-            const K y = chunk[j][lo + sub];
-            p1 = j < x.k ? !(x.v < y) : y < x.v;
-          }
-          if (lo + sub + 16 < hi) {
-            const K y = chunk[j][lo + sub + 16];
-            p2 = j < x.k ? !(x.v < y) : y < x.v;
+#pragma unroll
+          for (int u = 0; u < PR; ++u) {
+            if (lo + sub + 16 * u < hi) {
+              const K y = chunk[j][lo + sub + 16 * u];
+              pr[u] = j < x.k ? !(x.v < y) : y < x.v;
+            }
           }
         }
       }
       const unsigned hm = 0xffffu << (lane & 16);
-      const unsigned b1 = __ballot_sync(F, p1), b2 = __ballot_sync(F, p2);
-      if (st < 0) st = lo + __popc(b1 & hm) + __popc(b2 & hm);
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < PR; ++u) cnt += __popc(__ballot_sync(F, pr[u]) & hm);
+      if (st < 0) st = lo + cnt;
       if (sub == 0) s_state[b][j] = st;
     }
   }
